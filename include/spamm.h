@@ -1,0 +1,208 @@
+/*
+ * spamm.h -- C ABI of libspamm.so, the B200 (sm_100a) hot path of SpAMM / cuSpAMM.
+ *
+ * The method (arXiv 2103.13042, /root/reference/PAPER.md):
+ *   C ~= A*B where a tile pair (i,k,j) is multiplied only if
+ *   ||A[i,k]||_F * ||B[k,j]||_F >= tau                       (Alg. 1 l.7/10 PAPER.md:63,
+ *                                                              Alg. 2 l.5 PAPER.md:155)
+ *   with tiles of LoNum x LoNum elements, LoNum = 32          (Table 1 pins 32)
+ *   and the flat two-kernel semantics of Sec. 3.1:
+ *     stage 1  spamm_norms          tile Frobenius norms, Eq. 2
+ *     stage 2  spamm_build_skipmap  per-C-tile surviving k-lists
+ *     stage 3  spamm_multiply       C[i,j] = sum_{kept k} A[i,k]B[k,j], alpha=1, beta=0
+ *   Multi-GPU row partitioning of C (Sec. 3.4, Alg. 4): spamm_multiply_mgpu.
+ *
+ * Conventions (every entry point):
+ *   - Returns spamm_status. Nothing throws or aborts across the ABI. On error a
+ *     thread-local message is available from spamm_last_error().
+ *   - Matrix arguments are DEVICE pointers owned by the caller, row-major, with
+ *     explicit leading dimensions in ELEMENTS.  Requirements: pointer 16-byte
+ *     aligned and ld*sizeof(elem) a multiple of 16 (TMA), ld >= number of columns.
+ *     A host pointer returns SPAMM_E_INVALID (checked with cudaPointerGetAttributes).
+ *   - Element types: SPAMM_FP32 -> float A, B (CUDA-core FP32 multiply);
+ *     SPAMM_BF16 / SPAMM_FP16 -> 16-bit A, B (tcgen05 tensor cores, FP32 accumulate).
+ *     C is always float (ab_frag is FP32).
+ *   - Ragged sizes are allowed: the result equals zero padding to a multiple of
+ *     the tile, done by TMA out-of-bounds fill, never a physical pad.
+ *   - Everything is stream-ordered on the caller's stream (a cudaStream_t passed
+ *     as void*; NULL = legacy default stream).  Argument errors are reported
+ *     synchronously; asynchronous CUDA faults surface as SPAMM_E_CUDA on a later call.
+ *   - The plan OWNS its workspace (norm maps, skip map, schedules).  Pointers
+ *     returned by getters stay valid until the next mutating call on the plan or
+ *     spamm_plan_destroy().  A plan is not thread-safe; use one plan per stream.
+ *   - There is no CPU fallback and no alternative backend: an unsupported
+ *     combination returns SPAMM_E_UNSUPPORTED.
+ */
+#ifndef SPAMM_H_
+#define SPAMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPAMM_OK = 0,
+  SPAMM_E_INVALID = 1,      /* bad argument (size, pointer, alignment, NaN tau, ...) */
+  SPAMM_E_UNSUPPORTED = 2,  /* valid but not implemented (e.g. tile != 32)            */
+  SPAMM_E_CUDA = 3,         /* CUDA runtime / driver error                            */
+  SPAMM_E_NOMEM = 4,        /* device allocation failed                               */
+  SPAMM_E_NCCL = 5,         /* NCCL error in the multi-GPU path                       */
+  SPAMM_E_STATE = 6         /* call order violated (e.g. multiply before norms)       */
+} spamm_status;
+
+typedef enum {
+  SPAMM_FP32 = 0,  /* float inputs, CUDA-core FP32 FMA, two-level FP32 accumulation */
+  SPAMM_BF16 = 1,  /* bfloat16 inputs, tcgen05.mma kind::f16, FP32 accumulation in TMEM */
+  SPAMM_FP16 = 2   /* float16 inputs, same tensor-core path as BF16 */
+} spamm_precision;
+
+/* plan flags */
+#define SPAMM_FLAG_NONE           0u
+#define SPAMM_FLAG_TIMING         1u  /* record per-stage CUDA events (spamm_get_stats) */
+#define SPAMM_FLAG_SYNC_SKIPMAP   2u  /* size the skip map exactly with one stream sync
+                                         instead of reserving the worst case up front  */
+
+/* spamm_multiply flags */
+#define SPAMM_MUL_AUTO            1u  /* run spamm_norms + spamm_build_skipmap first (spamm_run) */
+
+/* spamm_multiply_mgpu flags (Sec. 3.4) */
+#define SPAMM_MGPU_INPUTS_REPLICATED 0u  /* every rank already holds full A and B           */
+#define SPAMM_MGPU_INPUTS_ON_ROOT    1u  /* rank 0 holds A and B; broadcast over NCCL first */
+#define SPAMM_MGPU_GATHER_C          2u  /* all-gather C rows so every rank holds full C     */
+
+typedef struct spamm_plan_s* spamm_plan_t;
+
+typedef struct {
+  int64_t M, N, K;            /* problem shape (C is M x N, inner dimension K)              */
+  int64_t BM, BK, BN;         /* tiles per dimension: ceil(M/tile), ceil(K/tile), ceil(N/tile) */
+  int32_t tile;               /* LoNum                                                      */
+  int32_t macro_i, macro_j;   /* C tiles per scheduling macro-tile (rows, cols)             */
+  int64_t kept;               /* kept (i,k,j) triples = sum V                */
+  int64_t macro_entries;      /* (k, mask) entries over all macro-tiles = MMA k-steps       */
+  double  valid_ratio;        /* kept / (BM*BK*BN)                          */
+  double  tau;
+  float   ms_norms, ms_skipmap, ms_multiply; /* last stage times if SPAMM_FLAG_TIMING, else -1 */
+  int32_t precision;          /* spamm_precision                                            */
+  int32_t row_begin, row_end; /* tile rows this plan multiplies (multi-GPU shard), [begin,end) */
+} spamm_stats;
+
+/* ---------------------------------------------------------------- plans --- */
+
+/* Square N x N problem ("square matrices N x N", alpha=1, beta=0).
+ * tile must be 32 (LoNum; other values -> SPAMM_E_UNSUPPORTED).
+ * tau >= 0 and finite (NaN / negative / inf -> SPAMM_E_INVALID).
+ * Allocates the plan's device workspace on the current device.
+ * Ownership: *p is owned by the caller and released with spamm_plan_destroy. */
+spamm_status spamm_plan(spamm_plan_t* p, int64_t N, int32_t tile, double tau, spamm_precision prec);
+
+/* Rectangular C(M x N) = A(M x K) * B(K x N), e.g. the im2col shapes of PAPER.md:338.
+ * flags: SPAMM_FLAG_*.  Same rules as spamm_plan. */
+spamm_status spamm_plan_ex(spamm_plan_t* p, int64_t M, int64_t N, int64_t K, int32_t tile, double tau,
+                           spamm_precision prec, uint32_t flags);
+
+/* Releases all device memory of the plan (synchronises the device). NULL is a no-op. */
+spamm_status spamm_plan_destroy(spamm_plan_t p);
+
+/* Change tau without recomputing norms; invalidates the skip map (the
+ * search re-evaluates the threshold on fixed norm maps). */
+spamm_status spamm_set_tau(spamm_plan_t p, double tau);
+
+/* -------------------------------------------------------------- stages --- */
+
+/* Stage 1 (Sec. 3.2, Eq. 2): tile Frobenius norms of A (M x K)
+ * and B (K x N) into plan-owned float64 maps nA[BM][BK] and nB^T[BN][BK]
+ * (nB stored transposed so both maps are contiguous along k).  Each norm is the
+ * float64 sum of squares of the tile in a fixed, tile-position-independent order,
+ * then sqrt.  A and B are read exactly once (HBM-bound). */
+spamm_status spamm_norms(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
+                         void* stream);
+
+/* Stage 2 (Alg. 2 lines 3-16; Sec. 3.5.1):
+ * keep(i,k,j) <=> !(nA[i][k] * nB[k][j] < tau) in float64 (NaN kept).  Emits
+ *   leaf CSR  : tile_ptr[BM*BN+1] (int64), k_idx[kept] (uint16, ascending per tile)
+ *   V[i][j]   : list lengths;  row_work[i] = sum_j V[i][j]
+ *   macro lists: per macro-tile of macro_i x macro_j C tiles, the union of kept k
+ *               in ascending order with a keep bit per C tile, and an LPT schedule.
+ * Requires spamm_norms on this plan (else SPAMM_E_STATE).  Stream-ordered; with
+ * SPAMM_FLAG_SYNC_SKIPMAP it synchronises the stream once to size the lists. */
+spamm_status spamm_build_skipmap(spamm_plan_t p, void* stream);
+
+/* Stage 3 (Sec. 3.3, Alg. 2/3): C[i,j] = sum over kept k, ascending,
+ * of A[i,k] * B[k,j] for every C tile (tiles with no kept k are written as 0).
+ * A, B must be the same arrays given to spamm_norms (not checked).  C (float, M x N,
+ * ldc) is overwritten (beta = 0).  flags: SPAMM_MUL_AUTO runs stages 1 and 2 first.
+ * Without AUTO, requires spamm_build_skipmap (else SPAMM_E_STATE). */
+spamm_status spamm_multiply(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
+                            float* C, int64_t ldc, uint32_t flags, void* stream);
+
+/* All three stages, stream-ordered, no host synchronisation (== multiply with AUTO). */
+spamm_status spamm_run(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
+                       float* C, int64_t ldc, void* stream);
+
+/* ------------------------------------------------------------ multi-GPU --- */
+
+/* NCCL bootstrap helpers: rank 0 calls spamm_nccl_unique_id, the 128-byte id is
+ * broadcast by the caller (e.g. torch.distributed), then every rank calls
+ * spamm_nccl_comm_init on its own device.  The comm is owned by the caller. */
+spamm_status spamm_nccl_unique_id(uint8_t out_id[128]);
+spamm_status spamm_nccl_comm_init(void** comm, int nranks, int rank, const uint8_t id[128]);
+spamm_status spamm_nccl_comm_destroy(void* comm);
+
+/* Pure host function: contiguous split of BM tile rows into nranks ranges balanced by
+ * row_work (prefix sums cut at multiples of total/nranks; Sec. 3.5.1 load balance,
+ * PAPER.md:230-234, applied to the row partition of Sec. 3.4).
+ * row_begin has nranks+1 entries, row_begin[0]=0, row_begin[nranks]=BM, non-decreasing. */
+spamm_status spamm_partition_rows(const int64_t* row_work, int64_t BM, int nranks, int64_t* row_begin);
+
+/* Row-partitioned SpAMM over nranks GPUs of one node (Sec. 3.4, Alg. 4):
+ *   1. (INPUTS_ON_ROOT) ncclBroadcast of A and B from rank 0 into the caller's buffers;
+ *   2. each rank norms its share of A's and B's tile rows; ncclAllGather of the maps;
+ *   3. each rank counts kept pairs for its provisional rows; ncclAllGather of row work;
+ *      spamm_partition_rows cuts C tile-rows by work (identical on every rank);
+ *   4. each rank emits the lists of its rows and multiplies them into C rows;
+ *   5. (GATHER_C) C rows are exchanged so every rank holds all of C.
+ * A, B, C are full-size device buffers on every rank (only this rank's rows of C are
+ * written unless GATHER_C).  comm: ncclComm_t from spamm_nccl_comm_init. */
+spamm_status spamm_multiply_mgpu(spamm_plan_t p, void* nccl_comm, int rank, int nranks,
+                                 const void* A, int64_t lda, const void* B, int64_t ldb,
+                                 float* C, int64_t ldc, uint32_t flags, void* stream);
+
+/* -------------------------------------------------------- introspection --- */
+
+/* Device pointers to the float64 norm maps: dA = nA[BM][BK], dBt = nB^T[BN][BK]. */
+spamm_status spamm_get_norms(spamm_plan_t p, const double** dA, const double** dBt,
+                             int64_t* BM, int64_t* BK, int64_t* BN);
+
+/* Device pointers to the leaf CSR skip map; *kept is read back (synchronises). */
+spamm_status spamm_get_skipmap(spamm_plan_t p, const int64_t** d_tile_ptr, const uint16_t** d_k_idx,
+                               int64_t* kept);
+
+/* Device pointers to V[BM*BN] (int64) and row_work[BM] (int64). */
+spamm_status spamm_get_counts(spamm_plan_t p, const int64_t** d_V, const int64_t** d_row_work);
+
+/* Device pointers to the macro lists: ptr[GM*GN+1] (int64), entries[n] as pairs
+ * (uint32 k, uint32 mask), bit (li*macro_j + lj) = keep of C tile (I*macro_i+li, J*macro_j+lj);
+ * order[GM*GN] (int32) = LPT schedule (descending entry count). */
+spamm_status spamm_get_macro(spamm_plan_t p, const int64_t** d_ptr, const uint32_t** d_entries,
+                             const int32_t** d_order, int64_t* GM, int64_t* GN);
+
+/* Tile-row range of the last multi-GPU partition (nranks+1 entries, host memory). */
+spamm_status spamm_get_partition(spamm_plan_t p, int64_t* row_begin, int nranks);
+
+/* Counters and last stage times (synchronises the plan's last stream). */
+spamm_status spamm_get_stats(spamm_plan_t p, spamm_stats* out);
+
+const char* spamm_status_string(spamm_status s);
+const char* spamm_last_error(void);
+
+/* Number of tcgen05 / SIMT / norm / skip-map kernel launches issued by this process
+ * (for the bench's gpu_launches accounting). */
+int64_t spamm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAMM_H_ */

@@ -1,0 +1,459 @@
+// api.cu -- the C ABI of libspamm.so (include/spamm.h): plan lifetime, argument
+// validation, stage orchestration, introspection and error reporting.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+
+namespace spamm {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+spamm_status fail(spamm_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+spamm_status cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return e == cudaErrorMemoryAllocation ? SPAMM_E_NOMEM : SPAMM_E_CUDA;
+}
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ----------------------------------------------------------------- TMA maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void* base,
+                            uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_inner,
+                            uint32_t box_outer, CUtensorMapSwizzle swz) {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return fail(SPAMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * esize};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPAMM_E_INVALID, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return SPAMM_OK;
+}
+
+// --------------------------------------------------------------- validation
+static size_t esize_of(spamm_precision p) { return p == SPAMM_FP32 ? 4 : 2; }
+
+static spamm_status check_matrix(const void* ptr, int64_t rows, int64_t cols, int64_t ld, size_t esize,
+                                 const char* name) {
+  if (ptr == nullptr) return fail(SPAMM_E_INVALID, std::string(name) + " is NULL");
+  if (ld < cols) return fail(SPAMM_E_INVALID, std::string(name) + ": leading dimension < columns");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15u) != 0)
+    return fail(SPAMM_E_INVALID, std::string(name) + " is not 16-byte aligned");
+  if ((static_cast<uint64_t>(ld) * esize) % 16 != 0)
+    return fail(SPAMM_E_INVALID, std::string(name) + ": ld*sizeof(elem) must be a multiple of 16");
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SPAMM_E_INVALID, std::string(name) + " is not a CUDA pointer");
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(SPAMM_E_INVALID, std::string(name) + " is not a device pointer");
+  (void)rows;
+  return SPAMM_OK;
+}
+
+static bool tau_ok(double tau) { return std::isfinite(tau) && tau >= 0.0; }
+
+static spamm_status alloc(void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SPAMM_E_NOMEM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+  }
+  return SPAMM_OK;
+}
+
+static void free_plan(Plan* p) {
+  if (!p) return;
+  void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_ptr, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent,
+                  p->order, p->order_tmp, p->keys_tmp, p->cub_tmp};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (p->h_totals) cudaFreeHost(p->h_totals);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  delete p;
+}
+
+// worst-case leaf list reservation budget (bytes); above it the skip map is sized exactly
+static constexpr size_t kWorstCaseBudget = size_t(8) << 30;
+
+static spamm_status ensure_leaf_capacity(Plan& p, int64_t need) {
+  if (need <= p.leaf_cap) return SPAMM_OK;
+  if (p.leaf_k) cudaFree(p.leaf_k);
+  p.leaf_k = nullptr;
+  p.leaf_cap = 0;
+  SPAMM_TRY(alloc(reinterpret_cast<void**>(&p.leaf_k), sizeof(uint16_t) * static_cast<size_t>(need)));
+  p.leaf_cap = need;
+  return SPAMM_OK;
+}
+
+}  // namespace spamm
+
+using namespace spamm;
+
+extern "C" {
+
+const char* spamm_status_string(spamm_status s) {
+  switch (s) {
+    case SPAMM_OK: return "SPAMM_OK";
+    case SPAMM_E_INVALID: return "SPAMM_E_INVALID";
+    case SPAMM_E_UNSUPPORTED: return "SPAMM_E_UNSUPPORTED";
+    case SPAMM_E_CUDA: return "SPAMM_E_CUDA";
+    case SPAMM_E_NOMEM: return "SPAMM_E_NOMEM";
+    case SPAMM_E_NCCL: return "SPAMM_E_NCCL";
+    case SPAMM_E_STATE: return "SPAMM_E_STATE";
+  }
+  return "SPAMM_E_UNKNOWN";
+}
+
+const char* spamm_last_error(void) { return g_last_error.c_str(); }
+
+int64_t spamm_launch_count(void) { return g_launches.load(); }
+
+spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, int32_t tile, double tau,
+                           spamm_precision prec, uint32_t flags) {
+  if (!out) return fail(SPAMM_E_INVALID, "plan out-pointer is NULL");
+  *out = nullptr;
+  if (M <= 0 || N <= 0 || K <= 0) return fail(SPAMM_E_INVALID, "M, N, K must be positive");
+  if (!tau_ok(tau)) return fail(SPAMM_E_INVALID, "tau must be finite and >= 0");
+  if (prec != SPAMM_FP32 && prec != SPAMM_BF16 && prec != SPAMM_FP16)
+    return fail(SPAMM_E_INVALID, "unknown precision");
+  if (tile != kTile) {
+    if (tile == 64 || tile == 128) return fail(SPAMM_E_UNSUPPORTED, "only tile (LoNum) = 32 is implemented");
+    return fail(SPAMM_E_INVALID, "tile must be 32, 64 or 128");
+  }
+  const int64_t BM = (M + kTile - 1) / kTile, BK = (K + kTile - 1) / kTile, BN = (N + kTile - 1) / kTile;
+  if (BK > 65535) return fail(SPAMM_E_UNSUPPORTED, "K/tile must be <= 65535 (uint16 k lists)");
+  if (M > (int64_t(1) << 31) || N > (int64_t(1) << 31) || K > (int64_t(1) << 31))
+    return fail(SPAMM_E_UNSUPPORTED, "dimensions must be < 2^31 (TMA coordinates)");
+  int dev = 0;
+  SPAMM_CUDA_TRY(cudaGetDevice(&dev));
+  Plan* p = new Plan();
+  p->M = M;
+  p->N = N;
+  p->K = K;
+  p->tau = tau;
+  p->prec = prec;
+  p->flags = flags;
+  p->BM = BM;
+  p->BK = BK;
+  p->BN = BN;
+  p->MI = kMacroI;
+  p->MJ = prec == SPAMM_FP32 ? kMacroJ_simt : kMacroJ_umma;
+  p->GM = (BM + p->MI - 1) / p->MI;
+  p->GN = (BN + p->MJ - 1) / p->MJ;
+  p->device = dev;
+  p->row_begin_macro = 0;
+  p->row_end_macro = p->GM;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nleaf = BM * BN, nmac = p->GM * p->GN;
+  spamm_status st = SPAMM_OK;
+#define ALLOC(field, type, count)                                                                   \
+  if (st == SPAMM_OK)                                                                               \
+    st = alloc(reinterpret_cast<void**>(&p->field), sizeof(type) * static_cast<size_t>(count));
+  ALLOC(nA, double, BM * BK);
+  ALLOC(nBt, double, BN * BK);
+  ALLOC(V, int64_t, nleaf + 1);
+  ALLOC(U, int64_t, nmac + 1);
+  ALLOC(leaf_ptr, int64_t, nleaf + 1);
+  ALLOC(macro_ptr, int64_t, nmac + 1);
+  ALLOC(row_work, int64_t, BM);
+  ALLOC(order, int32_t, nmac);
+  ALLOC(order_tmp, int32_t, nmac);
+  ALLOC(keys_tmp, int64_t, nmac);
+#undef ALLOC
+  if (st == SPAMM_OK) {
+    p->cub_tmp_bytes = skipmap_cub_bytes(nleaf, nmac);
+    st = alloc(&p->cub_tmp, p->cub_tmp_bytes);
+  }
+  // macro lists: worst case GM*GN*BK entries (8 B each) -- small relative to A and B
+  if (st == SPAMM_OK) {
+    p->macro_cap = nmac * BK;
+    st = alloc(reinterpret_cast<void**>(&p->macro_ent), sizeof(uint2) * static_cast<size_t>(p->macro_cap));
+  }
+  // leaf lists: reserve the worst case unless it exceeds the budget or SYNC_SKIPMAP is set
+  if (st == SPAMM_OK && !(flags & SPAMM_FLAG_SYNC_SKIPMAP)) {
+    const size_t worst = sizeof(uint16_t) * static_cast<size_t>(nleaf) * static_cast<size_t>(BK);
+    if (worst <= kWorstCaseBudget) st = ensure_leaf_capacity(*p, nleaf * BK);
+  }
+  if (st == SPAMM_OK && cudaMallocHost(reinterpret_cast<void**>(&p->h_totals), 2 * sizeof(int64_t)) != cudaSuccess)
+    st = fail(SPAMM_E_NOMEM, "cudaMallocHost failed");
+  if (st == SPAMM_OK) {
+    for (auto& e : p->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) st = fail(SPAMM_E_CUDA, "cudaEventCreate failed");
+  }
+  if (st != SPAMM_OK) {
+    free_plan(p);
+    return st;
+  }
+  *out = reinterpret_cast<spamm_plan_t>(p);
+  return SPAMM_OK;
+}
+
+spamm_status spamm_plan(spamm_plan_t* p, int64_t N, int32_t tile, double tau, spamm_precision prec) {
+  return spamm_plan_ex(p, N, N, N, tile, tau, prec, SPAMM_FLAG_NONE);
+}
+
+spamm_status spamm_plan_destroy(spamm_plan_t h) {
+  if (!h) return SPAMM_OK;
+  cudaDeviceSynchronize();
+  free_plan(reinterpret_cast<Plan*>(h));
+  return SPAMM_OK;
+}
+
+spamm_status spamm_set_tau(spamm_plan_t h, double tau) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  if (!tau_ok(tau)) return fail(SPAMM_E_INVALID, "tau must be finite and >= 0");
+  Plan* p = reinterpret_cast<Plan*>(h);
+  p->tau = tau;
+  p->skipmap_ready = false;
+  return SPAMM_OK;
+}
+
+}  // extern "C"
+
+namespace spamm {
+
+// stage 1 over tile rows [ar0, ar1) of A and tile columns [bj0, bj1) of B
+spamm_status do_norms_range(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t ar0,
+                            int64_t ar1, int64_t bj0, int64_t bj1, cudaStream_t s) {
+  SPAMM_TRY(check_matrix(A, p.M, p.K, lda, esize_of(p.prec), "A"));
+  SPAMM_TRY(check_matrix(B, p.K, p.N, ldb, esize_of(p.prec), "B"));
+  const bool timing = p.flags & SPAMM_FLAG_TIMING;
+  if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[0], s));
+  // A (M x K): tile row i, tile col k -> nA[i*BK + k]
+  SPAMM_TRY(launch_norms(p, A, p.M, p.K, lda, p.nA, p.BK, 1, ar0, ar1, s));
+  // B (K x N) column strip [bj0*T, bj1*T): tile row k, tile col j -> nBt[j*BK + k]
+  if (bj1 > bj0) {
+    const size_t es = esize_of(p.prec);
+    const void* Bs = static_cast<const char*>(B) + static_cast<size_t>(bj0) * kTile * es;
+    const int64_t cols = std::min<int64_t>(p.N, bj1 * kTile) - bj0 * kTile;
+    SPAMM_TRY(launch_norms(p, Bs, p.K, cols, ldb, p.nBt + bj0 * p.BK, 1, p.BK, 0, p.BK, s));
+  }
+  if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[1], s));
+  p.ev_norms = timing;
+  p.norms_ready = true;
+  p.skipmap_ready = false;
+  p.last_stream = s;
+  return SPAMM_OK;
+}
+
+spamm_status do_norms(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t s) {
+  return do_norms_range(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, s);
+}
+
+spamm_status do_skipmap(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
+  if (!p.norms_ready) return fail(SPAMM_E_STATE, "spamm_build_skipmap before spamm_norms");
+  const bool timing = p.flags & SPAMM_FLAG_TIMING;
+  if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
+  SPAMM_TRY(launch_skipmap_count(p, gi0, gi1, s));
+  if (p.leaf_cap < p.BM * p.BN * p.BK) {
+    // exact sizing: one stream synchronisation
+    SPAMM_CUDA_TRY(cudaMemcpyAsync(p.h_totals, p.leaf_ptr + p.BM * p.BN, sizeof(int64_t),
+                                   cudaMemcpyDeviceToHost, s));
+    SPAMM_CUDA_TRY(cudaStreamSynchronize(s));
+    SPAMM_TRY(ensure_leaf_capacity(p, std::max<int64_t>(p.h_totals[0], 1)));
+  }
+  SPAMM_TRY(launch_skipmap_emit(p, gi0, gi1, s));
+  if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[3], s));
+  p.ev_skip = timing;
+  p.row_begin_macro = gi0;
+  p.row_end_macro = gi1;
+  p.skipmap_ready = true;
+  p.last_stream = s;
+  return SPAMM_OK;
+}
+
+spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                         cudaStream_t s) {
+  if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "spamm_multiply before spamm_build_skipmap");
+  SPAMM_TRY(check_matrix(A, p.M, p.K, lda, esize_of(p.prec), "A"));
+  SPAMM_TRY(check_matrix(B, p.K, p.N, ldb, esize_of(p.prec), "B"));
+  SPAMM_TRY(check_matrix(C, p.M, p.N, ldc, 4, "C"));
+  const bool timing = p.flags & SPAMM_FLAG_TIMING;
+  if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[4], s));
+  if (p.prec == SPAMM_FP32) {
+    SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
+                                   s));
+  } else {
+    SPAMM_TRY(launch_multiply_umma(p, A, lda, B, ldb, C, ldc, s));
+  }
+  if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[5], s));
+  p.ev_mul = timing;
+  p.last_stream = s;
+  return SPAMM_OK;
+}
+
+}  // namespace spamm
+
+extern "C" {
+
+spamm_status spamm_norms(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, void* stream) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  return do_norms(p, A, lda, B, ldb, static_cast<cudaStream_t>(stream));
+}
+
+spamm_status spamm_build_skipmap(spamm_plan_t h, void* stream) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  return do_skipmap(p, 0, p.GM, static_cast<cudaStream_t>(stream));
+}
+
+spamm_status spamm_multiply(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
+                            int64_t ldc, uint32_t flags, void* stream) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags & SPAMM_MUL_AUTO) {
+    SPAMM_TRY(do_norms(p, A, lda, B, ldb, s));
+    SPAMM_TRY(do_skipmap(p, 0, p.GM, s));
+  }
+  return do_multiply(p, A, lda, B, ldb, C, ldc, s);
+}
+
+spamm_status spamm_run(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
+                       int64_t ldc, void* stream) {
+  return spamm_multiply(h, A, lda, B, ldb, C, ldc, SPAMM_MUL_AUTO, stream);
+}
+
+spamm_status spamm_get_norms(spamm_plan_t h, const double** dA, const double** dBt, int64_t* BM, int64_t* BK,
+                             int64_t* BN) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  if (dA) *dA = p.nA;
+  if (dBt) *dBt = p.nBt;
+  if (BM) *BM = p.BM;
+  if (BK) *BK = p.BK;
+  if (BN) *BN = p.BN;
+  return p.norms_ready ? SPAMM_OK : fail(SPAMM_E_STATE, "norms not computed");
+}
+
+spamm_status spamm_get_skipmap(spamm_plan_t h, const int64_t** d_tile_ptr, const uint16_t** d_k_idx,
+                               int64_t* kept) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
+  if (d_tile_ptr) *d_tile_ptr = p.leaf_ptr;
+  if (d_k_idx) *d_k_idx = p.leaf_k;
+  if (kept) {
+    SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
+    SPAMM_CUDA_TRY(cudaMemcpy(kept, p.leaf_ptr + p.BM * p.BN, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
+  return SPAMM_OK;
+}
+
+spamm_status spamm_get_counts(spamm_plan_t h, const int64_t** d_V, const int64_t** d_row_work) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
+  if (d_V) *d_V = p.V;
+  if (d_row_work) *d_row_work = p.row_work;
+  return SPAMM_OK;
+}
+
+spamm_status spamm_get_macro(spamm_plan_t h, const int64_t** d_ptr, const uint32_t** d_entries,
+                             const int32_t** d_order, int64_t* GM, int64_t* GN) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
+  if (d_ptr) *d_ptr = p.macro_ptr;
+  if (d_entries) *d_entries = reinterpret_cast<const uint32_t*>(p.macro_ent);
+  if (d_order) *d_order = p.order;
+  if (GM) *GM = p.GM;
+  if (GN) *GN = p.GN;
+  return SPAMM_OK;
+}
+
+spamm_status spamm_get_partition(spamm_plan_t h, int64_t* row_begin, int nranks) {
+  if (!h || !row_begin) return fail(SPAMM_E_INVALID, "NULL argument");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  if (static_cast<int>(p.last_partition.size()) != nranks + 1)
+    return fail(SPAMM_E_STATE, "no partition for this rank count");
+  std::memcpy(row_begin, p.last_partition.data(), sizeof(int64_t) * (nranks + 1));
+  return SPAMM_OK;
+}
+
+spamm_status spamm_get_stats(spamm_plan_t h, spamm_stats* out) {
+  if (!h || !out) return fail(SPAMM_E_INVALID, "NULL argument");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  std::memset(out, 0, sizeof(*out));
+  out->M = p.M;
+  out->N = p.N;
+  out->K = p.K;
+  out->BM = p.BM;
+  out->BK = p.BK;
+  out->BN = p.BN;
+  out->tile = p.tile;
+  out->macro_i = p.MI;
+  out->macro_j = p.MJ;
+  out->tau = p.tau;
+  out->precision = p.prec;
+  out->row_begin = static_cast<int32_t>(p.row_begin_macro * p.MI);
+  out->row_end = static_cast<int32_t>(std::min<int64_t>(p.row_end_macro * p.MI, p.BM));
+  out->ms_norms = out->ms_skipmap = out->ms_multiply = -1.f;
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
+  if (p.skipmap_ready) {
+    int64_t tot[2];
+    SPAMM_CUDA_TRY(cudaMemcpy(&tot[0], p.leaf_ptr + p.BM * p.BN, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    SPAMM_CUDA_TRY(cudaMemcpy(&tot[1], p.macro_ptr + p.GM * p.GN, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    out->kept = tot[0];
+    out->macro_entries = tot[1];
+    out->valid_ratio = static_cast<double>(tot[0]) / (static_cast<double>(p.BM) * p.BK * p.BN);
+  }
+  if (p.ev_norms) cudaEventElapsedTime(&out->ms_norms, p.ev[0], p.ev[1]);
+  if (p.ev_skip) cudaEventElapsedTime(&out->ms_skipmap, p.ev[2], p.ev[3]);
+  if (p.ev_mul) cudaEventElapsedTime(&out->ms_multiply, p.ev[4], p.ev[5]);
+  return SPAMM_OK;
+}
+
+spamm_status spamm_partition_rows(const int64_t* row_work, int64_t BM, int nranks, int64_t* row_begin) {
+  if (!row_work || !row_begin) return fail(SPAMM_E_INVALID, "NULL argument");
+  if (BM <= 0 || nranks <= 0) return fail(SPAMM_E_INVALID, "BM and nranks must be positive");
+  // prefix sums; cut r is the first row whose exclusive prefix reaches r*total/nranks
+  long double total = 0;
+  for (int64_t i = 0; i < BM; ++i) {
+    if (row_work[i] < 0) return fail(SPAMM_E_INVALID, "negative row work");
+    total += static_cast<long double>(row_work[i]);
+  }
+  row_begin[0] = 0;
+  long double pre = 0;
+  int64_t i = 0;
+  for (int r = 1; r < nranks; ++r) {
+    const long double target = total * r / nranks;
+    while (i < BM && pre + static_cast<long double>(row_work[i]) / 2 < target) {
+      pre += static_cast<long double>(row_work[i]);
+      ++i;
+    }
+    row_begin[r] = std::max<int64_t>(i, row_begin[r - 1]);
+  }
+  row_begin[nranks] = BM;
+  return SPAMM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+"""GPU parity: the CUDA path through the C ABI vs the float64 oracle, same seeded inputs.
+
+Bars (BASELINE.json north_star): skip map bit-exact except triples whose norm product
+lies within 1e-6 relative of tau (counted, reported); C within 1e-5 relative
+Frobenius error for the FP32 path and 2e-2 for BF16/FP16.  Norm maps are float64 on
+both sides and agree to ~1e-15 relative (different summation order); we require 1e-12.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+T = 32
+BAND = 1e-6
+
+
+@pytest.fixture(scope="module")
+def sp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2103_13042_b200 import build
+    build.build()
+    from paper_2103_13042_b200 import spamm
+    return spamm
+
+
+def _dev(x: np.ndarray, prec: str, ld_mult: int = 8):
+    """Device copy of float32 host array x in the path's dtype, with a padded ld."""
+    m, n = x.shape
+    ld = -(-n // ld_mult) * ld_mult
+    dt = {"fp32": torch.float32, "bf16": torch.bfloat16, "fp16": torch.float16}[prec]
+    buf = torch.zeros((m, ld), dtype=dt, device="cuda")
+    buf[:, :n] = torch.from_numpy(np.ascontiguousarray(x)).to(dt)
+    return buf[:, :n]
+
+
+def _rounded(x: np.ndarray, prec: str) -> np.ndarray:
+    if prec == "bf16":
+        return synth.round_to_bf16(x)
+    if prec == "fp16":
+        return synth.round_to_fp16(x)
+    return x
+
+
+def _rel_fro(C, ref):
+    ref = np.asarray(ref, dtype=np.float64)
+    d = np.asarray(C, dtype=np.float64) - ref
+    nr = math.sqrt(float(np.sum(ref * ref)))
+    return math.sqrt(float(np.sum(d * d))) / (nr if nr > 0 else 1.0)
+
+
+def _run(sp, A32, B32, tau, prec, flags=0):
+    M, K = A32.shape
+    N = B32.shape[1]
+    plan = sp.Plan(M, N, K, tau, prec, flags=flags)
+    A, B = _dev(A32, prec), _dev(B32, prec)
+    Cbuf = torch.full((M, -(-N // 4) * 4), float("nan"), dtype=torch.float32, device="cuda")
+    C = Cbuf[:, :N]
+    plan.norms(A, B)
+    plan.build_skipmap()
+    plan.multiply(A, B, C)
+    torch.cuda.synchronize()
+    return plan, C.cpu().numpy()
+
+
+def _gpu_keep(sp, plan, BM, BK, BN):
+    ptr, kidx = sp.spamm_get_skipmap(plan.handle)
+    ptr, kidx = ptr.cpu().numpy(), kidx.cpu().numpy()
+    keep = np.zeros((BM, BK, BN), dtype=bool)
+    for t in range(BM * BN):
+        ks = kidx[ptr[t]:ptr[t + 1]]
+        assert np.all(np.diff(ks) > 0), "k lists must be strictly ascending"
+        keep[t // BN, ks, t % BN] = True
+    return keep
+
+
+def _check_skipmap(sp, plan, nA, nB, tau):
+    BM, BK = nA.shape
+    BN = nB.shape[1]
+    keep_o = oracle.keep_mask(nA, nB, tau)
+    keep_g = _gpu_keep(sp, plan, BM, BK, BN)
+    p = nA[:, :, None] * nB[None, :, :]
+    band = np.abs(p - tau) <= BAND * tau
+    diff = keep_o != keep_g
+    assert not np.any(diff & ~band), f"{int(np.sum(diff & ~band))} skip decisions differ outside the tie band"
+    V, rw = sp.spamm_get_counts(plan.handle)
+    V, rw = V.cpu().numpy(), rw.cpu().numpy()
+    np.testing.assert_array_equal(V, keep_g.sum(axis=1))
+    np.testing.assert_array_equal(rw, keep_g.sum(axis=(1, 2)))
+    return int(np.sum(diff)), int(np.sum(band))
+
+
+SHAPES = [(256, 256, 256), (100, 70, 45), (300, 257, 129), (129, 520, 384), (1, 1, 1), (33, 1000, 64)]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp16"])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_norms_match_oracle(sp, prec, shape):
+    M, N, K = shape
+    A = _rounded(synth.perturbed_decay_matrix(K, 0.97, seed=1, m=M), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.97, seed=2, m=K), prec)
+    plan = sp.Plan(M, N, K, 0.0, prec)
+    plan.norms(_dev(A, prec), _dev(B, prec))
+    nA_g, nBt_g = sp.spamm_get_norms(plan.handle)
+    np.testing.assert_allclose(nA_g.cpu().numpy(), oracle.tile_norms(A, T), rtol=1e-12, atol=0)
+    np.testing.assert_allclose(nBt_g.cpu().numpy().T, oracle.tile_norms(B, T), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_norms_toeplitz_bit_identical(sp, prec):
+    """Equal tiles (same block diagonal of a Toeplitz matrix) get bit-identical norms."""
+    N = 1024
+    A = _rounded(synth.decay_matrix(N, "exp", 0.99), prec)
+    plan = sp.Plan(N, N, N, 0.0, prec)
+    Ad = _dev(A, prec)
+    plan.norms(Ad, Ad)
+    nA = sp.spamm_get_norms(plan.handle)[0].cpu().numpy()
+    BD = N // T
+    for d in range(-BD + 1, BD):
+        diag = np.diagonal(nA, offset=d)
+        assert np.all(diag == diag[0]), d
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp16"])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("q", [0.0, 0.3, 0.7, 1.01])
+def test_spamm_parity_ragged(sp, prec, shape, q):
+    """Skip map bit-exact + C vs float64 oracle, ragged shapes, tau at product quantiles."""
+    M, N, K = shape
+    A = _rounded(synth.perturbed_decay_matrix(K, 0.95, seed=11, m=M), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=12, m=K), prec)
+    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+    prods = np.sort((nA[:, :, None] * nB[None, :, :]).ravel())
+    tau = 0.0 if q == 0.0 else (float(prods[-1]) * 2 if q > 1 else float(prods[int(q * (len(prods) - 1))]) * (1 + 1e-9))
+    plan, C = _run(sp, A, B, tau, prec)
+    _check_skipmap(sp, plan, nA, nB, tau)
+    ref = oracle.spamm(A, B, tau, T, nA, nB)
+    assert C.shape == ref.shape
+    if q > 1:
+        assert np.all(C == 0.0)
+        return
+    err = _rel_fro(C, ref)
+    bar = 1e-5 if prec == "fp32" else 2e-2
+    assert err <= bar, err
+    # tighter regression guard: FP32 accumulation of exactly-representable products
+    assert err <= (2e-6 if prec == "fp32" else 1e-5), err
+
+
+def test_macro_lists_match_oracle(sp):
+    M = N = K = 520
+    for prec, MJ in (("fp32", 4), ("bf16", 8)):
+        A = _rounded(synth.perturbed_decay_matrix(K, 0.95, seed=21, m=M), prec)
+        B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=22, m=K), prec)
+        nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+        tau = float(np.median(nA[:, :, None] * nB[None, :, :]))
+        plan, _ = _run(sp, A, B, tau, prec)
+        ptr, ent, order, GM, GN = sp.spamm_get_macro(plan.handle)
+        ref = oracle.macro_lists(nA, nB, tau, 4, MJ)
+        np.testing.assert_array_equal(ptr.cpu().numpy(), ref["ptr"])
+        np.testing.assert_array_equal(ent.cpu().numpy(), ref["entries"])
+        o = order.cpu().numpy()
+        assert sorted(o.tolist()) == list(range(GM * GN))
+        lens = np.diff(ref["ptr"])[o]
+        assert np.all(np.diff(lens) <= 0), "LPT order must be descending in work"
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_tau_zero_is_dense(sp, prec):
+    N = 384
+    A = _rounded(synth.random_matrix(N, N, seed=5), prec)
+    B = _rounded(synth.random_matrix(N, N, seed=6), prec)
+    plan, C = _run(sp, A, B, 0.0, prec)
+    st = plan.stats()
+    assert st["kept"] == (N // T) ** 3 and st["valid_ratio"] == 1.0
+    err = _rel_fro(C, oracle.dense_product(A, B))
+    assert err <= (1e-6 if prec == "fp32" else 1e-5), err
+
+
+def test_nan_propagates_like_gemm(sp):
+    N = 128
+    A = synth.random_matrix(N, N, seed=7)
+    A[5, 40] = np.nan
+    B = synth.random_matrix(N, N, seed=8)
+    plan, C = _run(sp, A, B, 1e30, "fp32")
+    # only pairs (i=0, k=1, j) have a NaN norm product -> kept; all others skipped
+    assert np.all(np.isnan(C[5, :]))
+    assert np.all(C[32:, :] == 0.0)
+    st = plan.stats()
+    assert st["kept"] == N // T
+
+
+def test_table1_counts_n2048(sp):
+    """The paper's dataset at Table 1's tau, N=2048:
+    GPU kept counts = oracle counts (no triple lies in the 1e-6 band there)."""
+    N = 2048
+    A = synth.decay_matrix(N, "alg", 0.1, c=0.1)
+    nA = oracle.tile_norms(A, T)
+    taus = [1.310666, 1.330525, 1.360312, 1.40003, 1.449676, 1.548969]
+    plan = sp.Plan(N, N, N, taus[0], "fp32")
+    Ad = _dev(A, "fp32")
+    plan.norms(Ad, Ad)
+    for tau in taus:
+        plan.set_tau(tau)
+        plan.build_skipmap()
+        diff, band = _check_skipmap(sp, plan, nA, nA, tau)
+        assert diff == 0 and band == 0
+        assert plan.stats()["kept"] == oracle.count_kept(nA, nA, tau)
+
+
+def test_table3_error_n1024_gpu(sp):
+    """End to end on the GPU (FP32): ||E||_F at the Table 3 valid ratios."""
+    N = 1024
+    A = synth.decay_matrix(N, "alg", 0.1, c=0.1)
+    AB = oracle.dense_product(A, A)
+    for tau, printed in ((1.4500655430308595, 996), (1.6619009145139256, 1302), (1.820188128117199, 1387)):
+        _, C = _run(sp, A, A, tau, "fp32")
+        err = math.sqrt(float(np.sum((AB - C.astype(np.float64)) ** 2)))
+        assert abs(err - printed) < 1.0, (tau, err)
+
+
+def test_errors_and_state(sp):
+    plan = sp.Plan(64, 64, 64, 1.0, "fp32")
+    A = torch.zeros((64, 64), device="cuda")
+    C = torch.zeros((64, 64), device="cuda")
+    with pytest.raises(sp.SpammError) as e:
+        plan.multiply(A, A, C)
+    assert e.value.status == sp.SPAMM_E_STATE
+    with pytest.raises(sp.SpammError) as e:
+        plan.norms(torch.zeros((64, 64)), A)     # host pointer
+    assert e.value.status == sp.SPAMM_E_INVALID
+    with pytest.raises(sp.SpammError) as e:
+        sp.Plan(64, 64, 64, 1.0, "fp32", tile=64)
+    assert e.value.status == sp.SPAMM_E_UNSUPPORTED
+
+
+def test_mgpu_single_rank_equals_single_gpu(sp):
+    N = 640
+    A = synth.perturbed_decay_matrix(N, 0.95, seed=31)
+    B = synth.perturbed_decay_matrix(N, 0.95, seed=32)
+    tau = 0.05
+    _, C1 = _run(sp, A, B, tau, "fp32")
+    plan = sp.Plan(N, N, N, tau, "fp32")
+    Ad, Bd = _dev(A, "fp32"), _dev(B, "fp32")
+    C = torch.zeros((N, N), device="cuda")
+    sp.spamm_multiply_mgpu(plan.handle, None, 0, 1, Ad, Bd, C, 0)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(C.cpu().numpy(), C1)
+    assert sp.spamm_get_partition(plan.handle, 1) == [0, N // T]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_full_size_bench_config_sampled(sp, prec):
+    """configs[1] at full size (N=8192, exp. decay lam=0.99, tau=1e-6) in the bench launch
+    configuration: exact kept count vs oracle, sampled C tiles vs oracle tiles."""
+    N, lam, tau = 8192, 0.99, 1e-6
+    A32 = _rounded(synth.decay_matrix(N, "exp", lam), prec)
+    nA = oracle.tile_norms(A32, T)
+    plan = sp.Plan(N, N, N, tau, prec)
+    Ad = _dev(A32, prec)
+    C = torch.empty((N, N), device="cuda")
+    plan.run(Ad, Ad, C)
+    torch.cuda.synchronize()
+    st = plan.stats()
+    band = oracle.band_count(nA, nA, tau)
+    assert abs(st["kept"] - oracle.count_kept(nA, nA, tau)) <= band
+    rng = np.random.default_rng(0)
+    BD = N // T
+    tiles = [(int(i), int(j)) for i, j in rng.integers(0, BD, size=(24, 2))]
+    tiles += [(d, d) for d in range(0, BD, 37)] + [(0, 1), (BD - 1, BD - 2), (BD - 1, BD - 1)]
+    Cn = C.cpu().numpy()
+    for i, j in tiles:
+        ref = oracle.spamm_tile(A32, A32, tau, T, i, j, nA, nA)
+        got = Cn[i * T:(i + 1) * T, j * T:(j + 1) * T]
+        nr = np.linalg.norm(ref)
+        if nr == 0:
+            assert np.all(got == 0)
+        else:
+            assert np.linalg.norm(got - ref) / nr <= (1e-5 if prec == "fp32" else 2e-2), (i, j)
