@@ -122,8 +122,9 @@ spamm_status spamm_norms(spamm_plan_t p, const void* A, int64_t lda, const void*
 
 /* Stage 2 (Alg. 2 lines 3-16; Sec. 3.5.1):
  * keep(i,k,j) <=> !(nA[i][k] * nB[k][j] < tau) in float64 (NaN kept).  Emits
- *   leaf CSR  : tile_ptr[BM*BN+1] (int64), k_idx[kept] (uint16, ascending per tile)
- *   V[i][j]   : list lengths;  row_work[i] = sum_j V[i][j]
+ *   leaf lists: k_idx[kept] (uint16), the list of C tile t = i*BN+j is the ascending run
+ *               k_idx[tile_start[t] .. tile_start[t] + V[t]) (lists stored macro-tile-major)
+ *   V[i][j]   : list lengths (PAPER.md:230);  row_work[i] = sum_j V[i][j]
  *   macro lists: per macro-tile of macro_i x macro_j C tiles, the union of kept k
  *               in ascending order with a keep bit per C tile, and an LPT schedule.
  * Requires spamm_norms on this plan (else SPAMM_E_STATE).  Stream-ordered; with
@@ -176,8 +177,10 @@ spamm_status spamm_multiply_mgpu(spamm_plan_t p, void* nccl_comm, int rank, int 
 spamm_status spamm_get_norms(spamm_plan_t p, const double** dA, const double** dBt,
                              int64_t* BM, int64_t* BK, int64_t* BN);
 
-/* Device pointers to the leaf CSR skip map; *kept is read back (synchronises). */
-spamm_status spamm_get_skipmap(spamm_plan_t p, const int64_t** d_tile_ptr, const uint16_t** d_k_idx,
+/* Device pointers to the per-C-tile k lists: tile_start[BM*BN] (int64) and k_idx[kept]
+ * (uint16); tile t's list is k_idx[tile_start[t] .. tile_start[t] + V[t]).
+ * *kept is read back (synchronises). */
+spamm_status spamm_get_skipmap(spamm_plan_t p, const int64_t** d_tile_start, const uint16_t** d_k_idx,
                                int64_t* kept);
 
 /* Device pointers to V[BM*BN] (int64) and row_work[BM] (int64). */

@@ -52,6 +52,21 @@ spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t e
   return SPAMM_OK;
 }
 
+spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                            uint64_t mid, uint64_t outer, uint64_t mid_stride_bytes, uint64_t outer_stride_bytes,
+                            uint32_t box0, uint32_t box1, uint32_t box2, CUtensorMapSwizzle swz) {
+  CUtensorMap dummy;
+  SPAMM_TRY(encode_tmap_2d(&dummy, dt, 2, base, 16, 1, 16, 8, 1, CU_TENSOR_MAP_SWIZZLE_NONE));  // resolves g_encode
+  cuuint64_t dims[3] = {inner, mid, outer};
+  cuuint64_t strides[2] = {mid_stride_bytes, outer_stride_bytes};
+  cuuint32_t box[3] = {box0, box1, box2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(map, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPAMM_E_INVALID, "cuTensorMapEncodeTiled(3d) failed (" + std::to_string(r) + ")");
+  return SPAMM_OK;
+}
+
 // --------------------------------------------------------------- validation
 static size_t esize_of(spamm_precision p) { return p == SPAMM_FP32 ? 4 : 2; }
 
@@ -89,8 +104,8 @@ static spamm_status alloc(void** p, size_t bytes) {
 
 static void free_plan(Plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_ptr, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent,
-                  p->order, p->order_tmp, p->keys_tmp, p->cub_tmp};
+  void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_start, p->L, p->leaf_base, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent, p->macro_run,
+                  p->order, p->hist, p->bucket_pos, p->cub_tmp};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->h_totals) cudaFreeHost(p->h_totals);
@@ -180,13 +195,21 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   ALLOC(nBt, double, BN * BK);
   ALLOC(V, int64_t, nleaf + 1);
   ALLOC(U, int64_t, nmac + 1);
-  ALLOC(leaf_ptr, int64_t, nleaf + 1);
+  ALLOC(leaf_start, int64_t, nleaf);
+  ALLOC(L, int64_t, nmac + 1);
+  ALLOC(leaf_base, int64_t, nmac + 1);
   ALLOC(macro_ptr, int64_t, nmac + 1);
   ALLOC(row_work, int64_t, BM);
   ALLOC(order, int32_t, nmac);
-  ALLOC(order_tmp, int32_t, nmac);
-  ALLOC(keys_tmp, int64_t, nmac);
+  ALLOC(hist, int64_t, BK + 2);
+  ALLOC(bucket_pos, int64_t, BK + 2);
 #undef ALLOC
+  if (st == SPAMM_OK && cudaMemset(p->V, 0, sizeof(int64_t) * (nleaf + 1)) != cudaSuccess)
+    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
+  if (st == SPAMM_OK && cudaMemset(p->U, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess)
+    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
+  if (st == SPAMM_OK && cudaMemset(p->L, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess)
+    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
   if (st == SPAMM_OK) {
     p->cub_tmp_bytes = skipmap_cub_bytes(nleaf, nmac);
     st = alloc(&p->cub_tmp, p->cub_tmp_bytes);
@@ -195,6 +218,8 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   if (st == SPAMM_OK) {
     p->macro_cap = nmac * BK;
     st = alloc(reinterpret_cast<void**>(&p->macro_ent), sizeof(uint2) * static_cast<size_t>(p->macro_cap));
+    if (st == SPAMM_OK && prec != SPAMM_FP32)
+      st = alloc(reinterpret_cast<void**>(&p->macro_run), sizeof(uint4) * static_cast<size_t>(p->macro_cap));
   }
   // leaf lists: reserve the worst case unless it exceeds the budget or SYNC_SKIPMAP is set
   if (st == SPAMM_OK && !(flags & SPAMM_FLAG_SYNC_SKIPMAP)) {
@@ -274,7 +299,7 @@ spamm_status do_skipmap(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   SPAMM_TRY(launch_skipmap_count(p, gi0, gi1, s));
   if (p.leaf_cap < p.BM * p.BN * p.BK) {
     // exact sizing: one stream synchronisation
-    SPAMM_CUDA_TRY(cudaMemcpyAsync(p.h_totals, p.leaf_ptr + p.BM * p.BN, sizeof(int64_t),
+    SPAMM_CUDA_TRY(cudaMemcpyAsync(p.h_totals, p.leaf_base + p.GM * p.GN, sizeof(int64_t),
                                    cudaMemcpyDeviceToHost, s));
     SPAMM_CUDA_TRY(cudaStreamSynchronize(s));
     SPAMM_TRY(ensure_leaf_capacity(p, std::max<int64_t>(p.h_totals[0], 1)));
@@ -354,16 +379,16 @@ spamm_status spamm_get_norms(spamm_plan_t h, const double** dA, const double** d
   return p.norms_ready ? SPAMM_OK : fail(SPAMM_E_STATE, "norms not computed");
 }
 
-spamm_status spamm_get_skipmap(spamm_plan_t h, const int64_t** d_tile_ptr, const uint16_t** d_k_idx,
+spamm_status spamm_get_skipmap(spamm_plan_t h, const int64_t** d_tile_start, const uint16_t** d_k_idx,
                                int64_t* kept) {
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
   if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
-  if (d_tile_ptr) *d_tile_ptr = p.leaf_ptr;
+  if (d_tile_start) *d_tile_start = p.leaf_start;
   if (d_k_idx) *d_k_idx = p.leaf_k;
   if (kept) {
     SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
-    SPAMM_CUDA_TRY(cudaMemcpy(kept, p.leaf_ptr + p.BM * p.BN, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    SPAMM_CUDA_TRY(cudaMemcpy(kept, p.leaf_base + p.GM * p.GN, sizeof(int64_t), cudaMemcpyDeviceToHost));
   }
   return SPAMM_OK;
 }
@@ -420,7 +445,7 @@ spamm_status spamm_get_stats(spamm_plan_t h, spamm_stats* out) {
   SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
   if (p.skipmap_ready) {
     int64_t tot[2];
-    SPAMM_CUDA_TRY(cudaMemcpy(&tot[0], p.leaf_ptr + p.BM * p.BN, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    SPAMM_CUDA_TRY(cudaMemcpy(&tot[0], p.leaf_base + p.GM * p.GN, sizeof(int64_t), cudaMemcpyDeviceToHost));
     SPAMM_CUDA_TRY(cudaMemcpy(&tot[1], p.macro_ptr + p.GM * p.GN, sizeof(int64_t), cudaMemcpyDeviceToHost));
     out->kept = tot[0];
     out->macro_entries = tot[1];

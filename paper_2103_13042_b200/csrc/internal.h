@@ -35,14 +35,17 @@ struct Plan {
   double* nBt = nullptr;     // [BN][BK]  (nB transposed)
   int64_t* V = nullptr;      // [BM*BN + 1] leaf counts, then (after scan) unused
   int64_t* U = nullptr;      // [GM*GN + 1] macro union counts
-  int64_t* leaf_ptr = nullptr;   // [BM*BN + 1]
+  int64_t* leaf_start = nullptr; // [BM*BN] start of each C tile's k list in leaf_k (macro-major)
+  int64_t* L = nullptr;          // [GM*GN + 1] kept pairs per macro-tile
+  int64_t* leaf_base = nullptr;  // [GM*GN + 1] exclusive scan of L
   int64_t* macro_ptr = nullptr;  // [GM*GN + 1]
   int64_t* row_work = nullptr;   // [BM]
   uint16_t* leaf_k = nullptr;    // [leaf_cap]
   uint2* macro_ent = nullptr;    // [macro_cap] (k, mask)
+  uint4* macro_run = nullptr;    // [macro_cap] tensor path: k|nruns|cols, packed MMA runs
   int32_t* order = nullptr;      // [GM*GN] LPT schedule
-  int32_t* order_tmp = nullptr;  // [GM*GN]
-  int64_t* keys_tmp = nullptr;   // [GM*GN]
+  int64_t* hist = nullptr;       // [BK+2] histogram of macro union counts
+  int64_t* bucket_pos = nullptr; // [BK+2] descending bucket starts (consumed by emit)
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
   int64_t leaf_cap = 0, macro_cap = 0;
@@ -92,6 +95,11 @@ spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const voi
                                   int64_t ldc, cudaStream_t s);
 
 size_t skipmap_cub_bytes(int64_t nleaf, int64_t nmac);
+
+// 3-D map: dims {inner, mid, outer} with byte strides {mid_stride, outer_stride}.
+spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                            uint64_t mid, uint64_t outer, uint64_t mid_stride_bytes, uint64_t outer_stride_bytes,
+                            uint32_t box0, uint32_t box1, uint32_t box2, CUtensorMapSwizzle swz);
 
 // TMA tensor-map encoder from the driver (resolved once via cudaGetDriverEntryPoint).
 spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void* base,

@@ -233,15 +233,16 @@ def spamm_get_norms(plan):
 
 
 def spamm_get_skipmap(plan):
-    """(tile_ptr int64 [BM*BN+1], k_idx int32 [kept]) copies of the leaf CSR skip map."""
+    """(tile_start int64 [BM*BN], k_idx int32 [kept]) copies: the k list of C tile t is
+    k_idx[tile_start[t] : tile_start[t] + V[t]] (V from spamm_get_counts)."""
     st = spamm_get_stats(plan)
     tp, ki = ctypes.c_void_p(), ctypes.c_void_p()
     kept = ctypes.c_int64()
     _check(_lib.spamm_get_skipmap(plan, ctypes.byref(tp), ctypes.byref(ki), ctypes.byref(kept)))
-    ptr = _view(tp.value, (st["BM"] * st["BN"] + 1,), "<i8", torch.int64)
+    start = _view(tp.value, (st["BM"] * st["BN"],), "<i8", torch.int64)
     k = _view(ki.value, (kept.value,), "<u2", torch.uint16) if kept.value else torch.zeros(0, dtype=torch.uint16,
                                                                                                device="cuda")
-    return ptr, k.to(torch.int32)
+    return start, k.to(torch.int32)
 
 
 def spamm_get_counts(plan):

@@ -70,11 +70,13 @@ def _run(sp, A32, B32, tau, prec, flags=0):
 
 
 def _gpu_keep(sp, plan, BM, BK, BN):
-    ptr, kidx = sp.spamm_get_skipmap(plan.handle)
-    ptr, kidx = ptr.cpu().numpy(), kidx.cpu().numpy()
+    start, kidx = sp.spamm_get_skipmap(plan.handle)
+    V = sp.spamm_get_counts(plan.handle)[0].cpu().numpy().reshape(-1)
+    start, kidx = start.cpu().numpy(), kidx.cpu().numpy()
     keep = np.zeros((BM, BK, BN), dtype=bool)
+    assert int(V.sum()) == len(kidx)
     for t in range(BM * BN):
-        ks = kidx[ptr[t]:ptr[t + 1]]
+        ks = kidx[start[t]:start[t] + V[t]]
         assert np.all(np.diff(ks) > 0), "k lists must be strictly ascending"
         keep[t // BN, ks, t % BN] = True
     return keep
