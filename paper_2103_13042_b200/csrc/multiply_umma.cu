@@ -35,15 +35,15 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kStages = 4;                      // ring stages, each holding kPer k-steps
+constexpr int kStages = 3;                      // ring stages, each holding kPer k-steps
 constexpr int kPer = 1;
 constexpr int kABytes = 128 * 32 * 2;           // 8 KB per k-step
 constexpr int kBBoxBytes = 32 * 32 * 2;         // 2 KB per 32 x 32 box
 constexpr int kBBytes = 8 * kBBoxBytes;         // 16 KB per k-step
 constexpr int kThreads = 256;
-constexpr int kCStageBytes = 32 * 16 * 4;       // one 32x16 FP32 C box (64-B rows, SWIZZLE_64B) per epilogue warp
+constexpr int kCStageBytes = 32 * 32 * 4;       // one 32x32 FP32 C box (SWIZZLE_128B); 2 per epilogue warp
 constexpr size_t kRingBytes = static_cast<size_t>(kStages) * kPer * (kABytes + kBBytes);
-constexpr size_t kSmemBytes = 1024 + kRingBytes + 4 * kCStageBytes + 1024;   // 2 CTAs per SM
+constexpr size_t kSmemBytes = 1024 + kRingBytes + 8 * kCStageBytes + 1024;   // 2 CTAs per SM
 constexpr uint32_t kTmemCols = 256;             // one 128x256 FP32 accumulator per CTA (2 CTAs per SM)
 
 __device__ __forceinline__ int64_t snake(int64_t r, int G, int b) { return r * G + ((r & 1) ? (G - 1 - b) : b); }
@@ -80,14 +80,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                           // [stage][slot] 8 KB
   uint8_t* sB = smem + kStages * kPer * kABytes;                // [stage][slot] 16 KB
-  uint8_t* sC = smem + kRingBytes;                              // [4 warps] 2 KB
-  uint64_t* full = reinterpret_cast<uint64_t*>(sC + 4 * kCStageBytes);
+  uint8_t* sC = smem + kRingBytes;                              // [4 warps][2 bufs] 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + 8 * kCStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint4* srun = reinterpret_cast<uint4*>(tempty + 2);           // [stage][slot]: pre-decoded runs
   uint32_t* scount = reinterpret_cast<uint32_t*>(srun + kStages * kPer);   // k-steps in the stage
-  uint4* sent = reinterpret_cast<uint4*>(scount + kStages);     // [32]: producer entry batch (16-B aligned)
+  uint4* sent = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(scount + kStages) + 15) & ~uintptr_t(15));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sent + 32);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -293,27 +293,23 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (dbg_mode == 7) continue;                          // debug 7: TMEM loads only
         tmem_st_32x32b_x32_zero(taddr);
         if (dbg_mode == 8) continue;                          // debug 8: TMEM load + zero store
-        uint8_t* box = sC + q * kCStageBytes;
-        // two 32x16 boxes per 32-column chunk; row = lane (64 B), 16-byte piece j at j ^ ((row >> 1) & 3)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (c + h > 0) {
-            if (lane == 0) bulk_wait_group_read<0>();   // previous store out of this box
-            __syncwarp();
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int pj = j ^ ((lane >> 1) & 3);
-            *reinterpret_cast<uint4*>(box + lane * 64 + pj * 16) =
-                make_uint4(v[16 * h + 4 * j], v[16 * h + 4 * j + 1], v[16 * h + 4 * j + 2], v[16 * h + 4 * j + 3]);
-          }
-          fence_proxy_async_smem();
+        uint8_t* box = sC + (q * 2 + (c & 1)) * kCStageBytes;
+        if (c >= 2) {
+          if (lane == 0) bulk_wait_group_read<1>();   // the store issued from this buffer two chunks ago
           __syncwarp();
-          if (lane == 0 && dbg_mode != 4 && dbg_mode < 5) {   // debug 4/5: no C store
-            tma_store_2d(&tC, box, static_cast<int32_t>(J * 256 + c * 32 + h * 16),
-                         static_cast<int32_t>(I * 128 + q * 32));
-            bulk_commit_group();
-          }
+        }
+        // row = lane (128 B); 16-byte chunk j stored at j ^ (row % 8)  (SWIZZLE_128B)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int pj = j ^ (lane & 7);
+          *reinterpret_cast<uint4*>(box + lane * 128 + pj * 16) =
+              make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && dbg_mode != 4 && dbg_mode < 5) {   // debug 4/5: no C store
+          tma_store_2d(&tC, box, static_cast<int32_t>(J * 256 + c * 32), static_cast<int32_t>(I * 128 + q * 32));
+          bulk_commit_group();
         }
       }
       if (lane == 0) bulk_wait_group_read<0>();
@@ -338,8 +334,8 @@ template <uint32_t kFmt>
 spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                         cudaStream_t s, CUtensorMapDataType dt) {
   CUtensorMap tA, tB, tB8, tB4, tB2, tB1, tC;
-  SPAMM_TRY(encode_tmap_2d(&tC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, p.N, p.M, ldc, 16, 32,
-                           CU_TENSOR_MAP_SWIZZLE_64B));
+  SPAMM_TRY(encode_tmap_2d(&tC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, p.N, p.M, ldc, 32, 32,
+                           CU_TENSOR_MAP_SWIZZLE_128B));
   SPAMM_TRY(encode_tmap_2d(&tA, dt, 2, A, p.K, p.M, lda, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_tmap_2d(&tB, dt, 2, B, p.N, p.K, ldb, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
   // B as stacked [32 k][32 n] boxes: dims {32 n, K, N/32} with strides {ldb, 32} elements.
