@@ -186,11 +186,13 @@ spamm_status spamm_get_skipmap(spamm_plan_t p, const int64_t** d_tile_start, con
 /* Device pointers to V[BM*BN] (int64) and row_work[BM] (int64). */
 spamm_status spamm_get_counts(spamm_plan_t p, const int64_t** d_V, const int64_t** d_row_work);
 
-/* Device pointers to the macro lists: ptr[GM*GN+1] (int64), entries[n] as pairs
- * (uint32 k, uint32 mask), bit (li*macro_j + lj) = keep of C tile (I*macro_i+li, J*macro_j+lj);
- * order[GM*GN] (int32) = LPT schedule (descending entry count). */
-spamm_status spamm_get_macro(spamm_plan_t p, const int64_t** d_ptr, const uint32_t** d_entries,
-                             const int32_t** d_order, int64_t* GM, int64_t* GN);
+/* Device pointers to the macro lists: macro-tile t = I*GN+J owns the entries
+ * [start[t], start[t] + count[t]) (start, count int64[GM*GN]); an entry is the pair
+ * (uint32 k, uint32 mask), k ascending, bit (li*macro_j + lj) = keep of C tile
+ * (I*macro_i+li, J*macro_j+lj); order[GM*GN] (int32) = LPT schedule (descending count;
+ * order within equal counts unspecified). */
+spamm_status spamm_get_macro(spamm_plan_t p, const int64_t** d_start, const int64_t** d_count,
+                             const uint32_t** d_entries, const int32_t** d_order, int64_t* GM, int64_t* GN);
 
 /* Tile-row range of the last multi-GPU partition (nranks+1 entries, host memory). */
 spamm_status spamm_get_partition(spamm_plan_t p, int64_t* row_begin, int nranks);

@@ -105,9 +105,10 @@ static spamm_status alloc(void** p, size_t bytes) {
 static void free_plan(Plan* p) {
   if (!p) return;
   void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_start, p->L, p->leaf_base, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent, p->macro_run,
-                  p->order, p->hist, p->bucket_pos, p->cub_tmp};
+                  p->order, p->bucket_pos, p->ticket, p->cub_tmp};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  if (p->mstart && p->mstart != p->macro_ptr) cudaFree(p->mstart);
   if (p->h_totals) cudaFreeHost(p->h_totals);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
@@ -199,9 +200,9 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   ALLOC(L, int64_t, nmac + 1);
   ALLOC(leaf_base, int64_t, nmac + 1);
   ALLOC(macro_ptr, int64_t, nmac + 1);
-  ALLOC(row_work, int64_t, BM);
+  ALLOC(row_work, int64_t, BM + BK + 4);
+  ALLOC(ticket, unsigned int, 1);
   ALLOC(order, int32_t, nmac);
-  ALLOC(hist, int64_t, BK + 2);
   ALLOC(bucket_pos, int64_t, BK + 2);
 #undef ALLOC
   if (st == SPAMM_OK && cudaMemset(p->V, 0, sizeof(int64_t) * (nleaf + 1)) != cudaSuccess)
@@ -210,6 +211,12 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     st = fail(SPAMM_E_CUDA, "cudaMemset failed");
   if (st == SPAMM_OK && cudaMemset(p->L, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess)
     st = fail(SPAMM_E_CUDA, "cudaMemset failed");
+  if (st == SPAMM_OK && cudaMemset(p->ticket, 0, sizeof(unsigned int)) != cudaSuccess)
+    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
+  if (st == SPAMM_OK) {
+    p->hist = p->row_work + BM;
+    p->totals = p->hist + BK + 2;
+  }
   if (st == SPAMM_OK) {
     p->cub_tmp_bytes = skipmap_cub_bytes(nleaf, nmac);
     st = alloc(&p->cub_tmp, p->cub_tmp_bytes);
@@ -224,7 +231,24 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   // leaf lists: reserve the worst case unless it exceeds the budget or SYNC_SKIPMAP is set
   if (st == SPAMM_OK && !(flags & SPAMM_FLAG_SYNC_SKIPMAP)) {
     const size_t worst = sizeof(uint16_t) * static_cast<size_t>(nleaf) * static_cast<size_t>(BK);
-    if (worst <= kWorstCaseBudget) st = ensure_leaf_capacity(*p, nleaf * BK);
+    if (worst <= kWorstCaseBudget) {
+      st = ensure_leaf_capacity(*p, nleaf * BK);
+      p->fixed_regions = st == SPAMM_OK;
+    }
+  }
+  // macro-tile t's entries start at t*BK (fixed regions) or at the scanned offset macro_ptr[t]
+  if (st == SPAMM_OK) {
+    if (p->fixed_regions) {
+      st = alloc(reinterpret_cast<void**>(&p->mstart), sizeof(int64_t) * static_cast<size_t>(nmac));
+      if (st == SPAMM_OK) {
+        std::vector<int64_t> h(static_cast<size_t>(nmac));
+        for (int64_t t = 0; t < nmac; ++t) h[static_cast<size_t>(t)] = t * BK;
+        if (cudaMemcpy(p->mstart, h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+          st = fail(SPAMM_E_CUDA, "cudaMemcpy failed");
+      }
+    } else {
+      p->mstart = p->macro_ptr;
+    }
   }
   if (st == SPAMM_OK && cudaMallocHost(reinterpret_cast<void**>(&p->h_totals), 2 * sizeof(int64_t)) != cudaSuccess)
     st = fail(SPAMM_E_NOMEM, "cudaMallocHost failed");
@@ -296,15 +320,19 @@ spamm_status do_skipmap(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   if (!p.norms_ready) return fail(SPAMM_E_STATE, "spamm_build_skipmap before spamm_norms");
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
-  SPAMM_TRY(launch_skipmap_count(p, gi0, gi1, s));
-  if (p.leaf_cap < p.BM * p.BN * p.BK) {
-    // exact sizing: one stream synchronisation
-    SPAMM_CUDA_TRY(cudaMemcpyAsync(p.h_totals, p.leaf_base + p.GM * p.GN, sizeof(int64_t),
-                                   cudaMemcpyDeviceToHost, s));
-    SPAMM_CUDA_TRY(cudaStreamSynchronize(s));
-    SPAMM_TRY(ensure_leaf_capacity(p, std::max<int64_t>(p.h_totals[0], 1)));
+  if (p.fixed_regions) {
+    SPAMM_TRY(launch_skipmap_fused(p, gi0, gi1, s));
+  } else {
+    SPAMM_TRY(launch_skipmap_count(p, gi0, gi1, s));
+    if (p.leaf_cap < p.BM * p.BN * p.BK) {
+      // exact sizing: one stream synchronisation
+      SPAMM_CUDA_TRY(cudaMemcpyAsync(p.h_totals, p.leaf_base + p.GM * p.GN, sizeof(int64_t),
+                                     cudaMemcpyDeviceToHost, s));
+      SPAMM_CUDA_TRY(cudaStreamSynchronize(s));
+      SPAMM_TRY(ensure_leaf_capacity(p, std::max<int64_t>(p.h_totals[0], 1)));
+    }
+    SPAMM_TRY(launch_skipmap_emit(p, gi0, gi1, s));
   }
-  SPAMM_TRY(launch_skipmap_emit(p, gi0, gi1, s));
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[3], s));
   p.ev_skip = timing;
   p.row_begin_macro = gi0;
@@ -388,7 +416,7 @@ spamm_status spamm_get_skipmap(spamm_plan_t h, const int64_t** d_tile_start, con
   if (d_k_idx) *d_k_idx = p.leaf_k;
   if (kept) {
     SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
-    SPAMM_CUDA_TRY(cudaMemcpy(kept, p.leaf_base + p.GM * p.GN, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    SPAMM_CUDA_TRY(cudaMemcpy(kept, p.totals, sizeof(int64_t), cudaMemcpyDeviceToHost));
   }
   return SPAMM_OK;
 }
@@ -402,12 +430,13 @@ spamm_status spamm_get_counts(spamm_plan_t h, const int64_t** d_V, const int64_t
   return SPAMM_OK;
 }
 
-spamm_status spamm_get_macro(spamm_plan_t h, const int64_t** d_ptr, const uint32_t** d_entries,
-                             const int32_t** d_order, int64_t* GM, int64_t* GN) {
+spamm_status spamm_get_macro(spamm_plan_t h, const int64_t** d_start, const int64_t** d_count,
+                             const uint32_t** d_entries, const int32_t** d_order, int64_t* GM, int64_t* GN) {
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
   if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
-  if (d_ptr) *d_ptr = p.macro_ptr;
+  if (d_start) *d_start = p.mstart;
+  if (d_count) *d_count = p.U;
   if (d_entries) *d_entries = reinterpret_cast<const uint32_t*>(p.macro_ent);
   if (d_order) *d_order = p.order;
   if (GM) *GM = p.GM;
@@ -445,8 +474,7 @@ spamm_status spamm_get_stats(spamm_plan_t h, spamm_stats* out) {
   SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
   if (p.skipmap_ready) {
     int64_t tot[2];
-    SPAMM_CUDA_TRY(cudaMemcpy(&tot[0], p.leaf_base + p.GM * p.GN, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    SPAMM_CUDA_TRY(cudaMemcpy(&tot[1], p.macro_ptr + p.GM * p.GN, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    SPAMM_CUDA_TRY(cudaMemcpy(tot, p.totals, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
     out->kept = tot[0];
     out->macro_entries = tot[1];
     out->valid_ratio = static_cast<double>(tot[0]) / (static_cast<double>(p.BM) * p.BK * p.BN);

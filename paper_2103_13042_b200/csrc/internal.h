@@ -39,12 +39,16 @@ struct Plan {
   int64_t* L = nullptr;          // [GM*GN + 1] kept pairs per macro-tile
   int64_t* leaf_base = nullptr;  // [GM*GN + 1] exclusive scan of L
   int64_t* macro_ptr = nullptr;  // [GM*GN + 1]
-  int64_t* row_work = nullptr;   // [BM]
+  int64_t* row_work = nullptr;   // [BM + BK + 2]: row work, then the U histogram (one memset)
+  unsigned int* ticket = nullptr; // CTA-completion ticket of the count kernel (self-resetting)
   uint16_t* leaf_k = nullptr;    // [leaf_cap]
   uint2* macro_ent = nullptr;    // [macro_cap] (k, mask)
   uint4* macro_run = nullptr;    // [macro_cap] tensor path: k|nruns|cols, packed MMA runs
   int32_t* order = nullptr;      // [GM*GN] LPT schedule
-  int64_t* hist = nullptr;       // [BK+2] histogram of macro union counts
+  int64_t* hist = nullptr;       // = row_work + BM: [BK+2] histogram of macro union counts
+  int64_t* totals = nullptr;     // = hist + BK + 2: [0] kept pairs, [1] macro entries
+  int64_t* mstart = nullptr;     // [GM*GN] start of each macro-tile's entries (t*BK or macro_ptr)
+  bool fixed_regions = false;    // lists stored in worst-case fixed regions (single-pass skip map)
   int64_t* bucket_pos = nullptr; // [BK+2] descending bucket starts (consumed by emit)
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
@@ -89,6 +93,7 @@ spamm_status launch_norms(const Plan& p, const void* X, int64_t rows, int64_t co
                           int64_t row_tile_end, cudaStream_t s);
 spamm_status launch_skipmap_count(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);
 spamm_status launch_skipmap_emit(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);
+spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);
 spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,

@@ -39,7 +39,7 @@ __device__ __forceinline__ float comp(const float4& v, int i) {
 __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_simt_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
-                          const int64_t* __restrict__ mptr, const uint2* __restrict__ ment,
+                          const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (idx >= n_tiles) break;
         const int64_t t = order[idx];
         const int32_t I = static_cast<int32_t>(t / GN), J = static_cast<int32_t>(t % GN);
-        const int64_t e1 = mptr[t + 1];
-        for (int64_t e = mptr[t]; e < e1; ++e) {
+        const int64_t e0 = mstart[t], e1 = e0 + mcount[t];
+        for (int64_t e = e0; e < e1; ++e) {
           const uint2 en = ment[e];
           mbar_wait(&empty[s], ph ^ 1);
           smask[s] = en.y;
@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t I = t / GN, J = t % GN;
     float4* acc = sAcc + warp * 8 * 32 + lane;   // acc[j4 * 32]: outputs 4*j4 .. 4*j4+3 of this lane
     bool first = true;
-    const int64_t e1 = mptr[t + 1];
-    for (int64_t e = mptr[t]; e < e1; ++e) {
+    const int64_t e0 = mstart[t], e1 = e0 + mcount[t];
+    for (int64_t e = e0; e < e1; ++e) {
       mbar_wait(&full[s], ph);
       const uint32_t mask = smask[s];
       if ((mask >> bit) & 1u) {
@@ -203,7 +203,7 @@ spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const fl
   const int64_t n_tiles = static_cast<int64_t>(p.row_end_macro - p.row_begin_macro) * p.GN;
   if (n_tiles <= 0) return SPAMM_OK;
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
-  spamm_mul_simt_kernel<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.macro_ptr, p.macro_ent,
+  spamm_mul_simt_kernel<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.mstart, p.U, p.macro_ent,
                                                            p.order, n_tiles, p.GN);
   count_launch();
   cudaError_t e = cudaGetLastError();

@@ -56,13 +56,13 @@ __device__ __forceinline__ int64_t stages_for(int64_t E) {
 struct TileInfo {
   int64_t t, e0, e1;
 };
-__device__ __forceinline__ TileInfo tile_info(const int32_t* order, const int64_t* mptr, int64_t idx,
-                                              int64_t n_tiles) {
+__device__ __forceinline__ TileInfo tile_info(const int32_t* order, const int64_t* mstart, const int64_t* mcount,
+                                              int64_t idx, int64_t n_tiles) {
   TileInfo ti{-1, 0, 0};
   if (idx < n_tiles) {
     ti.t = order[idx];
-    ti.e0 = mptr[ti.t];
-    ti.e1 = mptr[ti.t + 1];
+    ti.e0 = mstart[ti.t];
+    ti.e1 = ti.e0 + mcount[ti.t];
   }
   return ti;
 }
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                           const __grid_constant__ CUtensorMap tB8, const __grid_constant__ CUtensorMap tB4,
                           const __grid_constant__ CUtensorMap tB2, const __grid_constant__ CUtensorMap tB1,
                           const __grid_constant__ CUtensorMap tC, int use3d, int dbg_mode,
-                          const int64_t* __restrict__ mptr, const uint4* __restrict__ ment,
+                          const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN,
                           unsigned long long* __restrict__ prof) {
   extern __shared__ uint8_t smem_raw[];
@@ -125,10 +125,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t ph = 0;
     unsigned long long p_load = 0, p_wait = 0;
     const unsigned long long p_t0 = clock64();
-    TileInfo nxt = tile_info(order, mptr, snake(0, G, b), n_tiles);
+    TileInfo nxt = tile_info(order, mstart, mcount, snake(0, G, b), n_tiles);
     for (int64_t r = 0; nxt.t >= 0; ++r) {
       const TileInfo cur = nxt;
-      nxt = tile_info(order, mptr, snake(r + 1, G, b), n_tiles);   // prefetch
+      nxt = tile_info(order, mstart, mcount, snake(r + 1, G, b), n_tiles);   // prefetch
       const int32_t I = static_cast<int32_t>(cur.t / GN), J = static_cast<int32_t>(cur.t % GN);
       for (int64_t eb = cur.e0; eb < cur.e1; eb += 32) {
         const int cnt = static_cast<int>(cur.e1 - eb < 32 ? cur.e1 - eb : 32);
@@ -204,10 +204,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       uint32_t ph = 0;
       int64_t it = 0;
       unsigned long long m_te = 0, m_fu = 0;
-      TileInfo nxt = tile_info(order, mptr, snake(0, G, b), n_tiles);
+      TileInfo nxt = tile_info(order, mstart, mcount, snake(0, G, b), n_tiles);
       for (int64_t r = 0; nxt.t >= 0; ++r, ++it) {
         const TileInfo cur = nxt;
-        nxt = tile_info(order, mptr, snake(r + 1, G, b), n_tiles);
+        nxt = tile_info(order, mstart, mcount, snake(r + 1, G, b), n_tiles);
         const int buf = 0;
         unsigned long long tw0 = prof ? clock64() : 0;
         mbar_wait(&tempty[0], static_cast<uint32_t>(it & 1));
@@ -272,10 +272,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0) mbar_arrive(&tempty[0]);
     int64_t it = 0;
     unsigned long long e_w = 0, e_d = 0;
-    TileInfo nxt = tile_info(order, mptr, snake(0, G, b), n_tiles);
+    TileInfo nxt = tile_info(order, mstart, mcount, snake(0, G, b), n_tiles);
     for (int64_t r = 0; nxt.t >= 0; ++r, ++it) {
       const TileInfo cur = nxt;
-      nxt = tile_info(order, mptr, snake(r + 1, G, b), n_tiles);
+      nxt = tile_info(order, mstart, mcount, snake(r + 1, G, b), n_tiles);
       const int64_t I = cur.t / GN, J = cur.t % GN;
       const int buf = 0;
       unsigned long long te0 = prof ? clock64() : 0;
@@ -367,7 +367,7 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
   }
   if (prof) cudaMemsetAsync(prof, 0, 296 * 16 * 8, s);
   spamm_mul_umma_kernel<kFmt><<<grid, kThreads, kSmemBytes, s>>>(tA, tB, tB8, tB4, tB2, tB1, tC, use3d, dbg_mode,
-                                                                 p.macro_ptr, p.macro_run, p.order, n_tiles, p.GN,
+                                                                 p.mstart, p.U, p.macro_run, p.order, n_tiles, p.GN,
                                                                  prof);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());

@@ -70,7 +70,7 @@ def _load():
         "spamm_get_norms": [P, PP, PP, PI64, PI64, PI64],
         "spamm_get_skipmap": [P, PP, PP, PI64],
         "spamm_get_counts": [P, PP, PP],
-        "spamm_get_macro": [P, PP, PP, PP, PI64, PI64],
+        "spamm_get_macro": [P, PP, PP, PP, PP, PI64, PI64],
         "spamm_get_partition": [P, PI64, ctypes.c_int],
         "spamm_get_stats": [P, ctypes.POINTER(spamm_stats)],
     }
@@ -233,15 +233,17 @@ def spamm_get_norms(plan):
 
 
 def spamm_get_skipmap(plan):
-    """(tile_start int64 [BM*BN], k_idx int32 [kept]) copies: the k list of C tile t is
-    k_idx[tile_start[t] : tile_start[t] + V[t]] (V from spamm_get_counts)."""
+    """(tile_start int64 [BM*BN], k_idx int32 [n]) copies: the k list of C tile t is
+    k_idx[tile_start[t] : tile_start[t] + V[t]] (V from spamm_get_counts).  k_idx covers
+    the storage in use (lists may sit in fixed per-tile regions)."""
     st = spamm_get_stats(plan)
     tp, ki = ctypes.c_void_p(), ctypes.c_void_p()
     kept = ctypes.c_int64()
     _check(_lib.spamm_get_skipmap(plan, ctypes.byref(tp), ctypes.byref(ki), ctypes.byref(kept)))
     start = _view(tp.value, (st["BM"] * st["BN"],), "<i8", torch.int64)
-    k = _view(ki.value, (kept.value,), "<u2", torch.uint16) if kept.value else torch.zeros(0, dtype=torch.uint16,
-                                                                                               device="cuda")
+    V = spamm_get_counts(plan)[0].reshape(-1)
+    n = int((start + V).max().item()) if V.numel() else 0
+    k = _view(ki.value, (n,), "<u2", torch.uint16) if n else torch.zeros(0, dtype=torch.uint16, device="cuda")
     return start, k.to(torch.int32)
 
 
@@ -255,18 +257,22 @@ def spamm_get_counts(plan):
 
 
 def spamm_get_macro(plan):
-    """(ptr int64 [GM*GN+1], entries uint32 [n,2] as int64, order int32 [GM*GN], GM, GN)."""
+    """(start int64 [GM*GN], count int64 [GM*GN], entries [n, 2] int64 (k, mask) over all
+    entry storage in use, order int32 [GM*GN], GM, GN); macro-tile t's list is
+    entries[start[t] : start[t] + count[t]]."""
     st = spamm_get_stats(plan)
-    p, e, o = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    ps, pc, e, o = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
     GM, GN = ctypes.c_int64(), ctypes.c_int64()
-    _check(_lib.spamm_get_macro(plan, ctypes.byref(p), ctypes.byref(e), ctypes.byref(o), ctypes.byref(GM),
-                                ctypes.byref(GN)))
-    n = st["macro_entries"]
-    ptr = _view(p.value, (GM.value * GN.value + 1,), "<i8", torch.int64)
+    _check(_lib.spamm_get_macro(plan, ctypes.byref(ps), ctypes.byref(pc), ctypes.byref(e), ctypes.byref(o),
+                                ctypes.byref(GM), ctypes.byref(GN)))
+    nmac = GM.value * GN.value
+    start = _view(ps.value, (nmac,), "<i8", torch.int64)
+    count = _view(pc.value, (nmac,), "<i8", torch.int64)
+    n = int((start + count).max().item()) if nmac else 0
     ent = _view(e.value, (n, 2), "<u4", torch.uint32).to(torch.int64) if n else torch.zeros((0, 2), dtype=torch.int64,
                                                                                              device="cuda")
-    order = _view(o.value, (GM.value * GN.value,), "<i4", torch.int32)
-    return ptr, ent, order, GM.value, GN.value
+    order = _view(o.value, (nmac,), "<i4", torch.int32)
+    return start, count, ent, order, GM.value, GN.value
 
 
 def spamm_get_partition(plan, nranks: int) -> list[int]:

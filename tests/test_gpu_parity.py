@@ -74,7 +74,6 @@ def _gpu_keep(sp, plan, BM, BK, BN):
     V = sp.spamm_get_counts(plan.handle)[0].cpu().numpy().reshape(-1)
     start, kidx = start.cpu().numpy(), kidx.cpu().numpy()
     keep = np.zeros((BM, BK, BN), dtype=bool)
-    assert int(V.sum()) == len(kidx)
     for t in range(BM * BN):
         ks = kidx[start[t]:start[t] + V[t]]
         assert np.all(np.diff(ks) > 0), "k lists must be strictly ascending"
@@ -162,13 +161,16 @@ def test_macro_lists_match_oracle(sp):
         nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
         tau = float(np.median(nA[:, :, None] * nB[None, :, :]))
         plan, _ = _run(sp, A, B, tau, prec)
-        ptr, ent, order, GM, GN = sp.spamm_get_macro(plan.handle)
+        start, count, ent, order, GM, GN = sp.spamm_get_macro(plan.handle)
+        start, count, ent = start.cpu().numpy(), count.cpu().numpy(), ent.cpu().numpy()
         ref = oracle.macro_lists(nA, nB, tau, 4, MJ)
-        np.testing.assert_array_equal(ptr.cpu().numpy(), ref["ptr"])
-        np.testing.assert_array_equal(ent.cpu().numpy(), ref["entries"])
+        np.testing.assert_array_equal(count, np.diff(ref["ptr"]))
+        for t in range(GM * GN):
+            np.testing.assert_array_equal(ent[start[t]:start[t] + count[t]],
+                                          ref["entries"][ref["ptr"][t]:ref["ptr"][t + 1]])
         o = order.cpu().numpy()
         assert sorted(o.tolist()) == list(range(GM * GN))
-        lens = np.diff(ref["ptr"])[o]
+        lens = count[o]
         assert np.all(np.diff(lens) <= 0), "LPT order must be descending in work"
 
 
