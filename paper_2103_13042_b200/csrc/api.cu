@@ -295,15 +295,9 @@ spamm_status do_norms_range(Plan& p, const void* A, int64_t lda, const void* B, 
   SPAMM_TRY(check_matrix(B, p.K, p.N, ldb, esize_of(p.prec), "B"));
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[0], s));
-  // A (M x K): tile row i, tile col k -> nA[i*BK + k]
-  SPAMM_TRY(launch_norms(p, A, p.M, p.K, lda, p.nA, p.BK, 1, ar0, ar1, s));
-  // B (K x N) column strip [bj0*T, bj1*T): tile row k, tile col j -> nBt[j*BK + k]
-  if (bj1 > bj0) {
-    const size_t es = esize_of(p.prec);
-    const void* Bs = static_cast<const char*>(B) + static_cast<size_t>(bj0) * kTile * es;
-    const int64_t cols = std::min<int64_t>(p.N, bj1 * kTile) - bj0 * kTile;
-    SPAMM_TRY(launch_norms(p, Bs, p.K, cols, ldb, p.nBt + bj0 * p.BK, 1, p.BK, 0, p.BK, s));
-  }
+  // A (M x K): tile row i, tile col k -> nA[i*BK + k];  B (K x N) column strip [bj0*T, bj1*T):
+  // tile row k, tile col j -> nBt[j*BK + k]
+  SPAMM_TRY(launch_norms2(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s));
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[1], s));
   p.ev_norms = timing;
   p.norms_ready = true;

@@ -88,9 +88,9 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 
 // stage launchers (implemented in the .cu files) -----------------------------
-spamm_status launch_norms(const Plan& p, const void* X, int64_t rows, int64_t cols, int64_t ld,
-                          double* out, int64_t out_rs, int64_t out_cs, int64_t row_tile_begin,
-                          int64_t row_tile_end, cudaStream_t s);
+// norms of A's tile rows [ar0, ar1) and B's tile columns [bj0, bj1) in one launch
+spamm_status launch_norms2(const Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B,
+                           int64_t ldb, int64_t bj0, int64_t bj1, cudaStream_t s);
 spamm_status launch_skipmap_count(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);
 spamm_status launch_skipmap_emit(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);
 spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);

@@ -1,140 +1,170 @@
 // norms.cu -- stage 1: tile Frobenius norms (Eq. 2; get-norm kernel Sec. 3.2,
 // PAPER.md:105-123).
 //
-// B200 design (not the paper's one-block-per-tile reduction): the matrix is read
-// exactly once, fully coalesced, with 16-byte streaming loads; a CTA covers one
-// 32-row tile strip and a chunk of columns.  Each lane owns 16 B of a row (4 FP32
-// or 8 BF16/FP16 values), accumulates x*x in float64 over its 4 rows, the lanes of
-// one tile combine with an xor-shuffle butterfly and the 8 warps combine in smem
-// in warp order.  The operation sequence per tile does not depend on the tile's
-// position, so equal tiles give bit-identical norms (Toeplitz inputs).
+// B200 design (not the paper's one-block-per-tile shared-memory tree): the matrices are
+// read exactly once by TMA.  A CTA owns one 32-row tile strip and a range of 512-byte-wide
+// column boxes ([32 rows x 512 B] = 8 FP32 tiles or 4... see kColsPerBox); one thread issues
+// the bulk tensor loads into a 4-deep shared-memory ring (mbarrier completion), the 4
+// warps each reduce 8 rows of a box: every lane squares 16 contiguous bytes per row in
+// float64, the lanes of one tile combine with an xor butterfly and the warps' partials
+// are summed in warp order.  The operation sequence per tile does not depend on the
+// tile's position, so equal tiles give bit-identical norms (Toeplitz inputs).  TMA's
+// out-of-bounds zero fill implements the zero padding of PAPER.md:99.  A and B are
+// normed by one launch.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace spamm {
 namespace {
 
-constexpr int kWarps = 8;         // rows w, w+8, w+16, w+24 of the strip
-constexpr int kGroups = 8;        // 32*V-column groups per CTA
+using namespace sm100;
+
+constexpr int kThreads = 128;          // 4 warps x 8 rows of a 32-row box
+constexpr int kStages = 4;
+constexpr int kBoxBytesRow = 512;      // bytes per box row (256 BF16 / 128 FP32 columns)
+constexpr int kBoxBytes = 32 * kBoxBytesRow;   // 16 KB
+constexpr int kBoxesPerCta = 8;        // column boxes walked by one CTA
+constexpr size_t kSmemBytes = 128 + static_cast<size_t>(kStages) * kBoxBytes + 1024;
 
 template <typename T>
-__device__ __forceinline__ double sq_sum_vec(const T* p, int n_valid);
-
+__device__ __forceinline__ double sq16(const uint4& raw);
 template <>
-__device__ __forceinline__ double sq_sum_vec<float>(const float* p, int n_valid) {
+__device__ __forceinline__ double sq16<float>(const uint4& raw) {
   double s = 0.0;
-  if (n_valid >= 4) {
-    float4 v = __ldcs(reinterpret_cast<const float4*>(p));
-    s = fma((double)v.x, (double)v.x, s);
-    s = fma((double)v.y, (double)v.y, s);
-    s = fma((double)v.z, (double)v.z, s);
-    s = fma((double)v.w, (double)v.w, s);
-  } else {
-    for (int e = 0; e < 4; ++e) {
-      double x = e < n_valid ? (double)p[e] : 0.0;
-      s = fma(x, x, s);
-    }
-  }
-  return s;
-}
-
-template <typename H>
-__device__ __forceinline__ double to_d(H h);
-template <>
-__device__ __forceinline__ double to_d<__nv_bfloat16>(__nv_bfloat16 h) { return (double)__bfloat162float(h); }
-template <>
-__device__ __forceinline__ double to_d<__half>(__half h) { return (double)__half2float(h); }
-
-template <typename H>
-__device__ __forceinline__ double sq_sum_vec16(const H* p, int n_valid) {
-  double s = 0.0;
-  if (n_valid >= 8) {
-    int4 raw = __ldcs(reinterpret_cast<const int4*>(p));
-    const H* h = reinterpret_cast<const H*>(&raw);
+  const float* f = reinterpret_cast<const float*>(&raw);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      double x = to_d<H>(h[e]);
-      s = fma(x, x, s);
-    }
-  } else {
-    for (int e = 0; e < 8; ++e) {
-      double x = e < n_valid ? to_d<H>(p[e]) : 0.0;
-      s = fma(x, x, s);
-    }
+  for (int e = 0; e < 4; ++e) s = fma(static_cast<double>(f[e]), static_cast<double>(f[e]), s);
+  return s;
+}
+template <>
+__device__ __forceinline__ double sq16<__nv_bfloat16>(const uint4& raw) {
+  double s = 0.0;
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const double x = static_cast<double>(__bfloat162float(h[e]));
+    s = fma(x, x, s);
   }
   return s;
 }
 template <>
-__device__ __forceinline__ double sq_sum_vec<__nv_bfloat16>(const __nv_bfloat16* p, int n_valid) {
-  return sq_sum_vec16<__nv_bfloat16>(p, n_valid);
-}
-template <>
-__device__ __forceinline__ double sq_sum_vec<__half>(const __half* p, int n_valid) {
-  return sq_sum_vec16<__half>(p, n_valid);
+__device__ __forceinline__ double sq16<__half>(const uint4& raw) {
+  double s = 0.0;
+  const __half* h = reinterpret_cast<const __half*>(&raw);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const double x = static_cast<double>(__half2float(h[e]));
+    s = fma(x, x, s);
+  }
+  return s;
 }
 
-// grid = (ceil(cols / (kGroups*32*V)), tile rows); block = 256.
+struct NormJob {
+  int64_t rows, cols;          // matrix extent (elements)
+  double* out;                 // output map
+  int64_t out_rs, out_cs;      // out[it*rs + kt*cs]
+  int64_t r0, nrow;            // tile rows [r0, r0+nrow)
+  int64_t ncb;                 // CTAs along the columns
+};
+
+// grid = (max ncb, nrowA + nrowB); blockIdx.y < nrowA -> job A else job B.
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) tile_norms_kernel(const T* __restrict__ X, int64_t rows,
-                                                                  int64_t cols, int64_t ld,
-                                                                  double* __restrict__ out, int64_t out_rs,
-                                                                  int64_t out_cs, int64_t tile_row0) {
-  constexpr int V = 16 / sizeof(T);   // elements per lane-load
-  constexpr int LPT = kTile / V;      // lanes per tile
-  constexpr int TPG = 32 / LPT;       // tiles per warp group (= V)
-  __shared__ double part[kWarps][kGroups * TPG];
+__global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                              const __grid_constant__ CUtensorMap tmB, NormJob ja,
+                                                              NormJob jb) {
+  constexpr int V = 16 / sizeof(T);              // elements per 16-byte lane load
+  constexpr int kCols = kBoxBytesRow / sizeof(T);  // columns per box
+  constexpr int LPT = 32 / V;                    // lanes per 32-column tile
+  constexpr int TPB = kCols / 32;                // tiles per box
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint8_t* ring = smem;
+  __shared__ uint64_t full[kStages];
+  __shared__ double part[4][kBoxesPerCta * TPB];
 
+  const bool isA = blockIdx.y < ja.nrow;
+  const NormJob& j = isA ? ja : jb;
+  const CUtensorMap* tm = isA ? &tmA : &tmB;
+  const int64_t it = j.r0 + (isA ? blockIdx.y : blockIdx.y - ja.nrow);
+  if (static_cast<int64_t>(blockIdx.x) >= j.ncb) return;
+  const int64_t box0 = static_cast<int64_t>(blockIdx.x) * kBoxesPerCta;
+  const int64_t nbox_total = (j.cols + kCols - 1) / kCols;
+  const int nbox = static_cast<int>(nbox_total - box0 < kBoxesPerCta ? nbox_total - box0 : kBoxesPerCta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t it = tile_row0 + blockIdx.y;
-  const int64_t col_base = static_cast<int64_t>(blockIdx.x) * kGroups * 32 * V;
-  const int64_t row0 = it * kTile + warp;
-
-#pragma unroll 2
-  for (int g = 0; g < kGroups; ++g) {
-    const int64_t c = col_base + static_cast<int64_t>(g) * 32 * V + lane * V;
-    double s = 0.0;
-    const int64_t nv64 = cols - c;
-    const int nv = nv64 <= 0 ? 0 : (nv64 >= V ? V : static_cast<int>(nv64));
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int64_t row = row0 + 8 * r;
-      if (row < rows && nv > 0) s += sq_sum_vec<T>(X + row * ld + c, nv);
-    }
-    // combine the LPT lanes of each tile (butterfly; order independent of tile position)
-#pragma unroll
-    for (int o = LPT / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((lane % LPT) == 0) part[warp][g * TPG + lane / LPT] = s;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(tm);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < kGroups * TPG; t += blockDim.x) {
-    double tot = 0.0;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < nbox && b < kStages; ++b) {
+      mbar_arrive_expect_tx(&full[b], kBoxBytes);
+      tma_load_2d(ring + b * kBoxBytes, tm, &full[b], static_cast<int32_t>((box0 + b) * kCols),
+                  static_cast<int32_t>(it * 32));
+    }
+  }
+  for (int b = 0; b < nbox; ++b) {
+    const int s = b % kStages;
+    mbar_wait(&full[s], static_cast<uint32_t>((b / kStages) & 1));
+    const uint8_t* box = ring + s * kBoxBytes;
+    double acc = 0.0;                            // this lane's 16 bytes in the warp's 8 rows
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) tot += part[w][t];
-    const int64_t kt = (col_base / kTile) + t;
-    if (kt * kTile < cols) out[it * out_rs + kt * out_cs] = sqrt(tot);
+    for (int r = 0; r < 8; ++r) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(box + (warp * 8 + r) * kBoxBytesRow + lane * 16);
+      acc += sq16<T>(raw);
+    }
+#pragma unroll
+    for (int o = LPT / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((lane % LPT) == 0) part[warp][b * TPB + lane / LPT] = acc;
+    __syncthreads();                             // everyone is done with stage s
+    if (threadIdx.x == 0 && b + kStages < nbox) {
+      mbar_arrive_expect_tx(&full[s], kBoxBytes);
+      tma_load_2d(ring + s * kBoxBytes, tm, &full[s], static_cast<int32_t>((box0 + b + kStages) * kCols),
+                  static_cast<int32_t>(it * 32));
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nbox * TPB; t += kThreads) {
+    const double tot = ((part[0][t] + part[1][t]) + part[2][t]) + part[3][t];
+    const int64_t kt = box0 * TPB + t;
+    if (kt * 32 < j.cols) j.out[it * j.out_rs + kt * j.out_cs] = sqrt(tot);
   }
 }
 
 template <typename T>
-spamm_status launch_t(const void* X, int64_t rows, int64_t cols, int64_t ld, double* out, int64_t out_rs,
-                      int64_t out_cs, int64_t r0, int64_t r1, cudaStream_t s) {
-  constexpr int V = 16 / sizeof(T);
-  const int64_t per_block = static_cast<int64_t>(kGroups) * 32 * V;
-  const int64_t gx = (cols + per_block - 1) / per_block;
-  const int64_t gy = r1 - r0;
-  if (gx <= 0 || gy <= 0) return SPAMM_OK;
-  if (gy > 65535) {
-    // chunk the tile rows over several launches (grid.y limit)
-    for (int64_t a = r0; a < r1; a += 65535) {
-      SPAMM_TRY(launch_t<T>(X, rows, cols, ld, out, out_rs, out_cs, a, a + 65535 < r1 ? a + 65535 : r1, s));
-    }
-    return SPAMM_OK;
+spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B, int64_t ldb,
+                      int64_t bj0, int64_t bj1, cudaStream_t s, CUtensorMapDataType dt) {
+  constexpr int kCols = kBoxBytesRow / sizeof(T);
+  CUtensorMap tA{}, tB{};
+  NormJob ja{p.M, p.K, p.nA, p.BK, 1, ar0, ar1 - ar0, 0};
+  // B column strip [bj0*32, bj1*32): treated as a (K x cols) matrix; tile row k, tile col j -> nBt[j*BK + k]
+  const int64_t bcols = std::min<int64_t>(p.N, bj1 * kTile) - bj0 * kTile;
+  NormJob jb{p.K, bcols > 0 ? bcols : 0, p.nBt + bj0 * p.BK, 1, p.BK, 0, bj1 > bj0 ? p.BK : 0, 0};
+  const int64_t per_cta = static_cast<int64_t>(kBoxesPerCta) * kCols;
+  ja.ncb = ja.nrow > 0 ? (ja.cols + per_cta - 1) / per_cta : 0;
+  jb.ncb = jb.nrow > 0 ? (jb.cols + per_cta - 1) / per_cta : 0;
+  if (ja.nrow > 0)
+    SPAMM_TRY(encode_tmap_2d(&tA, dt, sizeof(T), A, p.K, p.M, lda, kCols, 32, CU_TENSOR_MAP_SWIZZLE_NONE));
+  if (jb.nrow > 0) {
+    const void* Bs = static_cast<const char*>(B) + static_cast<size_t>(bj0) * kTile * sizeof(T);
+    SPAMM_TRY(encode_tmap_2d(&tB, dt, sizeof(T), Bs, bcols, p.K, ldb, kCols, 32, CU_TENSOR_MAP_SWIZZLE_NONE));
   }
+  static bool attr = false;
+  if (!attr) {
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kSmemBytes)));
+    attr = true;
+  }
+  const int64_t gx = std::max(ja.ncb, jb.ncb);
+  const int64_t gy = ja.nrow + jb.nrow;
+  if (gx <= 0 || gy <= 0) return SPAMM_OK;
+  if (gy > 65535) return fail(SPAMM_E_UNSUPPORTED, "more than 65535 tile rows in one norm launch");
   dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
-  tile_norms_kernel<T><<<grid, kWarps * 32, 0, s>>>(static_cast<const T*>(X), rows, cols, ld, out, out_rs,
-                                                    out_cs, r0);
+  tile_norms_kernel<T><<<grid, kThreads, kSmemBytes, s>>>(tA, tB, ja, jb);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
@@ -142,12 +172,15 @@ spamm_status launch_t(const void* X, int64_t rows, int64_t cols, int64_t ld, dou
 
 }  // namespace
 
-spamm_status launch_norms(const Plan& p, const void* X, int64_t rows, int64_t cols, int64_t ld, double* out,
-                          int64_t out_rs, int64_t out_cs, int64_t r0, int64_t r1, cudaStream_t s) {
+spamm_status launch_norms2(const Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B,
+                           int64_t ldb, int64_t bj0, int64_t bj1, cudaStream_t s) {
   switch (p.prec) {
-    case SPAMM_FP32: return launch_t<float>(X, rows, cols, ld, out, out_rs, out_cs, r0, r1, s);
-    case SPAMM_BF16: return launch_t<__nv_bfloat16>(X, rows, cols, ld, out, out_rs, out_cs, r0, r1, s);
-    case SPAMM_FP16: return launch_t<__half>(X, rows, cols, ld, out, out_rs, out_cs, r0, r1, s);
+    case SPAMM_FP32:
+      return launch_t<float>(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+    case SPAMM_BF16:
+      return launch_t<__nv_bfloat16>(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+    case SPAMM_FP16:
+      return launch_t<__half>(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
   }
   return fail(SPAMM_E_UNSUPPORTED, "precision");
 }

@@ -159,7 +159,9 @@ def test_macro_lists_match_oracle(sp):
         A = _rounded(synth.perturbed_decay_matrix(K, 0.95, seed=21, m=M), prec)
         B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=22, m=K), prec)
         nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
-        tau = float(np.median(nA[:, :, None] * nB[None, :, :]))
+        prods = np.unique(nA[:, :, None] * nB[None, :, :])
+        mid = len(prods) // 2
+        tau = float(0.5 * (prods[mid] + prods[mid + 1]))   # in a gap: no product in the tie band
         plan, _ = _run(sp, A, B, tau, prec)
         start, count, ent, order, GM, GN = sp.spamm_get_macro(plan.handle)
         start, count, ent = start.cpu().numpy(), count.cpu().numpy(), ent.cpu().numpy()
