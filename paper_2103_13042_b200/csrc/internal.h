@@ -41,6 +41,7 @@ struct Plan {
   int64_t* macro_ptr = nullptr;  // [GM*GN + 1]
   int64_t* row_work = nullptr;   // [BM + BK + 2]: row work, then the U histogram (one memset)
   unsigned int* ticket = nullptr; // CTA-completion ticket of the count kernel (self-resetting)
+  unsigned int* sched = nullptr;  // dynamic tile counter of the multiply kernels (reset per launch)
   uint16_t* leaf_k = nullptr;    // [leaf_cap]
   uint2* macro_ent = nullptr;    // [macro_cap] (k, mask)
   uint4* macro_run = nullptr;    // [macro_cap] tensor path: k|nruns|cols, packed MMA runs

@@ -26,6 +26,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -43,8 +44,12 @@ constexpr int kBBytes = 8 * kBBoxBytes;         // 16 KB per k-step
 constexpr int kThreads = 256;
 constexpr int kCStageBytes = 32 * 32 * 4;       // one 32x32 FP32 C box (SWIZZLE_128B); 2 per epilogue warp
 constexpr size_t kRingBytes = static_cast<size_t>(kStages) * kPer * (kABytes + kBBytes);
-constexpr size_t kSmemBytes = 1024 + kRingBytes + 8 * kCStageBytes + 1024;   // 2 CTAs per SM
+constexpr size_t kSmemBytes = 1024 + kRingBytes + 8 * kCStageBytes + 1280;   // 2 CTAs per SM
 constexpr uint32_t kTmemCols = 256;             // one 128x256 FP32 accumulator per CTA (2 CTAs per SM)
+
+// run word of a k-step whose 4 x 8 keep bits are all set: j0 = 0, len = 8, pattern 1111
+constexpr uint32_t kFullRun = 0u | (7u << 3) | (15u << 6);
+constexpr int kTQ = 4;   // tile ring depth (dynamic LPT scheduling)
 
 __device__ __forceinline__ int64_t snake(int64_t r, int G, int b) { return r * G + ((r & 1) ? (G - 1 - b) : b); }
 
@@ -75,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                           const __grid_constant__ CUtensorMap tC, int use3d, int dbg_mode,
                           const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN,
-                          unsigned long long* __restrict__ prof) {
+                          unsigned int* __restrict__ sched, unsigned long long* __restrict__ prof) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                           // [stage][slot] 8 KB
@@ -88,7 +93,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint4* srun = reinterpret_cast<uint4*>(tempty + 2);           // [stage][slot]: pre-decoded runs
   uint32_t* scount = reinterpret_cast<uint32_t*>(srun + kStages * kPer);   // k-steps in the stage
   uint4* sent = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(scount + kStages) + 15) & ~uintptr_t(15));
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sent + 32);
+  TileInfo* tq = reinterpret_cast<TileInfo*>(sent + 32);       // [kTQ] tiles claimed by the producer
+  uint64_t* tq_full = reinterpret_cast<uint64_t*>(tq + kTQ);
+  uint64_t* tq_empty = tq_full + kTQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + kTQ);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -98,6 +106,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     mbar_init(&tfull[0], 1);
     mbar_init(&tempty[0], 4);
+    for (int q = 0; q < kTQ; ++q) {
+      mbar_init(&tq_full[q], 1);
+      mbar_init(&tq_empty[q], 5);   // MMA thread + 4 epilogue warps
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -105,7 +117,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const int G = gridDim.x, b = blockIdx.x;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -125,10 +136,35 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t ph = 0;
     unsigned long long p_load = 0, p_wait = 0;
     const unsigned long long p_t0 = clock64();
-    TileInfo nxt = tile_info(order, mstart, mcount, snake(0, G, b), n_tiles);
-    for (int64_t r = 0; nxt.t >= 0; ++r) {
+    // Dynamic LPT scheduling: tiles are claimed in global order (descending work) from an
+    // atomic counter, one tile ahead, and published to the MMA / epilogue roles via tq[].
+    int tq_s = 0;
+    uint32_t tq_ph = 0;
+    TileInfo nxt;
+    {
+      unsigned int idx = 0;
+      if (lane == 0) idx = atomicAdd(sched, 1u);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      nxt = tile_info(order, mstart, mcount, idx, n_tiles);
+    }
+    for (;;) {
       const TileInfo cur = nxt;
-      nxt = tile_info(order, mstart, mcount, snake(r + 1, G, b), n_tiles);   // prefetch
+      if (cur.t >= 0) {
+        unsigned int idx = 0;
+        if (lane == 0) idx = atomicAdd(sched, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        nxt = tile_info(order, mstart, mcount, idx, n_tiles);   // consumed next iteration
+      }
+      if (lane == 0) {
+        mbar_wait(&tq_empty[tq_s], tq_ph ^ 1);
+        tq[tq_s] = cur;
+        mbar_arrive(&tq_full[tq_s]);
+      }
+      if (++tq_s == kTQ) {
+        tq_s = 0;
+        tq_ph ^= 1;
+      }
+      if (cur.t < 0) break;
       const int32_t I = static_cast<int32_t>(cur.t / GN), J = static_cast<int32_t>(cur.t % GN);
       for (int64_t eb = cur.e0; eb < cur.e1; eb += 32) {
         const int cnt = static_cast<int>(cur.e1 - eb < 32 ? cur.e1 - eb : 32);
@@ -142,6 +178,34 @@ __global__ void __launch_bounds__(kThreads, 2)
             unsigned long long tw0 = prof ? clock64() : 0;
             mbar_wait(&empty[s], ph ^ 1);
             if (prof) p_wait += clock64() - tw0;
+            if (kPer == 1 && use3d && dbg_mode == 0) {
+              // lean path: one k-step per stage
+              const uint4 en = sent[q0];
+              srun[s] = en;
+              const uint32_t cols = en.x >> 24;
+              const int32_t k0 = static_cast<int32_t>(en.x & 0xFFFFu) * 32;
+              uint8_t* adst = sA + s * kABytes;
+              uint8_t* bdst = sB + s * kBBytes;
+              const int jb = J * 8;
+              if (cols == 0xFFu) {
+                mbar_arrive_expect_tx(&full[s], kABytes + kBBytes);
+                tma_load_2d(adst, &tA, &full[s], k0, I * 128);
+                tma_load_3d(bdst, &tB8, &full[s], 0, k0, jb);
+              } else {
+                const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
+                int off = c0;
+                mbar_arrive_expect_tx(&full[s], kABytes + kBBoxBytes * len);
+                tma_load_2d(adst, &tA, &full[s], k0, I * 128);
+                if (len & 4) { tma_load_3d(bdst + off * kBBoxBytes, &tB4, &full[s], 0, k0, jb + off); off += 4; }
+                if (len & 2) { tma_load_3d(bdst + off * kBBoxBytes, &tB2, &full[s], 0, k0, jb + off); off += 2; }
+                if (len & 1) { tma_load_3d(bdst + off * kBBoxBytes, &tB1, &full[s], 0, k0, jb + off); }
+              }
+              if (++s == kStages) {
+                s = 0;
+                ph ^= 1;
+              }
+              continue;
+            }
             uint32_t bytes = 0;
             for (int q = 0; q < nq; ++q) {
               const uint32_t cols = sent[q0 + q].x >> 24;
@@ -204,10 +268,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       uint32_t ph = 0;
       int64_t it = 0;
       unsigned long long m_te = 0, m_fu = 0;
-      TileInfo nxt = tile_info(order, mstart, mcount, snake(0, G, b), n_tiles);
-      for (int64_t r = 0; nxt.t >= 0; ++r, ++it) {
-        const TileInfo cur = nxt;
-        nxt = tile_info(order, mstart, mcount, snake(r + 1, G, b), n_tiles);
+      int tq_s = 0;
+      uint32_t tq_ph = 0;
+      for (;; ++it) {
+        mbar_wait(&tq_full[tq_s], tq_ph);
+        const TileInfo cur = tq[tq_s];
+        mbar_arrive(&tq_empty[tq_s]);
+        if (++tq_s == kTQ) {
+          tq_s = 0;
+          tq_ph ^= 1;
+        }
+        if (cur.t < 0) break;
         const int buf = 0;
         unsigned long long tw0 = prof ? clock64() : 0;
         mbar_wait(&tempty[0], static_cast<uint32_t>(it & 1));
@@ -221,7 +292,25 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (prof) m_fu += clock64() - tf0;
           tc_fence_after();
           uint32_t nq;
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nq) : "r"(scount_addr + s * 4));
+          if (kPer == 1) {
+            uint4 rs;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(rs.x), "=r"(rs.y), "=r"(rs.z), "=r"(rs.w)
+                         : "r"(srun_addr + s * 16));
+            if (((rs.x >> 16) & 15u) == 1u && rs.y == kFullRun && dbg_mode == 0) {
+              // full 4 x 8 keep mask: two N=256 MMAs, no lane mask
+              constexpr uint32_t idesc_full = idesc_base | (8u << 19);
+              const uint64_t ad0 = smem_desc(a_addr0 + s * kABytes, 16, 512, kLayoutSW64);
+              const uint64_t bd0 = smem_desc(b_addr0 + s * kBBytes, kBBoxBytes, 512, kLayoutSW64);
+              umma_f16(dcol, ad0, bd0, idesc_full, 1u, 0u, 0u, 0u, 0u);
+              umma_f16(dcol, ad0 + (32 >> 4), bd0 + (1024 >> 4), idesc_full, 1u, 0u, 0u, 0u, 0u);
+              nq = 0;
+            } else {
+              nq = 1;
+            }
+          } else {
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nq) : "r"(scount_addr + s * 4));
+          }
           for (uint32_t q = 0; q < nq; ++q) {
             uint4 rs;
             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -272,10 +361,18 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0) mbar_arrive(&tempty[0]);
     int64_t it = 0;
     unsigned long long e_w = 0, e_d = 0;
-    TileInfo nxt = tile_info(order, mstart, mcount, snake(0, G, b), n_tiles);
-    for (int64_t r = 0; nxt.t >= 0; ++r, ++it) {
-      const TileInfo cur = nxt;
-      nxt = tile_info(order, mstart, mcount, snake(r + 1, G, b), n_tiles);
+    int tq_s = 0;
+    uint32_t tq_ph = 0;
+    for (;; ++it) {
+      mbar_wait(&tq_full[tq_s], tq_ph);
+      const TileInfo cur = tq[tq_s];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tq_empty[tq_s]);
+      if (++tq_s == kTQ) {
+        tq_s = 0;
+        tq_ph ^= 1;
+      }
+      if (cur.t < 0) break;
       const int64_t I = cur.t / GN, J = cur.t % GN;
       const int buf = 0;
       unsigned long long te0 = prof ? clock64() : 0;
@@ -366,9 +463,10 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
     cudaMalloc(&prof, 296 * 16 * 8);
   }
   if (prof) cudaMemsetAsync(prof, 0, 296 * 16 * 8, s);
+  SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
   spamm_mul_umma_kernel<kFmt><<<grid, kThreads, kSmemBytes, s>>>(tA, tB, tB8, tB4, tB2, tB1, tC, use3d, dbg_mode,
                                                                  p.mstart, p.U, p.macro_run, p.order, n_tiles, p.GN,
-                                                                 prof);
+                                                                 p.sched, prof);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (prof) {
@@ -376,8 +474,13 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
     cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     double acc[16] = {0};
-    for (int c = 0; c < grid; ++c)
+    double mn = 1e30, mx = 0;
+    for (int c = 0; c < grid; ++c) {
       for (int k = 0; k < 16; ++k) acc[k] += static_cast<double>(h[c * 16 + k]) / grid;
+      mn = std::min(mn, static_cast<double>(h[c * 16 + 6]));
+      mx = std::max(mx, static_cast<double>(h[c * 16 + 6]));
+    }
+    fprintf(stderr, "[umma prof] per-CTA MMA-thread cycles: min %.0f max %.0f mean %.0f\n", mn, mx, acc[6]);
     fprintf(stderr,
             "[umma prof] mean cycles/CTA: total %.0f | producer batch-load %.0f empty-wait %.0f | mma tempty-wait %.0f "
             "full-wait %.0f | epi tfull-wait %.0f drain %.0f\n",
