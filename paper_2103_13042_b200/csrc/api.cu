@@ -109,6 +109,7 @@ static void free_plan(Plan* p) {
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->mstart && p->mstart != p->macro_ptr) cudaFree(p->mstart);
+  if (p->Uw && p->Uw != p->U) cudaFree(p->Uw);
   if (p->h_totals) cudaFreeHost(p->h_totals);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
@@ -250,6 +251,13 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     } else {
       p->mstart = p->macro_ptr;
     }
+  }
+  if (st == SPAMM_OK) {
+    p->umma_variant = umma_variant_from_env();
+    if (p->fixed_regions && prec != SPAMM_FP32 && umma_variant_wide(p->umma_variant))
+      st = alloc(reinterpret_cast<void**>(&p->Uw), sizeof(int64_t) * static_cast<size_t>(nmac + 1));
+    else
+      p->Uw = p->U;
   }
   if (st == SPAMM_OK && cudaMallocHost(reinterpret_cast<void**>(&p->h_totals), 2 * sizeof(int64_t)) != cudaSuccess)
     st = fail(SPAMM_E_NOMEM, "cudaMallocHost failed");

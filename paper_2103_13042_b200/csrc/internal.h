@@ -49,6 +49,8 @@ struct Plan {
   int64_t* hist = nullptr;       // = row_work + BM: [BK+2] histogram of macro union counts
   int64_t* totals = nullptr;     // = hist + BK + 2: [0] kept pairs, [1] macro entries
   int64_t* mstart = nullptr;     // [GM*GN] start of each macro-tile's entries (t*BK or macro_ptr)
+  int umma_variant = 0;          // tensor-path kernel configuration (multiply_umma.cu)
+  int64_t* Uw = nullptr;         // [GM*GN] tensor-path entries per macro-tile (pairs merged) or = U
   bool fixed_regions = false;    // lists stored in worst-case fixed regions (single-pass skip map)
   int64_t* bucket_pos = nullptr; // [BK+2] descending bucket starts (consumed by emit)
   void* cub_tmp = nullptr;
@@ -97,6 +99,8 @@ spamm_status launch_skipmap_emit(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t
 spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);
 spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
+int umma_variant_from_env();       // SPAMM_UMMA_VARIANT: 0 = 2 CTAs/SM 32-deep, 1 = 2 CTAs/SM 64-deep, 2 = 1 CTA/SM 64-deep
+bool umma_variant_wide(int v);     // does the variant consume merged 64-deep k-steps?
 spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 

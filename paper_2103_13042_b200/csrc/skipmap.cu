@@ -238,7 +238,8 @@ __device__ __forceinline__ uint32_t col_pattern8(uint32_t mask, int lj) {
   return ((mask >> lj) & 1u) | (((mask >> (8 + lj)) & 1u) << 1) | (((mask >> (16 + lj)) & 1u) << 2) |
          (((mask >> (24 + lj)) & 1u) << 3);
 }
-__device__ __forceinline__ uint4 encode_runs(uint32_t k, uint32_t mask) {
+// .w bit 31: width-2 entry (k-tiles k and k+1 share the mask; one 64-deep k-step)
+__device__ __forceinline__ uint4 encode_runs(uint32_t k, uint32_t mask, uint32_t wide = 0u) {
   uint32_t words[3] = {0u, 0u, 0u};
   uint32_t nr = 0, cols = 0;
   int j = 0;
@@ -254,7 +255,7 @@ __device__ __forceinline__ uint4 encode_runs(uint32_t k, uint32_t mask) {
     }
     j = j1;
   }
-  return make_uint4(k | (nr << 16) | (cols << 24), words[0], words[1], words[2]);
+  return make_uint4(k | (nr << 16) | (cols << 24), words[0], words[1], words[2] | (wide << 31));
 }
 
 template <int MI, int MJ>
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                       int64_t* __restrict__ U, int64_t* __restrict__ Lm, unsigned long long* __restrict__ row_work,
                       unsigned long long* __restrict__ hist, int64_t* __restrict__ leaf_start,
                       uint16_t* __restrict__ leaf_k, uint2* __restrict__ macro_ent, uint4* __restrict__ macro_run,
-                      LastArgs la) {
+                      int64_t* __restrict__ Uw, int merge_ok, LastArgs la) {
   constexpr int NB = MI * MJ;
   __shared__ int64_t s_warp[33];
   __shared__ int s_last;
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int64_t lstart = vl ? leaf * BK : 0;
     int64_t lbase = lstart;                 // lane b: running write offset of C tile b
     int64_t mbase = tile * BK;              // macro-tile region
+    int64_t wbase = tile * BK;              // tensor-path entries (aligned equal-mask k pairs merged)
     const uint32_t lt = (1u << lane) - 1u;
     ChunkVals<MI, MJ> cur = load_chunk<MI, MJ>(nA, nBt, BM, BK, BN, I, J, lane);
     for (int64_t kc = 0; kc < BK; kc += 32) {
@@ -390,12 +392,20 @@ __global__ void __launch_bounds__(kWarps * 32)
       cur = nxt;
       const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
       if (any == 0u) continue;
-      if (mask) {
-        const int64_t e = mbase + __popc(any & lt);
-        macro_ent[e] = make_uint2(static_cast<uint32_t>(k), mask);
-        if (MJ == 8 && macro_run != nullptr) macro_run[e] = encode_runs(static_cast<uint32_t>(k), mask);
-      }
+      if (mask) macro_ent[mbase + __popc(any & lt)] = make_uint2(static_cast<uint32_t>(k), mask);
       mbase += __popc(any);
+      if (MJ == 8 && macro_run != nullptr) {
+        // k-tiles 2p and 2p+1 with the same non-zero mask become one 64-deep k-step
+        const uint32_t mnext = __shfl_down_sync(0xffffffffu, mask, 1);
+        const uint32_t mprev = __shfl_up_sync(0xffffffffu, mask, 1);
+        const bool even = (lane & 1) == 0;
+        const bool wide = merge_ok && even && mask != 0u && mnext == mask;
+        const bool absorbed = merge_ok && !even && mask != 0u && mprev == mask;
+        const bool emit = mask != 0u && !absorbed;
+        const uint32_t bal = __ballot_sync(0xffffffffu, emit);
+        if (emit) macro_run[wbase + __popc(bal & lt)] = encode_runs(static_cast<uint32_t>(k), mask, wide ? 1u : 0u);
+        wbase += __popc(bal);
+      }
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const bool bit = (mask >> b) & 1u;
@@ -426,6 +436,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     if (lane == 0) {
       Lm[tile] = lsum;
       U[tile] = u;
+      if (Uw != nullptr) Uw[tile] = wbase - tile * BK;
       atomicAdd(hist + u, 1ull);
     }
   }
@@ -450,7 +461,8 @@ spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   skip_fused_kernel<kMacroI, MJ><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
       p.nA, p.nBt, p.BM, p.BK, p.BN, p.tau, p.GN, gi0, n_macro, p.V, p.U, p.L,
       reinterpret_cast<unsigned long long*>(p.row_work), reinterpret_cast<unsigned long long*>(p.hist),
-      p.leaf_start, p.leaf_k, p.macro_ent, p.macro_run, la);
+      p.leaf_start, p.leaf_k, p.macro_ent, p.macro_run, p.Uw != p.U ? p.Uw : nullptr,
+      static_cast<int>(p.Uw != p.U && p.N % 32 == 0), la);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;

@@ -33,7 +33,7 @@ def test_sm100a_only_cubin(sp):
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", sp.LIB_PATH], capture_output=True,
                           text=True).stdout
     # tcgen05 MMA, TMEM load/store and TMA are present in the product library
-    for mnemonic in ("UTCHMMA", "LDTM", "STTM", "UTMALDG"):
+    for mnemonic in ("UTCHMMA", "UTCBAR", "LDTM", "UTMALDG"):
         assert mnemonic in sass, mnemonic
 
 
