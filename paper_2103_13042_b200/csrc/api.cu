@@ -323,9 +323,11 @@ spamm_status do_skipmap(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   if (!p.norms_ready) return fail(SPAMM_E_STATE, "spamm_build_skipmap before spamm_norms");
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
+  p.leaf_ready = false;
   if (p.fixed_regions) {
     SPAMM_TRY(launch_skipmap_fused(p, gi0, gi1, s));
   } else {
+    p.leaf_ready = true;   // the emit pass writes the per-C-tile lists itself
     SPAMM_TRY(launch_skipmap_count(p, gi0, gi1, s));
     if (p.leaf_cap < p.BM * p.BN * p.BK) {
       // exact sizing: one stream synchronisation
@@ -410,11 +412,22 @@ spamm_status spamm_get_norms(spamm_plan_t h, const double** dA, const double** d
   return p.norms_ready ? SPAMM_OK : fail(SPAMM_E_STATE, "norms not computed");
 }
 
+// The fused skip-map pass writes the macro-level lists only; the per-C-tile view is
+// expanded from them on first request (same stream, then synchronised).
+static spamm_status ensure_leaf_lists(spamm::Plan& p) {
+  if (p.leaf_ready) return SPAMM_OK;
+  SPAMM_TRY(launch_leaf_expand(p, p.last_stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
+  p.leaf_ready = true;
+  return SPAMM_OK;
+}
+
 spamm_status spamm_get_skipmap(spamm_plan_t h, const int64_t** d_tile_start, const uint16_t** d_k_idx,
                                int64_t* kept) {
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
   if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
+  SPAMM_TRY(ensure_leaf_lists(p));
   if (d_tile_start) *d_tile_start = p.leaf_start;
   if (d_k_idx) *d_k_idx = p.leaf_k;
   if (kept) {
@@ -428,6 +441,7 @@ spamm_status spamm_get_counts(spamm_plan_t h, const int64_t** d_V, const int64_t
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
   if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
+  if (d_V) SPAMM_TRY(ensure_leaf_lists(p));
   if (d_V) *d_V = p.V;
   if (d_row_work) *d_row_work = p.row_work;
   return SPAMM_OK;

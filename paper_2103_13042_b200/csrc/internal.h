@@ -62,6 +62,7 @@ struct Plan {
   // state
   bool norms_ready = false;
   bool skipmap_ready = false;
+  bool leaf_ready = false;       // per-C-tile lists (V, leaf_start, leaf_k) materialised
   int64_t row_begin_macro = 0, row_end_macro = 0;   // macro-row range the skip map / multiply covers
   std::vector<int64_t> last_partition;
   cudaStream_t last_stream = nullptr;
@@ -99,6 +100,7 @@ spamm_status launch_skipmap_emit(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t
 spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s);
 spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
+spamm_status launch_leaf_expand(Plan& p, cudaStream_t s);   // per-C-tile lists from macro lists
 int umma_variant_from_env();       // SPAMM_UMMA_VARIANT: 0 = 2 CTAs/SM 32-deep, 1 = 2 CTAs/SM 64-deep, 2 = 1 CTA/SM 64-deep
 bool umma_variant_wide(int v);     // does the variant consume merged 64-deep k-steps?
 spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,

@@ -23,6 +23,10 @@
 // All passes evaluate the identical predicate code, so lists match counts exactly.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace spamm {
@@ -334,18 +338,44 @@ struct LastArgs {
   int64_t t0, t1;        // macro-tiles of the range [t0, t1)
   int64_t* totals;       // [0] kept pairs, [1] macro entries
   unsigned int* ticket;
+  unsigned long long* tstamp;   // debug (SPAMM_DEBUG_SKIP_PROF): [0] first CTA start, [1] last CTA enter, [2] exit
 };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  return g;
+}
 
-__device__ void last_cta_order(const LastArgs& la, int64_t* s_warp) {
+// Bucket starts live in shared memory when they fit (atomics there are ~10x cheaper than
+// global ones, and this loop is the serial tail of the launch).
+constexpr int kSmemBuckets = 2048;
+__device__ void last_cta_order(const LastArgs& la, int64_t* s_warp, unsigned long long* s_pos) {
   block_scan_array(la.hist, la.bucket_pos, la.nbucket, true, s_warp);
   __syncthreads();
+  const bool in_smem = la.nbucket <= kSmemBuckets;
+  unsigned long long* pos = in_smem ? s_pos : reinterpret_cast<unsigned long long*>(la.bucket_pos);
+  if (in_smem)
+    for (int64_t b = threadIdx.x; b < la.nbucket; b += blockDim.x) s_pos[b] = static_cast<unsigned long long>(la.bucket_pos[b]);
+  __syncthreads();
+  constexpr int R = 8;   // independent loads / atomics in flight per thread
   int64_t kept = 0, ents = 0;
-  for (int64_t t = la.t0 + threadIdx.x; t < la.t1; t += blockDim.x) {
-    const int64_t u = la.U[t];
-    const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(la.bucket_pos) + u, 1ull);
-    la.order[slot] = static_cast<int32_t>(t);
-    kept += la.L[t];
-    ents += u;
+  for (int64_t base = la.t0; base < la.t1; base += static_cast<int64_t>(blockDim.x) * R) {
+    int64_t u[R], l[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+      u[r] = t < la.t1 ? la.U[t] : -1;
+      l[r] = t < la.t1 ? la.L[t] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (u[r] < 0) continue;
+      const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+      const unsigned long long slot = atomicAdd(pos + u[r], 1ull);
+      la.order[slot] = static_cast<int32_t>(t);
+      kept += l[r];
+      ents += u[r];
+    }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -358,87 +388,161 @@ __device__ void last_cta_order(const LastArgs& la, int64_t* s_warp) {
   }
 }
 
+// One CTA per macro-tile: warp w evaluates k = kb + 32 w + lane of each 256-wide k block,
+// so a macro-tile's MI x MJ x 256 keep bits are decided by 256 threads at once.  Per-warp
+// counts (k-steps, tensor-path entries) are scanned across the 8 warps in shared memory,
+// then every warp writes its part of the ascending macro lists.  Only the macro-level
+// lists -- (k, keep mask) per k-step, which hold every keep bit -- are written here; the
+// per-C-tile k lists are expanded from them on request (leaf_expand_kernel).  Row work
+// and kept-pair counts are popcounts of the masks.
+constexpr int kFusedWarps = 8;
+constexpr int kKB = 32 * kFusedWarps;   // k per block: thread (w, lane) owns k = kb + 32 w + lane
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 template <int MI, int MJ>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kFusedWarps * 32, 4)
     skip_fused_kernel(const double* __restrict__ nA, const double* __restrict__ nBt, int64_t BM, int64_t BK,
-                      int64_t BN, double tau, int64_t GN, int64_t gi0, int64_t n_macro, int64_t* __restrict__ V,
-                      int64_t* __restrict__ U, int64_t* __restrict__ Lm, unsigned long long* __restrict__ row_work,
-                      unsigned long long* __restrict__ hist, int64_t* __restrict__ leaf_start,
-                      uint16_t* __restrict__ leaf_k, uint2* __restrict__ macro_ent, uint4* __restrict__ macro_run,
-                      int64_t* __restrict__ Uw, int merge_ok, LastArgs la) {
-  constexpr int NB = MI * MJ;
+                      int64_t BN, double tau, int64_t GN, int64_t gi0, int64_t n_macro, int64_t* __restrict__ U,
+                      int64_t* __restrict__ Lm, unsigned long long* __restrict__ row_work,
+                      unsigned long long* __restrict__ hist, uint2* __restrict__ macro_ent,
+                      uint4* __restrict__ macro_run, int64_t* __restrict__ Uw, int merge_ok, LastArgs la) {
+  constexpr int W = kFusedWarps;
+  constexpr int R = MI + MJ;              // norm rows per macro-tile: MI of A, MJ of B^T
+  __shared__ uint32_t s_cm[W], s_cr[W], s_rw[W][MI];
   __shared__ int64_t s_warp[33];
   __shared__ int s_last;
-  const int lane = threadIdx.x & 31;
-  const int64_t m = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
-  if (m < n_macro) {
+  // dynamic: each thread's own norm column, double-buffered [2][R][kKB]; reused by the
+  // last CTA for the bucket positions (kSmemBuckets <= 2 * R * kKB)
+  extern __shared__ double s_dyn[];
+  double(*s_val)[R][kKB] = reinterpret_cast<double(*)[R][kKB]>(s_dyn);
+  unsigned long long* s_pos = reinterpret_cast<unsigned long long*>(s_dyn);
+  static_assert(kSmemBuckets <= 2 * R * kKB, "bucket array must fit the staging buffer");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = threadIdx.x;
+  if (la.tstamp && threadIdx.x == 0) atomicMin(la.tstamp, gtimer());
+  // stage the norms of unit (macro-tile mm, k block kk) for this thread's column
+  auto stage = [&](int64_t mm, int64_t kk, int buf) {
+    if (mm < n_macro) {
+      const int64_t I = gi0 + mm / GN, J = mm % GN;
+      const int64_t k = kk + col;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool isA = r < MI;
+        const int64_t row = isA ? I * MI + r : J * MJ + (r - MI);
+        const bool ok = k < BK && row < (isA ? BM : BN);
+        if (ok)
+          cp_async8(&s_val[buf][r][col], (isA ? nA : nBt) + row * BK + k);
+        else
+          s_val[buf][r][col] = 0.0;   // out of range loads as 0 and is masked by index
+      }
+    }
+    cp_async_commit();
+  };
+  // Persistent CTAs walk (macro-tile, k block) units; the next unit's norms are in flight
+  // while the current one is decided.
+  int64_t m = blockIdx.x, kb = 0;
+  int buf = 0;
+  stage(m, kb, 0);
+  int64_t mbase = 0, wbase = 0;
+  uint32_t rw[MI];
+  const uint32_t lt = (1u << lane) - 1u;
+  while (m < n_macro) {
+    int64_t nm = m, nk = kb + kKB;
+    if (nk >= BK) {
+      nm = m + gridDim.x;
+      nk = 0;
+    }
+    stage(nm, nk, buf ^ 1);
+    cp_async_wait1();
     const int64_t I = gi0 + m / GN, J = m % GN;
     const int64_t tile = I * GN + J;
     const uint32_t valid = valid_bits<MI, MJ>(BM, BN, I, J);
-    const int li = lane / MJ, lj = lane % MJ;
-    const bool vl = lane < NB && ((valid >> lane) & 1u);
-    const int64_t leaf = (I * MI + li) * BN + (J * MJ + lj);
-    const int64_t lstart = vl ? leaf * BK : 0;
-    int64_t lbase = lstart;                 // lane b: running write offset of C tile b
-    int64_t mbase = tile * BK;              // macro-tile region
-    int64_t wbase = tile * BK;              // tensor-path entries (aligned equal-mask k pairs merged)
-    const uint32_t lt = (1u << lane) - 1u;
-    ChunkVals<MI, MJ> cur = load_chunk<MI, MJ>(nA, nBt, BM, BK, BN, I, J, lane);
-    for (int64_t kc = 0; kc < BK; kc += 32) {
-      ChunkVals<MI, MJ> nxt = cur;
-      if (kc + 32 < BK) nxt = load_chunk<MI, MJ>(nA, nBt, BM, BK, BN, I, J, kc + 32 + lane);   // prefetch
-      const int64_t k = kc + lane;
-      const uint32_t mask = chunk_mask<MI, MJ>(cur, valid, tau);
-      cur = nxt;
-      const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
-      if (any == 0u) continue;
-      if (mask) macro_ent[mbase + __popc(any & lt)] = make_uint2(static_cast<uint32_t>(k), mask);
-      mbase += __popc(any);
-      if (MJ == 8 && macro_run != nullptr) {
-        // k-tiles 2p and 2p+1 with the same non-zero mask become one 64-deep k-step
-        const uint32_t mnext = __shfl_down_sync(0xffffffffu, mask, 1);
-        const uint32_t mprev = __shfl_up_sync(0xffffffffu, mask, 1);
-        const bool even = (lane & 1) == 0;
-        const bool wide = merge_ok && even && mask != 0u && mnext == mask;
-        const bool absorbed = merge_ok && !even && mask != 0u && mprev == mask;
-        const bool emit = mask != 0u && !absorbed;
-        const uint32_t bal = __ballot_sync(0xffffffffu, emit);
-        if (emit) macro_run[wbase + __popc(bal & lt)] = encode_runs(static_cast<uint32_t>(k), mask, wide ? 1u : 0u);
-        wbase += __popc(bal);
-      }
+    if (kb == 0) {
+      mbase = tile * BK;                    // macro-tile region
+      wbase = tile * BK;                    // tensor-path entries (aligned equal-mask k pairs merged)
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const bool bit = (mask >> b) & 1u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-        if (bal == 0u) continue;
-        const int64_t base = __shfl_sync(0xffffffffu, lbase, b);
-        if (bit) leaf_k[base + __popc(bal & lt)] = static_cast<uint16_t>(k);
-        if (lane == b) lbase += __popc(bal);
-      }
+      for (int li = 0; li < MI; ++li) rw[li] = 0u;
     }
-    const uint32_t my = static_cast<uint32_t>(lbase - lstart);
-    const uint32_t u = static_cast<uint32_t>(mbase - tile * BK);
-    if (vl) {
-      V[leaf] = my;
-      leaf_start[leaf] = lstart;
-    }
-    uint32_t rs = vl ? my : 0u;   // row work: sum over the MJ lanes of each tile row
+    const int64_t k = kb + col;
+    ChunkVals<MI, MJ> cv;
+    cv.kin = k < BK;
 #pragma unroll
-    for (int o = 1; o < MJ; o <<= 1) {
-      const uint32_t other = __shfl_down_sync(0xffffffffu, rs, o);
-      if ((lj + o) < MJ) rs += other;
-    }
-    if (lane < NB && lj == 0 && I * MI + li < BM && rs)
-      atomicAdd(row_work + I * MI + li, static_cast<unsigned long long>(rs));
-    uint32_t lsum = vl ? my : 0u;
+    for (int li = 0; li < MI; ++li) cv.a[li] = s_val[buf][li][col];
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    for (int lj = 0; lj < MJ; ++lj) cv.b[lj] = s_val[buf][MI + lj][col];
+    const uint32_t mask = chunk_mask<MI, MJ>(cv, valid, tau);
+#pragma unroll
+    for (int li = 0; li < MI; ++li) rw[li] += __popc((mask >> (li * MJ)) & ((1u << MJ) - 1u));
+    const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
+    bool wide = false, emit = false;
+    if (MJ == 8 && macro_run != nullptr) {
+      // k-tiles 2p and 2p+1 with the same non-zero mask become one 64-deep k-step
+      const uint32_t mnext = __shfl_down_sync(0xffffffffu, mask, 1);
+      const uint32_t mprev = __shfl_up_sync(0xffffffffu, mask, 1);
+      const bool even = (lane & 1) == 0;
+      wide = merge_ok && even && mask != 0u && mnext == mask;
+      const bool absorbed = merge_ok && !even && mask != 0u && mprev == mask;
+      emit = mask != 0u && !absorbed;
+    }
+    const uint32_t bal_r = __ballot_sync(0xffffffffu, emit);
     if (lane == 0) {
-      Lm[tile] = lsum;
-      U[tile] = u;
-      if (Uw != nullptr) Uw[tile] = wbase - tile * BK;
-      atomicAdd(hist + u, 1ull);
+      s_cm[warp] = __popc(any);
+      s_cr[warp] = __popc(bal_r);
     }
+    __syncthreads();
+    uint32_t om = 0, orr = 0, tm = 0, tr = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t cm = s_cm[w], cr = s_cr[w];
+      if (w < warp) {
+        om += cm;
+        orr += cr;
+      }
+      tm += cm;
+      tr += cr;
+    }
+    if (mask) macro_ent[mbase + om + __popc(any & lt)] = make_uint2(static_cast<uint32_t>(k), mask);
+    if (emit) macro_run[wbase + orr + __popc(bal_r & lt)] = encode_runs(static_cast<uint32_t>(k), mask, wide ? 1u : 0u);
+    mbase += tm;
+    wbase += tr;
+    if (kb + kKB >= BK) {   // last k block of the macro-tile: counts
+#pragma unroll
+      for (int li = 0; li < MI; ++li) {
+        uint32_t v = rw[li];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_rw[warp][li] = v;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t r = 0;   // lane li < MI: kept pairs of tile row I*MI + li
+        if (lane < MI)
+#pragma unroll
+          for (int w = 0; w < W; ++w) r += s_rw[w][lane];
+        if (lane < MI && I * MI + lane < BM && r)
+          atomicAdd(row_work + I * MI + lane, static_cast<unsigned long long>(r));
+        uint32_t lsum = r;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        if (lane == 0) {
+          const uint32_t u = static_cast<uint32_t>(mbase - tile * BK);
+          Lm[tile] = lsum;
+          U[tile] = u;
+          if (Uw != nullptr) Uw[tile] = wbase - tile * BK;
+          atomicAdd(hist + u, 1ull);
+        }
+      }
+    }
+    __syncthreads();   // s_cm / s_cr / s_rw and this buffer are rewritten next
+    m = nm;
+    kb = nk;
+    buf ^= 1;
   }
   __threadfence();
   __syncthreads();
@@ -449,22 +553,82 @@ __global__ void __launch_bounds__(kWarps * 32)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  last_cta_order(la, s_warp);
+  asm volatile("cp.async.wait_all;" ::: "memory");   // the staging buffer becomes s_pos
+  __syncthreads();
+  if (la.tstamp && threadIdx.x == 0) la.tstamp[1] = gtimer();
+  last_cta_order(la, s_warp, s_pos);
   if (threadIdx.x == 0) *la.ticket = 0u;
+  if (la.tstamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) la.tstamp[2] = gtimer();
+  }
+}
+
+// Per-C-tile k lists (fixed regions: C tile (i,j) owns slots [(i*BN+j)*BK, +V)) expanded
+// from the macro lists: one warp per macro-tile, lane b appends the k-steps whose mask has
+// bit b -- ascending k, exactly the skip map the fused pass decided.
+template <int MI, int MJ>
+__global__ void __launch_bounds__(kWarps * 32)
+    leaf_expand_kernel(int64_t BM, int64_t BK, int64_t BN, int64_t GN, int64_t gi0, int64_t n_macro,
+                       const int64_t* __restrict__ U, const uint2* __restrict__ macro_ent, int64_t* __restrict__ V,
+                       int64_t* __restrict__ leaf_start, uint16_t* __restrict__ leaf_k) {
+  constexpr int NB = MI * MJ;
+  const int lane = threadIdx.x & 31;
+  const int64_t m = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  if (m >= n_macro) return;
+  const int64_t I = gi0 + m / GN, J = m % GN;
+  const int64_t tile = I * GN + J;
+  const uint32_t valid = valid_bits<MI, MJ>(BM, BN, I, J);
+  const int li = lane / MJ, lj = lane % MJ;
+  const bool vl = lane < NB && ((valid >> lane) & 1u);
+  const int64_t leaf = (I * MI + li) * BN + (J * MJ + lj);
+  const int64_t lstart = leaf * BK;
+  int64_t n = 0;
+  const int64_t u = U[tile];
+  for (int64_t e0 = 0; e0 < u; e0 += 32) {
+    const uint2 mine = e0 + lane < u ? macro_ent[tile * BK + e0 + lane] : make_uint2(0u, 0u);
+    const int cnt = static_cast<int>(u - e0 < 32 ? u - e0 : 32);
+    for (int q = 0; q < cnt; ++q) {
+      const uint32_t k = __shfl_sync(0xffffffffu, mine.x, q), mask = __shfl_sync(0xffffffffu, mine.y, q);
+      if (vl && ((mask >> lane) & 1u)) leaf_k[lstart + n++] = static_cast<uint16_t>(k);
+    }
+  }
+  if (vl) {
+    V[leaf] = n;
+    leaf_start[leaf] = lstart;
+  }
 }
 
 template <int MJ>
 spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   const int64_t n_macro = (gi1 - gi0) * p.GN;
-  const int64_t blocks = n_macro > 0 ? (n_macro + kWarps - 1) / kWarps : 1;
-  LastArgs la{p.hist, p.bucket_pos, p.BK + 1, p.U, p.L, p.order, gi0 * p.GN, gi1 * p.GN, p.totals, p.ticket};
-  skip_fused_kernel<kMacroI, MJ><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
-      p.nA, p.nBt, p.BM, p.BK, p.BN, p.tau, p.GN, gi0, n_macro, p.V, p.U, p.L,
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(n_macro, static_cast<int64_t>(p.num_sms) * 4));
+  static unsigned long long* tst = nullptr;
+  if (getenv("SPAMM_DEBUG_SKIP_PROF") && !tst) cudaMalloc(&tst, 64);
+  if (tst) {
+    const unsigned long long init[3] = {~0ull, 0, 0};
+    cudaMemcpyAsync(tst, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  }
+  LastArgs la{p.hist, p.bucket_pos, p.BK + 1, p.U, p.L, p.order, gi0 * p.GN, gi1 * p.GN, p.totals, p.ticket, tst};
+  constexpr int dyn = 2 * (kMacroI + MJ) * kKB * static_cast<int>(sizeof(double));
+  static bool attr = false;
+  if (!attr) {
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(skip_fused_kernel<kMacroI, MJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    attr = true;
+  }
+  skip_fused_kernel<kMacroI, MJ><<<static_cast<unsigned>(blocks), kFusedWarps * 32, dyn, s>>>(
+      p.nA, p.nBt, p.BM, p.BK, p.BN, p.tau, p.GN, gi0, n_macro, p.U, p.L,
       reinterpret_cast<unsigned long long*>(p.row_work), reinterpret_cast<unsigned long long*>(p.hist),
-      p.leaf_start, p.leaf_k, p.macro_ent, p.macro_run, p.Uw != p.U ? p.Uw : nullptr,
-      static_cast<int>(p.Uw != p.U && p.N % 32 == 0), la);
+      p.macro_ent, p.macro_run, p.Uw != p.U ? p.Uw : nullptr, static_cast<int>(p.Uw != p.U && p.N % 32 == 0), la);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
+  if (tst) {
+    unsigned long long h[3];
+    cudaMemcpyAsync(h, tst, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[skip prof] main part %.2f us, last-CTA order pass %.2f us\n", (h[1] - h[0]) * 1e-3,
+            (h[2] - h[1]) * 1e-3);
+  }
   return SPAMM_OK;
 }
 
@@ -546,6 +710,24 @@ spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_
   SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 4), s));
   if (p.MJ == kMacroJ_umma) return fused_t<kMacroJ_umma>(p, gi0, gi1, s);
   return fused_t<kMacroJ_simt>(p, gi0, gi1, s);
+}
+
+spamm_status launch_leaf_expand(Plan& p, cudaStream_t s) {
+  const int64_t gi0 = p.row_begin_macro, gi1 = p.row_end_macro;
+  const int64_t nleaf = p.BM * p.BN;
+  if (gi0 != 0 || gi1 != p.GM) SPAMM_CUDA_TRY(cudaMemsetAsync(p.V, 0, sizeof(int64_t) * (nleaf + 1), s));
+  const int64_t n_macro = (gi1 - gi0) * p.GN;
+  if (n_macro <= 0) return SPAMM_OK;
+  const int64_t blocks = (n_macro + kWarps - 1) / kWarps;
+  if (p.MJ == kMacroJ_umma)
+    leaf_expand_kernel<kMacroI, kMacroJ_umma><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
+        p.BM, p.BK, p.BN, p.GN, gi0, n_macro, p.U, p.macro_ent, p.V, p.leaf_start, p.leaf_k);
+  else
+    leaf_expand_kernel<kMacroI, kMacroJ_simt><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
+        p.BM, p.BK, p.BN, p.GN, gi0, n_macro, p.U, p.macro_ent, p.V, p.leaf_start, p.leaf_k);
+  count_launch();
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
 }
 
 spamm_status launch_skipmap_emit(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
