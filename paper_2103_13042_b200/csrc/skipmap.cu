@@ -65,14 +65,22 @@ __device__ __forceinline__ ChunkVals<MI, MJ> load_chunk(const double* __restrict
 // keep bits of one chunk: bit li*MJ+lj <=> !(a*b < tau), for in-range (i, k, j) only.
 template <int MI, int MJ>
 __device__ __forceinline__ uint32_t chunk_mask(const ChunkVals<MI, MJ>& v, uint32_t valid, double tau) {
-  // Exact pre-filter: norms are >= 0 (or NaN), rounding is monotone, so
-  // max(a) * max(b) < tau implies every a*b < tau.  NaN-propagating maxima keep NaN pairs.
-  double amax = 0.0, bmax = 0.0;
+  // Exact pre-filters: norms are >= 0 (or NaN) and rounding is monotone, so
+  //   max(a) * max(b) < tau   =>  every a*b < tau   (NaN-propagating maxima keep NaN pairs);
+  //   min(a) * min(b) >= tau  =>  every a*b >= tau  (NaN pairs are kept either way).
+  double amax = 0.0, bmax = 0.0, amin = v.a[0], bmin = v.b[0];
 #pragma unroll
-  for (int li = 0; li < MI; ++li) amax = (v.a[li] > amax || v.a[li] != v.a[li]) ? v.a[li] : amax;
+  for (int li = 0; li < MI; ++li) {
+    amax = (v.a[li] > amax || v.a[li] != v.a[li]) ? v.a[li] : amax;
+    amin = fmin(amin, v.a[li]);
+  }
 #pragma unroll
-  for (int lj = 0; lj < MJ; ++lj) bmax = (v.b[lj] > bmax || v.b[lj] != v.b[lj]) ? v.b[lj] : bmax;
+  for (int lj = 0; lj < MJ; ++lj) {
+    bmax = (v.b[lj] > bmax || v.b[lj] != v.b[lj]) ? v.b[lj] : bmax;
+    bmin = fmin(bmin, v.b[lj]);
+  }
   if (!v.kin || valid == 0u || __dmul_rn(amax, bmax) < tau) return 0u;
+  if (__dmul_rn(amin, bmin) >= tau) return valid;
   uint32_t mask = 0u;
 #pragma unroll
   for (int li = 0; li < MI; ++li)
@@ -83,7 +91,6 @@ __device__ __forceinline__ uint32_t chunk_mask(const ChunkVals<MI, MJ>& v, uint3
     }
   return mask & valid;
 }
-
 // bit li*MJ+lj set iff C tile (I*MI+li, J*MJ+lj) exists
 template <int MI, int MJ>
 __device__ __forceinline__ uint32_t valid_bits(int64_t BM, int64_t BN, int64_t I, int64_t J) {
@@ -244,6 +251,8 @@ __device__ __forceinline__ uint32_t col_pattern8(uint32_t mask, int lj) {
 }
 // .w bit 31: width-2 entry (k-tiles k and k+1 share the mask; one 64-deep k-step)
 __device__ __forceinline__ uint4 encode_runs(uint32_t k, uint32_t mask, uint32_t wide = 0u) {
+  if (mask == 0xFFFFFFFFu)   // all 4 x 8 pairs kept: one run j0 = 0, len = 8, pattern 1111
+    return make_uint4(k | (1u << 16) | (0xFFu << 24), 0u | (7u << 3) | (15u << 6), 0u, wide << 31);
   uint32_t words[3] = {0u, 0u, 0u};
   uint32_t nr = 0, cols = 0;
   int j = 0;
@@ -458,8 +467,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
       nm = m + gridDim.x;
       nk = 0;
     }
+    const long long c0 = clock64();
     stage(nm, nk, buf ^ 1);
     cp_async_wait1();
+    const long long c1 = clock64();
     const int64_t I = gi0 + m / GN, J = m % GN;
     const int64_t tile = I * GN + J;
     const uint32_t valid = valid_bits<MI, MJ>(BM, BN, I, J);
@@ -540,15 +551,25 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
       }
     }
     __syncthreads();   // s_cm / s_cr / s_rw and this buffer are rewritten next
+    if (la.tstamp && threadIdx.x == 0) {
+      atomicAdd(la.tstamp + 3, static_cast<unsigned long long>(c1 - c0));
+      atomicAdd(la.tstamp + 4, static_cast<unsigned long long>(clock64() - c1));
+      atomicAdd(la.tstamp + 5, 1ull);
+    }
     m = nm;
     kb = nk;
     buf ^= 1;
   }
+  const long long cf0 = clock64();
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int t = atomicAdd(la.ticket, 1u);
     s_last = (t == gridDim.x - 1);
+    if (la.tstamp) {
+      atomicAdd(la.tstamp + 6, static_cast<unsigned long long>(clock64() - cf0));
+      atomicMax(la.tstamp + 7, gtimer());
+    }
   }
   __syncthreads();
   if (!s_last) return;
@@ -604,9 +625,9 @@ spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   const int64_t n_macro = (gi1 - gi0) * p.GN;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(n_macro, static_cast<int64_t>(p.num_sms) * 4));
   static unsigned long long* tst = nullptr;
-  if (getenv("SPAMM_DEBUG_SKIP_PROF") && !tst) cudaMalloc(&tst, 64);
+  if (getenv("SPAMM_DEBUG_SKIP_PROF") && !tst) cudaMalloc(&tst, 128);
   if (tst) {
-    const unsigned long long init[3] = {~0ull, 0, 0};
+    const unsigned long long init[12] = {~0ull, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(tst, init, sizeof(init), cudaMemcpyHostToDevice, s);
   }
   LastArgs la{p.hist, p.bucket_pos, p.BK + 1, p.U, p.L, p.order, gi0 * p.GN, gi1 * p.GN, p.totals, p.ticket, tst};
@@ -623,11 +644,13 @@ spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (tst) {
-    unsigned long long h[3];
+    unsigned long long h[12];
     cudaMemcpyAsync(h, tst, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    fprintf(stderr, "[skip prof] main part %.2f us, last-CTA order pass %.2f us\n", (h[1] - h[0]) * 1e-3,
-            (h[2] - h[1]) * 1e-3);
+    fprintf(stderr, "[skip prof] main part %.2f us, last-CTA order pass %.2f us; per unit: wait %.0f cyc, work %.0f cyc "
+            "(%llu units); per CTA fence+ticket %.0f cyc; last ticket at +%.2f us\n", (h[1] - h[0]) * 1e-3,
+            (h[2] - h[1]) * 1e-3, double(h[3]) / h[5], double(h[4]) / h[5], h[5], double(h[6]) / blocks,
+            (h[7] - h[0]) * 1e-3);
   }
   return SPAMM_OK;
 }
