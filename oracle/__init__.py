@@ -130,7 +130,7 @@ def macro_lists(nA: np.ndarray, nB: np.ndarray, tau: float, MI: int, MJ: int) ->
     Not a paper construct: the grouping the GPU scheduler uses, written out from
     the keep definition (bit ``li*MJ + lj`` of entry k of group (I,J) is
     keep(I*MI+li, k, J*MJ+lj)).  Returns dict with ``ptr`` (GM*GN+1) and
-    ``entries`` (n, 2) int64 rows (k, mask).
+    ``entries`` (n, 2) uint64 rows (k, mask).
     """
     BM, BK = nA.shape
     BN = nB.shape[1]
@@ -154,8 +154,9 @@ def macro_lists(nA: np.ndarray, nB: np.ndarray, tau: float, MI: int, MJ: int) ->
                 if mask:
                     ents.append((k, mask))
             ptr.append(len(ents))
+    # uint64: 8 x 8 groups use all 64 mask bits
     return {"ptr": np.asarray(ptr, dtype=np.int64),
-            "entries": np.asarray(ents, dtype=np.int64).reshape(-1, 2)}
+            "entries": np.asarray(ents, dtype=np.uint64).reshape(-1, 2)}
 
 
 def spamm(A: np.ndarray, B: np.ndarray, tau: float, T: int,

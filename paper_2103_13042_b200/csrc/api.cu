@@ -180,7 +180,13 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->BM = BM;
   p->BK = BK;
   p->BN = BN;
-  p->MI = kMacroI;
+  // the CTA-pair tensor path needs fixed list regions and whole 32-column B boxes
+  const bool fixed_ok = !(flags & SPAMM_FLAG_SYNC_SKIPMAP) &&
+                        sizeof(uint16_t) * static_cast<size_t>(BM * BN) * static_cast<size_t>(BK) <= kWorstCaseBudget;
+  p->umma_variant = umma_variant_from_env();
+  p->pair = prec != SPAMM_FP32 && fixed_ok && N % 32 == 0 && p->umma_variant == 3;
+  if (prec != SPAMM_FP32 && !p->pair && p->umma_variant == 3) p->umma_variant = 0;
+  p->MI = p->pair ? kMacroI_pair : kMacroI;
   p->MJ = prec == SPAMM_FP32 ? kMacroJ_simt : kMacroJ_umma;
   p->GM = (BM + p->MI - 1) / p->MI;
   p->GN = (BN + p->MJ - 1) / p->MJ;
@@ -226,9 +232,12 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   // macro lists: worst case GM*GN*BK entries (8 B each) -- small relative to A and B
   if (st == SPAMM_OK) {
     p->macro_cap = nmac * BK;
-    st = alloc(reinterpret_cast<void**>(&p->macro_ent), sizeof(uint2) * static_cast<size_t>(p->macro_cap));
+    // (k, mask) entries: 8 bytes, or 16 bytes (k, mask_lo, mask_hi, 0) for 8 x 8 pair tiles
+    st = alloc(reinterpret_cast<void**>(&p->macro_ent), (p->pair ? 16 : 8) * static_cast<size_t>(p->macro_cap));
+    // tensor-path entries: a pair-path k-step with more than 6 runs takes two entries
     if (st == SPAMM_OK && prec != SPAMM_FP32)
-      st = alloc(reinterpret_cast<void**>(&p->macro_run), sizeof(uint4) * static_cast<size_t>(p->macro_cap));
+      st = alloc(reinterpret_cast<void**>(&p->macro_run),
+                 sizeof(uint4) * static_cast<size_t>(p->macro_cap) * (p->pair ? 2 : 1));
   }
   // leaf lists: reserve the worst case unless it exceeds the budget or SYNC_SKIPMAP is set
   if (st == SPAMM_OK && !(flags & SPAMM_FLAG_SYNC_SKIPMAP)) {
@@ -253,7 +262,6 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     }
   }
   if (st == SPAMM_OK) {
-    p->umma_variant = umma_variant_from_env();
     if (p->fixed_regions && prec != SPAMM_FP32 && umma_variant_wide(p->umma_variant))
       st = alloc(reinterpret_cast<void**>(&p->Uw), sizeof(int64_t) * static_cast<size_t>(nmac + 1));
     else
@@ -359,7 +367,10 @@ spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int
     SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
                                    s));
   } else {
-    SPAMM_TRY(launch_multiply_umma(p, A, lda, B, ldb, C, ldc, s));
+    if (p.pair)
+      SPAMM_TRY(launch_multiply_pair(p, A, lda, B, ldb, C, ldc, s));
+    else
+      SPAMM_TRY(launch_multiply_umma(p, A, lda, B, ldb, C, ldc, s));
   }
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[5], s));
   p.ev_mul = timing;

@@ -569,7 +569,7 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
 int umma_variant_from_env() {
   const char* v = getenv("SPAMM_UMMA_VARIANT");
   const int x = v ? atoi(v) : 0;
-  return x >= 0 && x <= 2 ? x : 0;
+  return x >= 0 && x <= 3 ? x : 0;
 }
 bool umma_variant_wide(int v) { return v != 0; }
 

@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -33,6 +34,10 @@ namespace spamm {
 namespace {
 
 constexpr int kWarps = 8;
+
+// keep bits of one k-step of a macro-tile: bit li*MJ+lj; 64-bit for the 8 x 8 pair tiles
+template <int MI, int MJ>
+using mask_t = typename std::conditional<(MI * MJ > 32), unsigned long long, uint32_t>::type;
 
 template <int MI, int MJ>
 struct ChunkVals {
@@ -64,7 +69,8 @@ __device__ __forceinline__ ChunkVals<MI, MJ> load_chunk(const double* __restrict
 
 // keep bits of one chunk: bit li*MJ+lj <=> !(a*b < tau), for in-range (i, k, j) only.
 template <int MI, int MJ>
-__device__ __forceinline__ uint32_t chunk_mask(const ChunkVals<MI, MJ>& v, uint32_t valid, double tau) {
+__device__ __forceinline__ mask_t<MI, MJ> chunk_mask(const ChunkVals<MI, MJ>& v, mask_t<MI, MJ> valid, double tau) {
+  using M_ = mask_t<MI, MJ>;
   // Exact pre-filters: norms are >= 0 (or NaN) and rounding is monotone, so
   //   max(a) * max(b) < tau   =>  every a*b < tau   (NaN-propagating maxima keep NaN pairs);
   //   min(a) * min(b) >= tau  =>  every a*b >= tau  (NaN pairs are kept either way).
@@ -81,28 +87,27 @@ __device__ __forceinline__ uint32_t chunk_mask(const ChunkVals<MI, MJ>& v, uint3
   }
   if (!v.kin || valid == 0u || __dmul_rn(amax, bmax) < tau) return 0u;
   if (__dmul_rn(amin, bmin) >= tau) return valid;
-  uint32_t mask = 0u;
+  M_ mask = 0u;
 #pragma unroll
   for (int li = 0; li < MI; ++li)
 #pragma unroll
     for (int lj = 0; lj < MJ; ++lj) {
       const double prod = __dmul_rn(v.a[li], v.b[lj]);
-      mask |= static_cast<uint32_t>(!(prod < tau)) << (li * MJ + lj);
+      mask |= static_cast<M_>(!(prod < tau)) << (li * MJ + lj);
     }
   return mask & valid;
 }
 // bit li*MJ+lj set iff C tile (I*MI+li, J*MJ+lj) exists
 template <int MI, int MJ>
-__device__ __forceinline__ uint32_t valid_bits(int64_t BM, int64_t BN, int64_t I, int64_t J) {
-  uint32_t v = 0u;
+__device__ __forceinline__ mask_t<MI, MJ> valid_bits(int64_t BM, int64_t BN, int64_t I, int64_t J) {
+  mask_t<MI, MJ> v = 0u;
 #pragma unroll
   for (int li = 0; li < MI; ++li)
 #pragma unroll
     for (int lj = 0; lj < MJ; ++lj)
-      if (I * MI + li < BM && J * MJ + lj < BN) v |= 1u << (li * MJ + lj);
+      if (I * MI + li < BM && J * MJ + lj < BN) v |= static_cast<mask_t<MI, MJ>>(1u) << (li * MJ + lj);
   return v;
 }
-
 // Exclusive scan of n int64 values by one CTA; out has n+1 entries, out[n] = total.
 // If reverse, out[u] = sum_{u' > u} in[u'] (descending buckets).
 __device__ void block_scan_array(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
@@ -404,6 +409,49 @@ __device__ void last_cta_order(const LastArgs& la, int64_t* s_warp, unsigned lon
 // lists -- (k, keep mask) per k-step, which hold every keep bit -- are written here; the
 // per-C-tile k lists are expanded from them on request (leaf_expand_kernel).  Row work
 // and kept-pair counts are popcounts of the masks.
+// Runs of an 8 x 8 keep mask for the CTA-pair tensor path (multiply_pair.cu): adjacent
+// C-tile columns with the same non-zero 8-bit row pattern.  run = j0 | (len-1) << 3 |
+// pat << 6 (14 bits) in 16-bit slots, at most kPairRuns per entry; a k-step with more runs
+// is written as several entries for the same k (their MMAs accumulate).
+//   x = k | nruns << 16 | wide << 19,  y/z/w = runs 2q | 2q+1 << 16
+constexpr int kPairRuns = 6;
+__device__ __forceinline__ uint32_t col_pattern64(unsigned long long mask, int lj) {
+  // bits li*8 + lj (li = 0..7) -> bit li: the byte-spread bits are gathered by one multiply
+  const unsigned long long t = (mask >> lj) & 0x0101010101010101ull;
+  return static_cast<uint32_t>((t * 0x0102040810204080ull) >> 56) & 0xFFu;
+}
+__device__ __forceinline__ int pair_run_count(unsigned long long mask) {
+  int nr = 0;
+  uint32_t prev = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t pat = col_pattern64(mask, j);
+    nr += (pat != 0u && pat != prev) ? 1 : 0;
+    prev = pat;
+  }
+  return nr;
+}
+__device__ __forceinline__ uint4 encode_pair(uint32_t k, unsigned long long mask, uint32_t wide, int part) {
+  if (mask == ~0ull)   // all 8 x 8 pairs kept: one run j0 = 0, len = 8, pattern 0xFF
+    return make_uint4(k | (1u << 16) | (wide << 19), 0u | (7u << 3) | (0xFFu << 6), 0u, 0u);
+  uint32_t slot[kPairRuns] = {0u, 0u, 0u, 0u, 0u, 0u};
+  int nr = 0, n = 0;
+  int j = 0;
+  while (j < 8) {
+    const uint32_t pat = col_pattern64(mask, j);
+    int j1 = j + 1;
+    while (j1 < 8 && col_pattern64(mask, j1) == pat) ++j1;
+    if (pat) {
+      if (nr >= part * kPairRuns && nr < (part + 1) * kPairRuns)
+        slot[n++] = static_cast<uint32_t>(j) | (static_cast<uint32_t>(j1 - j - 1) << 3) | (pat << 6);
+      ++nr;
+    }
+    j = j1;
+  }
+  return make_uint4(k | (static_cast<uint32_t>(n) << 16) | (wide << 19), slot[0] | (slot[1] << 16),
+                    slot[2] | (slot[3] << 16), slot[4] | (slot[5] << 16));
+}
+
 constexpr int kFusedWarps = 8;
 constexpr int kKB = 32 * kFusedWarps;   // k per block: thread (w, lane) owns k = kb + 32 w + lane
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* src) {
@@ -419,8 +467,11 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
     skip_fused_kernel(const double* __restrict__ nA, const double* __restrict__ nBt, int64_t BM, int64_t BK,
                       int64_t BN, double tau, int64_t GN, int64_t gi0, int64_t n_macro, int64_t* __restrict__ U,
                       int64_t* __restrict__ Lm, unsigned long long* __restrict__ row_work,
-                      unsigned long long* __restrict__ hist, uint2* __restrict__ macro_ent,
+                      unsigned long long* __restrict__ hist, void* __restrict__ macro_ent_v,
                       uint4* __restrict__ macro_run, int64_t* __restrict__ Uw, int merge_ok, LastArgs la) {
+  using M_ = mask_t<MI, MJ>;
+  constexpr bool kPair = MI * MJ > 32;    // 8 x 8 tiles: 64-bit masks, (k, mask_lo, mask_hi, 0) entries
+  constexpr int kRunStride = kPair ? 2 : 1;   // tensor-path region per macro-tile: kRunStride * BK entries
   constexpr int W = kFusedWarps;
   constexpr int R = MI + MJ;              // norm rows per macro-tile: MI of A, MJ of B^T
   __shared__ uint32_t s_cm[W], s_cr[W], s_rw[W][MI];
@@ -473,10 +524,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
     const long long c1 = clock64();
     const int64_t I = gi0 + m / GN, J = m % GN;
     const int64_t tile = I * GN + J;
-    const uint32_t valid = valid_bits<MI, MJ>(BM, BN, I, J);
+    const M_ valid = valid_bits<MI, MJ>(BM, BN, I, J);
     if (kb == 0) {
       mbase = tile * BK;                    // macro-tile region
-      wbase = tile * BK;                    // tensor-path entries (aligned equal-mask k pairs merged)
+      wbase = tile * BK * kRunStride;       // tensor-path entries
 #pragma unroll
       for (int li = 0; li < MI; ++li) rw[li] = 0u;
     }
@@ -487,25 +538,36 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
     for (int li = 0; li < MI; ++li) cv.a[li] = s_val[buf][li][col];
 #pragma unroll
     for (int lj = 0; lj < MJ; ++lj) cv.b[lj] = s_val[buf][MI + lj][col];
-    const uint32_t mask = chunk_mask<MI, MJ>(cv, valid, tau);
+    const M_ mask = chunk_mask<MI, MJ>(cv, valid, tau);
 #pragma unroll
-    for (int li = 0; li < MI; ++li) rw[li] += __popc((mask >> (li * MJ)) & ((1u << MJ) - 1u));
+    for (int li = 0; li < MI; ++li)
+      rw[li] += static_cast<uint32_t>(__popcll(static_cast<unsigned long long>(mask >> (li * MJ)) & ((1ull << MJ) - 1ull)));
     const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
-    bool wide = false, emit = false;
+    // tensor-path entries: k-tiles 2p and 2p+1 with the same non-zero mask become one
+    // 64-deep k-step; the pair path splits k-steps with more than kPairRuns runs
+    bool wide = false;
+    uint32_t ne = 0;
     if (MJ == 8 && macro_run != nullptr) {
-      // k-tiles 2p and 2p+1 with the same non-zero mask become one 64-deep k-step
-      const uint32_t mnext = __shfl_down_sync(0xffffffffu, mask, 1);
-      const uint32_t mprev = __shfl_up_sync(0xffffffffu, mask, 1);
+      const M_ mnext = __shfl_down_sync(0xffffffffu, mask, 1);
+      const M_ mprev = __shfl_up_sync(0xffffffffu, mask, 1);
       const bool even = (lane & 1) == 0;
       wide = merge_ok && even && mask != 0u && mnext == mask;
       const bool absorbed = merge_ok && !even && mask != 0u && mprev == mask;
-      emit = mask != 0u && !absorbed;
+      if (mask != 0u && !absorbed) {
+        if constexpr (kPair)
+          ne = static_cast<uint32_t>((pair_run_count(mask) + kPairRuns - 1) / kPairRuns);
+        else
+          ne = 1u;
+      }
     }
-    const uint32_t bal_r = __ballot_sync(0xffffffffu, emit);
-    if (lane == 0) {
-      s_cm[warp] = __popc(any);
-      s_cr[warp] = __popc(bal_r);
+    uint32_t ie = ne;   // inclusive warp scan of entry counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ie, o);
+      if (lane >= o) ie += y;
     }
+    if (lane == 0) s_cm[warp] = __popc(any);
+    if (lane == 31) s_cr[warp] = ie;
     __syncthreads();
     uint32_t om = 0, orr = 0, tm = 0, tr = 0;
 #pragma unroll
@@ -518,8 +580,21 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
       tm += cm;
       tr += cr;
     }
-    if (mask) macro_ent[mbase + om + __popc(any & lt)] = make_uint2(static_cast<uint32_t>(k), mask);
-    if (emit) macro_run[wbase + orr + __popc(bal_r & lt)] = encode_runs(static_cast<uint32_t>(k), mask, wide ? 1u : 0u);
+    if (mask) {
+      if constexpr (kPair)
+        reinterpret_cast<uint4*>(macro_ent_v)[mbase + om + __popc(any & lt)] =
+            make_uint4(static_cast<uint32_t>(k), static_cast<uint32_t>(mask), static_cast<uint32_t>(mask >> 32), 0u);
+      else
+        reinterpret_cast<uint2*>(macro_ent_v)[mbase + om + __popc(any & lt)] =
+            make_uint2(static_cast<uint32_t>(k), static_cast<uint32_t>(mask));
+    }
+    for (uint32_t q = 0; q < ne; ++q) {
+      const int64_t at = wbase + orr + (ie - ne) + q;
+      if constexpr (kPair)
+        macro_run[at] = encode_pair(static_cast<uint32_t>(k), mask, wide ? 1u : 0u, static_cast<int>(q));
+      else
+        macro_run[at] = encode_runs(static_cast<uint32_t>(k), static_cast<uint32_t>(mask), wide ? 1u : 0u);
+    }
     mbase += tm;
     wbase += tr;
     if (kb + kKB >= BK) {   // last k block of the macro-tile: counts
@@ -545,7 +620,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
           const uint32_t u = static_cast<uint32_t>(mbase - tile * BK);
           Lm[tile] = lsum;
           U[tile] = u;
-          if (Uw != nullptr) Uw[tile] = wbase - tile * BK;
+          if (Uw != nullptr) Uw[tile] = wbase - tile * BK * kRunStride;
           atomicAdd(hist + u, 1ull);
         }
       }
@@ -591,36 +666,61 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
 template <int MI, int MJ>
 __global__ void __launch_bounds__(kWarps * 32)
     leaf_expand_kernel(int64_t BM, int64_t BK, int64_t BN, int64_t GN, int64_t gi0, int64_t n_macro,
-                       const int64_t* __restrict__ U, const uint2* __restrict__ macro_ent, int64_t* __restrict__ V,
+                       const int64_t* __restrict__ U, const void* __restrict__ macro_ent_v, int64_t* __restrict__ V,
                        int64_t* __restrict__ leaf_start, uint16_t* __restrict__ leaf_k) {
   constexpr int NB = MI * MJ;
+  constexpr int NL = (NB + 31) / 32;   // leaves per lane
+  using M_ = mask_t<MI, MJ>;
   const int lane = threadIdx.x & 31;
   const int64_t m = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   if (m >= n_macro) return;
   const int64_t I = gi0 + m / GN, J = m % GN;
   const int64_t tile = I * GN + J;
-  const uint32_t valid = valid_bits<MI, MJ>(BM, BN, I, J);
-  const int li = lane / MJ, lj = lane % MJ;
-  const bool vl = lane < NB && ((valid >> lane) & 1u);
-  const int64_t leaf = (I * MI + li) * BN + (J * MJ + lj);
-  const int64_t lstart = leaf * BK;
-  int64_t n = 0;
+  const M_ valid = valid_bits<MI, MJ>(BM, BN, I, J);
+  int64_t n[NL], lstart[NL], leaf[NL];
+  bool vl[NL];
+#pragma unroll
+  for (int h = 0; h < NL; ++h) {
+    const int b = lane + 32 * h;
+    vl[h] = b < NB && ((valid >> b) & 1u);
+    leaf[h] = (I * MI + b / MJ) * BN + (J * MJ + b % MJ);
+    lstart[h] = leaf[h] * BK;
+    n[h] = 0;
+  }
   const int64_t u = U[tile];
   for (int64_t e0 = 0; e0 < u; e0 += 32) {
-    const uint2 mine = e0 + lane < u ? macro_ent[tile * BK + e0 + lane] : make_uint2(0u, 0u);
+    const int64_t e = tile * BK + e0 + lane;
+    uint32_t mk = 0u;
+    M_ mm = 0u;
+    if (e0 + lane < u) {
+      if constexpr (NB > 32) {
+        const uint4 x = reinterpret_cast<const uint4*>(macro_ent_v)[e];
+        mk = x.x;
+        mm = static_cast<M_>(x.y) | (static_cast<M_>(x.z) << 32);
+      } else {
+        const uint2 x = reinterpret_cast<const uint2*>(macro_ent_v)[e];
+        mk = x.x;
+        mm = x.y;
+      }
+    }
     const int cnt = static_cast<int>(u - e0 < 32 ? u - e0 : 32);
     for (int q = 0; q < cnt; ++q) {
-      const uint32_t k = __shfl_sync(0xffffffffu, mine.x, q), mask = __shfl_sync(0xffffffffu, mine.y, q);
-      if (vl && ((mask >> lane) & 1u)) leaf_k[lstart + n++] = static_cast<uint16_t>(k);
+      const uint32_t k = __shfl_sync(0xffffffffu, mk, q);
+      const M_ mask = __shfl_sync(0xffffffffu, mm, q);
+#pragma unroll
+      for (int h = 0; h < NL; ++h)
+        if (vl[h] && ((mask >> (lane + 32 * h)) & 1u)) leaf_k[lstart[h] + n[h]++] = static_cast<uint16_t>(k);
     }
   }
-  if (vl) {
-    V[leaf] = n;
-    leaf_start[leaf] = lstart;
-  }
+#pragma unroll
+  for (int h = 0; h < NL; ++h)
+    if (vl[h]) {
+      V[leaf[h]] = n[h];
+      leaf_start[leaf[h]] = lstart[h];
+    }
 }
 
-template <int MJ>
+template <int MI, int MJ>
 spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   const int64_t n_macro = (gi1 - gi0) * p.GN;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(n_macro, static_cast<int64_t>(p.num_sms) * 4));
@@ -631,13 +731,13 @@ spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
     cudaMemcpyAsync(tst, init, sizeof(init), cudaMemcpyHostToDevice, s);
   }
   LastArgs la{p.hist, p.bucket_pos, p.BK + 1, p.U, p.L, p.order, gi0 * p.GN, gi1 * p.GN, p.totals, p.ticket, tst};
-  constexpr int dyn = 2 * (kMacroI + MJ) * kKB * static_cast<int>(sizeof(double));
+  constexpr int dyn = 2 * (MI + MJ) * kKB * static_cast<int>(sizeof(double));
   static bool attr = false;
   if (!attr) {
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(skip_fused_kernel<kMacroI, MJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(skip_fused_kernel<MI, MJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     attr = true;
   }
-  skip_fused_kernel<kMacroI, MJ><<<static_cast<unsigned>(blocks), kFusedWarps * 32, dyn, s>>>(
+  skip_fused_kernel<MI, MJ><<<static_cast<unsigned>(blocks), kFusedWarps * 32, dyn, s>>>(
       p.nA, p.nBt, p.BM, p.BK, p.BN, p.tau, p.GN, gi0, n_macro, p.U, p.L,
       reinterpret_cast<unsigned long long*>(p.row_work), reinterpret_cast<unsigned long long*>(p.hist),
       p.macro_ent, p.macro_run, p.Uw != p.U ? p.Uw : nullptr, static_cast<int>(p.Uw != p.U && p.N % 32 == 0), la);
@@ -731,8 +831,9 @@ spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_
   }
   // row_work [BM], hist [BK+2] and totals [2] are contiguous in one allocation (see api.cu)
   SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 4), s));
-  if (p.MJ == kMacroJ_umma) return fused_t<kMacroJ_umma>(p, gi0, gi1, s);
-  return fused_t<kMacroJ_simt>(p, gi0, gi1, s);
+  if (p.MI == kMacroI_pair) return fused_t<kMacroI_pair, kMacroJ_umma>(p, gi0, gi1, s);
+  if (p.MJ == kMacroJ_umma) return fused_t<kMacroI, kMacroJ_umma>(p, gi0, gi1, s);
+  return fused_t<kMacroI, kMacroJ_simt>(p, gi0, gi1, s);
 }
 
 spamm_status launch_leaf_expand(Plan& p, cudaStream_t s) {
@@ -742,7 +843,10 @@ spamm_status launch_leaf_expand(Plan& p, cudaStream_t s) {
   const int64_t n_macro = (gi1 - gi0) * p.GN;
   if (n_macro <= 0) return SPAMM_OK;
   const int64_t blocks = (n_macro + kWarps - 1) / kWarps;
-  if (p.MJ == kMacroJ_umma)
+  if (p.MI == kMacroI_pair)
+    leaf_expand_kernel<kMacroI_pair, kMacroJ_umma><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
+        p.BM, p.BK, p.BN, p.GN, gi0, n_macro, p.U, p.macro_ent, p.V, p.leaf_start, p.leaf_k);
+  else if (p.MJ == kMacroJ_umma)
     leaf_expand_kernel<kMacroI, kMacroJ_umma><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
         p.BM, p.BK, p.BN, p.GN, gi0, n_macro, p.U, p.macro_ent, p.V, p.leaf_start, p.leaf_k);
   else

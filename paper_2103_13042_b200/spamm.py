@@ -259,7 +259,8 @@ def spamm_get_counts(plan):
 def spamm_get_macro(plan):
     """(start int64 [GM*GN], count int64 [GM*GN], entries [n, 2] int64 (k, mask) over all
     entry storage in use, order int32 [GM*GN], GM, GN); macro-tile t's list is
-    entries[start[t] : start[t] + count[t]]."""
+    entries[start[t] : start[t] + count[t]].  Masks of 8 x 8 groups (CTA-pair path) use
+    all 64 bits: view them as uint64."""
     st = spamm_get_stats(plan)
     ps, pc, e, o = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
     GM, GN = ctypes.c_int64(), ctypes.c_int64()
@@ -269,8 +270,14 @@ def spamm_get_macro(plan):
     start = _view(ps.value, (nmac,), "<i8", torch.int64)
     count = _view(pc.value, (nmac,), "<i8", torch.int64)
     n = int((start + count).max().item()) if nmac else 0
-    ent = _view(e.value, (n, 2), "<u4", torch.uint32).to(torch.int64) if n else torch.zeros((0, 2), dtype=torch.int64,
-                                                                                             device="cuda")
+    wide = st["macro_i"] * st["macro_j"] > 32   # 8 x 8 pair tiles: (k, mask_lo, mask_hi, 0) words
+    if not n:
+        ent = torch.zeros((0, 2), dtype=torch.int64, device="cuda")
+    elif wide:
+        w = _view(e.value, (n, 4), "<u4", torch.uint32).to(torch.int64)
+        ent = torch.stack([w[:, 0], w[:, 1] | (w[:, 2] << 32)], dim=1)   # mask bit 63 wraps to negative int64
+    else:
+        ent = _view(e.value, (n, 2), "<u4", torch.uint32).to(torch.int64)
     order = _view(o.value, (nmac,), "<i4", torch.int32)
     return start, count, ent, order, GM.value, GN.value
 
