@@ -10,7 +10,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > $OUT/ncu_launch_bench.json 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:spamm_mul_umma -s 3 -c 1 -o $OUT/prof_umma -f \
    python bench.py --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tile_norms|skip_" -s 15 -c 5 -o $OUT/prof_norms_skip -f \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tile_norms|skip_" -s 4 -c 2 -o $OUT/prof_norms_skip -f \
    python bench.py --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:spamm_mul_simt -s 3 -c 1 -o $OUT/prof_simt -f \
    python bench.py --precision fp32 --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > /dev/null 2>&1

@@ -8,6 +8,7 @@ import argparse
 import csv
 import json
 import os
+import re
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -46,9 +47,10 @@ def summarise_rep(rep, tag, prec):
             t = to_bytes(r["dram__bytes_read.sum"], units["dram__bytes_read.sum"]) + \
                 to_bytes(r["dram__bytes_write.sum"], units["dram__bytes_write.sum"])
             lines.append(f"traffic (dram read+write) = {t:.4g} B")
-            key = "multiply" if "spamm_mul" in name else ("norms" if "tile_norms" in name else
-                                                          ("skipmap_" + name.split("::")[-1].split("<")[0].split("(")[0]))
-            traffic[key] = traffic.get(key, 0.0) + t if key == "norms" else t
+            base = re.search(r"(\w+)(?:<[^()]*>)?\(", name)
+            kname = base.group(1) if base else name
+            key = "multiply" if "spamm_mul" in name else ("norms" if "tile_norms" in name else "skipmap_" + kname)
+            traffic[key] = t   # one capture per kernel per step
     base = os.path.splitext(os.path.basename(rep))[0]
     with open(os.path.join(ROOT, "profiles", f"{tag}_{base}.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
@@ -70,8 +72,8 @@ def summarise_launches(path, tag):
     out += [f"{i},{k[:120].replace(',', ';')},{v:.0f}" for i, k, v in recs]
     # share of the last complete step (from the last tile_norms pair to the end)
     starts = [j for j, (_, k, _) in enumerate(recs) if "tile_norms" in k]
-    if len(starts) >= 2:
-        step = recs[starts[-2]:]
+    if starts:
+        step = recs[starts[-1]:]
         tot = sum(v for _, k, v in step if "FillFunctor" not in k)
         out.append("\n# share of one step (L2-flush fill excluded)")
         for _, k, v in step:
