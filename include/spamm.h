@@ -171,6 +171,26 @@ spamm_status spamm_multiply_mgpu(spamm_plan_t p, void* nccl_comm, int rank, int 
                                  const void* A, int64_t lda, const void* B, int64_t ldb,
                                  float* C, int64_t ldc, uint32_t flags, void* stream);
 
+/* ------------------------------------------------------------ tau search --- */
+
+/* Number of kept triples at tau, i.e. #{(i,k,j) : !(nA[i][k] * nB[k][j] < tau)} in float64
+ * over all BM*BK*BN triples, from the plan's norm maps without building
+ * a skip map.  Requires spamm_norms (else SPAMM_E_STATE); tau finite and >= 0 (else
+ * SPAMM_E_INVALID).  Synchronises `stream` once; *kept is host memory. */
+spamm_status spamm_count_kept(spamm_plan_t p, double tau, int64_t* kept, void* stream);
+
+/* Sec. 3.5.2: search tau for a target valid ratio `target` (fraction in
+ * [0,1]).  ave = mean of nA[i][k]*nB[k][j] over all BM*BK*BN triples (R17);
+ * tau = ave, bracket [0, k*ave] with k = 1 and k incremented while vr(k*ave) > target;
+ * bisection at the midpoint; stop when |vr - target| < tol (absolute, R16; the
+ * paper uses 0.01) or after max_iter evaluations.  Every vr evaluation is one count kernel
+ * (as spamm_count_kept) and one stream synchronisation.  Outputs (host memory): *tau, and
+ * if non-NULL *valid_ratio = vr(*tau), *iters = evaluations of the main loop.  The plan's
+ * tau is set to *tau and its skip map invalidated (call spamm_build_skipmap next).
+ * Requires spamm_norms (else SPAMM_E_STATE); bad target/tol/max_iter -> SPAMM_E_INVALID. */
+spamm_status spamm_tau_search(spamm_plan_t p, double target, double tol, int32_t max_iter,
+                              double* tau, double* valid_ratio, int32_t* iters, void* stream);
+
 /* -------------------------------------------------------- introspection --- */
 
 /* Device pointers to the float64 norm maps: dA = nA[BM][BK], dBt = nB^T[BN][BK]. */

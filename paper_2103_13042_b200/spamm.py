@@ -73,6 +73,8 @@ def _load():
         "spamm_get_macro": [P, PP, PP, PP, PP, PI64, PI64],
         "spamm_get_partition": [P, PI64, ctypes.c_int],
         "spamm_get_stats": [P, ctypes.POINTER(spamm_stats)],
+        "spamm_count_kept": [P, D, PI64, P],
+        "spamm_tau_search": [P, D, D, I32, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I32), P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -169,6 +171,22 @@ def spamm_run(plan, A, B, C, stream=None) -> None:
     b, ldb = _mat(B)
     c, ldc = _mat(C)
     _check(_lib.spamm_run(plan, a, lda, b, ldb, c, ldc, _stream(stream)))
+
+
+# -------------------------------------------------------------- tau search ---
+def spamm_count_kept(plan, tau: float, stream=None) -> int:
+    out = ctypes.c_int64()
+    _check(_lib.spamm_count_kept(plan, float(tau), ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+def spamm_tau_search(plan, target: float, tol: float = 0.01, max_iter: int = 20,
+                     stream=None) -> tuple[float, float, int]:
+    """Sec. 3.5.2 search; returns (tau, valid_ratio, iterations)."""
+    t, vr, it = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+    _check(_lib.spamm_tau_search(plan, float(target), float(tol), int(max_iter), ctypes.byref(t),
+                                 ctypes.byref(vr), ctypes.byref(it), _stream(stream)))
+    return t.value, vr.value, it.value
 
 
 # -------------------------------------------------------------- multi-GPU ---
@@ -348,3 +366,9 @@ class Plan:
 
     def stats(self):
         return spamm_get_stats(self.handle)
+
+    def count_kept(self, tau, stream=None):
+        return spamm_count_kept(self.handle, tau, stream)
+
+    def tau_search(self, target, tol=0.01, max_iter=20, stream=None):
+        return spamm_tau_search(self.handle, target, tol, max_iter, stream)

@@ -137,3 +137,138 @@ def round_to_bf16(x: np.ndarray) -> np.ndarray:
 def round_to_fp16(x: np.ndarray) -> np.ndarray:
     """float32 array holding the RNE-float16 values of x."""
     return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float32)
+
+
+# --------------------------------------------------------------------------------------------
+# configs[3]: electronic-structure-like banded decay and ReLU-sparsified im2col GEMM shapes
+# --------------------------------------------------------------------------------------------
+
+def normal01(seed: int, counter: np.ndarray) -> np.ndarray:
+    """Standard normal float64 via Box-Muller from two splitmix64 uniforms per counter."""
+    c = np.asarray(counter, dtype=np.uint64)
+    u1 = uniform01(seed, c * np.uint64(2))
+    u2 = uniform01(seed, c * np.uint64(2) + np.uint64(1))
+    return np.sqrt(-2.0 * np.log1p(-u1)) * np.cos(2.0 * np.pi * u2)
+
+
+def water_cluster_centres(n_mol: int = 569, spacing: float = 3.1, jitter: float = 0.3,
+                          seed: int = 2107) -> np.ndarray:
+    """(n_mol, 3) molecule centres in Angstrom, Morton (Z-curve) ordered.
+
+    The n_mol points of a cubic lattice (spacing 3.1 A, about the O-O distance in water)
+    nearest the origin (ties broken lexicographically), each jittered by N(0, jitter^2)
+    per axis.  The shape stands in for the ergo water-cluster density matrices the
+    paper multiplies (PAPER.md:320, 569 molecules at the size used there); no chemistry.
+    """
+    R = int(np.ceil((3.0 * n_mol / (4.0 * np.pi)) ** (1.0 / 3.0))) + 2
+    g = np.arange(-R, R + 1)
+    pts = np.stack(np.meshgrid(g, g, g, indexing="ij"), axis=-1).reshape(-1, 3)
+    d2 = (pts * pts).sum(axis=1)
+    order = np.lexsort((pts[:, 2], pts[:, 1], pts[:, 0], d2))[:n_mol]
+    pos = spacing * pts[order].astype(np.float64)
+    ctr = np.arange(3 * n_mol, dtype=np.uint64).reshape(n_mol, 3)
+    pos = pos + jitter * normal01(seed, ctr)
+    # Morton order of 10-bit quantised coordinates
+    q = pos - pos.min(axis=0)
+    q = np.minimum((q / max(float(q.max()), 1e-12) * 1023.0).astype(np.int64), 1023)
+    code = np.zeros(n_mol, dtype=np.int64)
+    for b in range(10):
+        for a in range(3):
+            code |= ((q[:, a] >> b) & 1) << (3 * b + a)
+    return pos[np.argsort(code, kind="stable")]
+
+
+def water_cluster_matrix(n_mol: int = 569, nbf: int = 24, alpha: float = 1.0,
+                         seed: int = 2107) -> np.ndarray:
+    """float32 (n, n), n = n_mol*nbf: a_ij = exp(-alpha * r(m(i), m(j))) * g_ij.
+
+    m(i) = i // nbf is the molecule of basis function i, r the centre distance in A,
+    g symmetric uniform in [-1, 1) from splitmix64 of (seed, min(i,j)*n + max(i,j)).
+    A = B ("power" of a density-like matrix).  n = 13656 for the default
+    569 molecules x 24 functions, which is not a multiple of 32 (exercises padding).
+    """
+    pos = water_cluster_centres(n_mol, seed=seed)
+    n = n_mol * nbf
+    mol = np.arange(n) // nbf
+    out = np.empty((n, n), dtype=np.float32)
+    cols = np.arange(n, dtype=np.int64)
+    step = max(1, (1 << 22) // n)
+    for r0 in range(0, n, step):
+        rows = np.arange(r0, min(n, r0 + step), dtype=np.int64)
+        dr = pos[mol[rows]][:, None, :] - pos[mol[cols]][None, :, :]
+        r = np.sqrt((dr * dr).sum(axis=-1))
+        lo = np.minimum(rows[:, None], cols[None, :]).astype(np.uint64)
+        hi = np.maximum(rows[:, None], cols[None, :]).astype(np.uint64)
+        g = 2.0 * uniform01(seed + 0x77, lo * np.uint64(n) + hi) - 1.0
+        out[r0:r0 + len(rows)] = (np.exp(-alpha * r) * g).astype(np.float32)
+    return out
+
+
+# VGG13 layers whose im2col GEMMs the paper sparsifies (PAPER.md:338, DESIGN.md reading R15):
+# name -> (C_out, C_in, H = W, batch)
+IM2COL_LAYERS = {"conv21": (128, 64, 16, 100), "conv31": (256, 128, 8, 100)}
+
+
+def conv_weight(c_out: int, c_in: int, seed: int, prune: float = 0.5) -> np.ndarray:
+    """float32 (c_out, c_in*9) 3x3 conv weights ~ N(0, 2/fan_in), the smallest |w| fraction
+    ``prune`` set to zero (magnitude pruning)."""
+    fan = c_in * 9
+    w = normal01(seed, np.arange(c_out * fan, dtype=np.uint64)).reshape(c_out, fan) * np.sqrt(2.0 / fan)
+    if prune > 0:
+        thr = np.quantile(np.abs(w), prune)
+        w = np.where(np.abs(w) <= thr, 0.0, w)
+    return w.astype(np.float32)
+
+
+def relu_activations(batch: int, c: int, h: int, seed: int) -> np.ndarray:
+    """float32 (batch, c, h, h): ReLU(N(b_c, 1)) * s_{n,c}, b_c ~ N(-0.5, 0.5^2),
+    s ~ LogNormal(0, 0.5^2); >= 50 % zeros like post-ReLU feature maps."""
+    b = -0.5 + 0.5 * normal01(seed, np.arange(c, dtype=np.uint64))
+    s = np.exp(0.5 * normal01(seed + 1, np.arange(batch * c, dtype=np.uint64))).reshape(batch, c)
+    z = normal01(seed + 2, np.arange(batch * c * h * h, dtype=np.uint64)).reshape(batch, c, h, h)
+    x = np.maximum(z + b[None, :, None, None], 0.0) * s[:, :, None, None]
+    return x.astype(np.float32)
+
+
+def im2col(x: np.ndarray) -> np.ndarray:
+    """(batch, c, h, w) -> (c*9, batch*h*w) columns of a 3x3, stride-1, pad-1 convolution;
+    row index c*9 + ky*3 + kx, column index (n*h + y)*w + x."""
+    nb, c, h, w = x.shape
+    xp = np.zeros((nb, c, h + 2, w + 2), dtype=x.dtype)
+    xp[:, :, 1:-1, 1:-1] = x
+    cols = np.empty((c, 3, 3, nb, h, w), dtype=x.dtype)
+    for ky in range(3):
+        for kx in range(3):
+            cols[:, ky, kx] = xp[:, :, ky:ky + h, kx:kx + w].transpose(1, 0, 2, 3)
+    return np.ascontiguousarray(cols.reshape(c * 9, nb * h * w))
+
+
+def im2col_gemm(layer: str, seed: int = 2107) -> tuple[np.ndarray, np.ndarray]:
+    """(A, B) = (pruned weights W [C_out x C_in*9], im2col(X) [C_in*9 x batch*H*W]) for a
+    VGG13 layer of IM2COL_LAYERS: conv21 128x576x25600, conv31 256x1152x6400."""
+    c_out, c_in, h, nb = IM2COL_LAYERS[layer]
+    W = conv_weight(c_out, c_in, seed)
+    X = relu_activations(nb, c_in, h, seed + 10)
+    return W, im2col(X)
+
+
+def toeplitz_block(table32: np.ndarray, r0: int, r1: int, c0: int, c1: int) -> np.ndarray:
+    """Rows r0:r1, columns c0:c1 of the Toeplitz matrix a_ij = table32[|i-j|]."""
+    rows = np.arange(r0, r1, dtype=np.int64)
+    cols = np.arange(c0, c1, dtype=np.int64)
+    return table32[np.abs(rows[:, None] - cols[None, :])]
+
+
+def toeplitz_device(table32: np.ndarray, n: int, dtype, device="cuda"):
+    """Device-resident (n, n) torch tensor a_ij = table32[|i-j|] in ``dtype`` (configs[4]:
+    N = 65536 does not fit comfortably in host memory).  Pure indexing: the same values
+    ``toeplitz(table32, n, n)`` holds, converted to ``dtype`` by torch's RNE cast."""
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(table32)).to(device)
+    out = torch.empty((n, n), dtype=dtype, device=device)
+    cols = torch.arange(n, device=device)
+    step = max(1, (1 << 26) // n)
+    for r0 in range(0, n, step):
+        rows = torch.arange(r0, min(n, r0 + step), device=device)
+        out[r0:r0 + len(rows)] = t[(rows[:, None] - cols[None, :]).abs()].to(dtype)
+    return out
