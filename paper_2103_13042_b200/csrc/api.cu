@@ -105,7 +105,7 @@ static spamm_status alloc(void** p, size_t bytes) {
 static void free_plan(Plan* p) {
   if (!p) return;
   void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_start, p->L, p->leaf_base, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent, p->macro_run,
-                  p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp};
+                  p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp, p->sk_scratch, p->sk_ticket, p->sk_wpre};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->mstart && p->mstart != p->macro_ptr) cudaFree(p->mstart);
@@ -209,7 +209,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   ALLOC(macro_ptr, int64_t, nmac + 1);
   ALLOC(row_work, int64_t, BM + BK + 4);
   ALLOC(ticket, unsigned int, 1);
-  ALLOC(sched, unsigned int, 1);
+  ALLOC(sched, unsigned int, 4);   // [0] tile claims, [1] zero-fill unit claims
   ALLOC(order, int32_t, nmac);
   ALLOC(bucket_pos, int64_t, BK + 2);
 #undef ALLOC

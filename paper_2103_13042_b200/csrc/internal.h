@@ -53,6 +53,11 @@ struct Plan {
   int umma_variant = 0;          // tensor-path kernel: 0-2 multiply_umma.cu, 3 = CTA pairs (multiply_pair.cu)
   bool pair = false;             // the CTA-pair path is in use (MI = 8, 16-byte macro entries)
   int64_t* Uw = nullptr;         // [GM*GN] tensor-path entries per macro-tile (pairs merged) or = U
+  // stream-K workspace of the tensor multiply (allocated on first use)
+  float* sk_scratch = nullptr;       // [2 * grid][128 * 256] FP32 partial tiles
+  unsigned int* sk_ticket = nullptr; // [GM*GN] contributors arrived per LPT position (self-resetting)
+  int64_t* sk_wpre = nullptr;        // [GM*GN + 1] exclusive prefix of Uw over the LPT order
+  int64_t sk_cap_tiles = 0, sk_cap_slots = 0;
   bool fixed_regions = false;    // lists stored in worst-case fixed regions (single-pass skip map)
   int64_t* bucket_pos = nullptr; // [BK+2] descending bucket starts (consumed by emit)
   void* cub_tmp = nullptr;

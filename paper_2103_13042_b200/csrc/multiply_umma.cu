@@ -56,7 +56,7 @@ struct Cfg {
   static constexpr int kStages = (kCtas == 2 && kWide) ? 2 : 4;
   static constexpr int kBufs = kCtas == 2 ? 1 : 2;                       // TMEM accumulators
   static constexpr uint32_t kTmemCols = 256u * kBufs;
-  static constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 512 + 1536;
+  static constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 1024 + 1536;
 };
 constexpr int kThreads = 384;                   // w0 TMA, w1 MMA, w2 TMEM alloc, w4-11 epilogue
 constexpr int kEpiWarps = 8;                    // 2 per TMEM lane quadrant, 4 column chunks each
@@ -67,18 +67,72 @@ constexpr uint32_t kFullRun = 0u | (7u << 3) | (15u << 6);
 // stream flags in srun[s].w (bits 0-19 hold runs 6-7, bit 31 marks a 64-deep k-step)
 constexpr uint32_t kFirst = 1u << 29, kLast = 1u << 30, kNoStep = 1u << 28, kEnd = 1u << 27;
 
+// A chunk of the k-step stream: macro-tile t (LPT position i), entries [e0, e1) of its list;
+// part != 0 when the chunk is not the whole list (stream-K split, combined via scratch).
 struct TileInfo {
-  int64_t t, e0, e1;
+  int64_t t, e0, e1, i;
+  int32_t part, pad;
 };
 __device__ __forceinline__ TileInfo tile_info(const int32_t* order, const int64_t* mstart, const int64_t* mcount,
                                               int64_t idx, int64_t n_tiles) {
-  TileInfo ti{-1, 0, 0};
+  TileInfo ti{-1, 0, 0, idx, 0, 0};
   if (idx < n_tiles) {
     ti.t = order[idx];
     ti.e0 = mstart[ti.t];
     ti.e1 = ti.e0 + mcount[ti.t];
   }
   return ti;
+}
+
+// Stream-K partition: CTA c of G owns k-steps [B(c), B(c+1)) of the LPT-ordered stream of
+// W steps, B(c) = c*W/G; owner(x) is the CTA whose range holds step x.
+__device__ __forceinline__ int64_t sk_bound(int64_t c, int64_t W, int64_t G) { return (c * W) / G; }
+__device__ __forceinline__ int64_t sk_owner(int64_t x, int64_t W, int64_t G) {
+  int64_t c = (x * G) / W;
+  while (c + 1 < G && sk_bound(c + 1, W, G) <= x) ++c;
+  while (c > 0 && sk_bound(c, W, G) > x) --c;
+  return c;
+}
+// scratch slot of contributor c2 to the partial tile at LPT position i: a CTA's first chunk
+// uses slot 2c, its last chunk slot 2c+1 (a single-chunk range uses 2c).
+__device__ __forceinline__ int64_t sk_slot(int64_t c2, int64_t c_lo, int64_t wi, int64_t W, int64_t G) {
+  return 2 * c2 + ((c2 == c_lo && sk_bound(c_lo, W, G) < wi) ? 1 : 0);
+}
+// Cost weight of one k-step entry for the stream-K split, in units of ~one MMA pair: the
+// issuing thread's per-step overhead (~3) plus one per MMA run (x2 for a 64-deep step).
+// Measured on B200: MMA-thread cycles per CTA track MMA count (corr 0.97), not step count.
+constexpr int64_t kMaxEntryW = 3 + 2 * 8;
+__device__ __forceinline__ int64_t entry_w(const uint4& en) {
+  const uint32_t nr = (en.x >> 16) & 15u;
+  return 3 + static_cast<int64_t>(nr) * ((en.w >> 31) ? 2 : 1);
+}
+// Smallest e in [0, n) whose start weight w_start + sum_{e' < e} w(e') is >= target (n if none);
+// whole warp, returns the same value in every lane.  *w_at = start weight of that entry.
+__device__ __forceinline__ int64_t find_entry(const uint4* __restrict__ ent, int64_t n, int64_t w_start, int64_t target,
+                                              int64_t* w_at) {
+  const int lane = threadIdx.x & 31;
+  int64_t base = 0, w = w_start;
+  while (base < n && w < target) {
+    const int64_t e = base + lane;
+    const int64_t we = e < n ? entry_w(ent[e]) : 0;
+    int64_t incl = we;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int64_t start = w + incl - we;                  // start weight of entry e
+    const uint32_t hit = __ballot_sync(0xffffffffu, e < n && start >= target);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      *w_at = __shfl_sync(0xffffffffu, start, l);
+      return base + l;
+    }
+    w += __shfl_sync(0xffffffffu, incl, 31);
+    base += 32;
+  }
+  *w_at = w;
+  return base < n ? base : n;
 }
 
 struct Maps {   // A (32- and 64-deep boxes); B as stacked 32-column boxes, 1..8 boxes, 32- or 64-deep
@@ -91,14 +145,38 @@ __global__ void __launch_bounds__(kThreads, kCtas)
                           const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
                           int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
+                          const int64_t* __restrict__ n_empty_p, const int64_t* __restrict__ wpre,
+                          float* __restrict__ sk_scratch, unsigned int* __restrict__ sk_ticket,
                           unsigned long long* __restrict__ prof, int dbg) {
   using C_ = Cfg<kCtas, kWide>;
+  // The LPT order lists macro-tiles by descending union length, so the tiles without any
+  // kept pair (C = 0 there; often most of a banded product) are its tail.  Default
+  // (n_empty_p == nullptr): they are claimed like any tile and written through the pipeline
+  // (one D = 0 MMA and an epilogue pass), which lets early-finishing CTAs absorb them at the
+  // end -- measured fastest.  With n_empty_p (required by stream-K) only the first n_work
+  // tiles go through the pipeline and the epilogue warps zero-fill the rest in 8-row units
+  // (bulk stores of a zero buffer, dealt round-robin).
+  const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
+  const int64_t n_work = n_tiles - n_empty;
+  // Stream-K (wpre != nullptr): the n_work non-empty tiles' k-steps, in LPT order, are one
+  // stream of W = wpre[n_work] steps split evenly over the grid; a tile cut by a range
+  // boundary is accumulated in parts whose FP32 partials meet in sk_scratch, and the last
+  // contributor (per-tile ticket) adds them in CTA order and stores C.  Otherwise CTAs
+  // claim whole tiles dynamically (sched[0]).
+  const bool streamk = wpre != nullptr;
+  // W is in entry-weight units (entry_w); an entry belongs to the worker whose range holds
+  // its start weight.  G = min(grid, W / kMaxEntryW) workers (CTAs >= G only zero-fill), so
+  // the contributors to a split tile are exactly owner(w0) .. owner(start of its last entry).
+  const int64_t skW = streamk ? wpre[n_work] : 0, skC = blockIdx.x;
+  // (workers' ranges are >= kMaxEntryW wide, so each holds at least one entry start)
+  const int64_t skGmax = skW / kMaxEntryW;
+  const int64_t skG = skGmax < static_cast<int64_t>(gridDim.x) ? (skGmax > 0 ? skGmax : 1) : static_cast<int64_t>(gridDim.x);
   constexpr int kStages = C_::kStages, kStageBytes = C_::kStageBytes, kASlot = C_::kASlot, kBufs = C_::kBufs;
   constexpr uint32_t kTmemCols = C_::kTmemCols;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sZero = smem + kStages * kStageBytes;                // 512-B zero atom
-  uint64_t* full = reinterpret_cast<uint64_t*>(sZero + 512);
+  uint8_t* sZero = smem + kStages * kStageBytes;                // 1 KB of zeros: MMA zero atom, bulk zero-fill source
+  uint64_t* full = reinterpret_cast<uint64_t*>(sZero + 1024);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -109,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
   uint4* sentB = sentA + 32;                                     // [32] producer B entry batch
   TileInfo* tq = reinterpret_cast<TileInfo*>(sentB + 32);       // [kTQ]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTQ);
+  volatile uint32_t* sk_flag = tmem_slot + 1;                    // stream-K: "this CTA combines" 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (prof && threadIdx.x == 0) {
@@ -116,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
     prof[blockIdx.x * 16 + 8] = g;
   }
-  for (int i = threadIdx.x; i < 512 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();   // the zero atom is read by tcgen05.mma (async proxy)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -160,12 +239,48 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     uint32_t tq_ph = 0;
     unsigned long long p_wait = 0, p_claim = 0;
     const unsigned long long p_t0 = clock64();
-    // tiles are claimed one ahead so the claim's latency hides behind the current tile
+    // dynamic mode: tiles are claimed one ahead so the claim's latency hides behind the
+    // current tile; stream-K mode: walk the tiles overlapping [b0, b1)
+    const bool worker = streamk && skC < skG;
+    const int64_t b0 = worker ? sk_bound(skC, skW, skG) : 0, b1 = worker ? sk_bound(skC + 1, skW, skG) : 0;
+    int64_t sk_i = 0;
+    if (streamk && b0 < b1) {   // largest i < n_work with wpre[i] <= b0
+      int64_t lo = 0, hi = n_work - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (wpre[mid] <= b0) lo = mid; else hi = mid - 1;
+      }
+      sk_i = lo;
+    }
+    auto sk_next = [&]() -> TileInfo {
+      TileInfo ti{-1, 0, 0, -1, 0, 0};
+      while (b0 < b1 && sk_i < n_work && wpre[sk_i] < b1) {
+        const int64_t w0 = wpre[sk_i], w1 = wpre[sk_i + 1];
+        const int64_t t = order[sk_i];
+        const int64_t ms = mstart[t], cnt = mcount[t];
+        int64_t wa = w0;
+        const int64_t ea = w0 >= b0 ? 0 : find_entry(ment + ms, cnt, w0, b0, &wa);
+        int64_t wb = w1;
+        const int64_t eb = w1 <= b1 ? cnt : ea + find_entry(ment + ms + ea, cnt - ea, wa, b1, &wb);
+        ++sk_i;
+        if (ea < eb) {
+          ti.t = t;
+          ti.i = sk_i - 1;
+          ti.e0 = ms + ea;
+          ti.e1 = ms + eb;
+          ti.part = (ea > 0 || eb < cnt) ? 1 : 0;
+          break;
+        }
+      }
+      return ti;
+    };
     TileInfo nxt;
-    {
+    if (streamk) {
+      nxt = sk_next();
+    } else {
       unsigned int idx = 0;
       if (lane == 0) idx = atomicAdd(sched, 1u);
-      nxt = tile_info(order, mstart, mcount, __shfl_sync(0xffffffffu, idx, 0), n_tiles);
+      nxt = tile_info(order, mstart, mcount, __shfl_sync(0xffffffffu, idx, 0), n_work);
     }
     auto next_stage = [&]() {
       if (++s == kStages) {
@@ -177,9 +292,13 @@ __global__ void __launch_bounds__(kThreads, kCtas)
       const TileInfo cur = nxt;
       const unsigned long long tc0 = prof ? clock64() : 0;
       if (cur.t >= 0) {
-        unsigned int idx = 0;
-        if (lane == 0) idx = atomicAdd(sched, 1u);
-        nxt = tile_info(order, mstart, mcount, __shfl_sync(0xffffffffu, idx, 0), n_tiles);
+        if (streamk) {
+          nxt = sk_next();
+        } else {
+          unsigned int idx = 0;
+          if (lane == 0) idx = atomicAdd(sched, 1u);
+          nxt = tile_info(order, mstart, mcount, __shfl_sync(0xffffffffu, idx, 0), n_work);
+        }
       }
       if (prof) p_claim += clock64() - tc0;
       if (lane == 0) {
@@ -318,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
       const uint32_t srun_addr = smem_u32(srun);
       const uint64_t zdesc = smem_desc(smem_u32(sZero), 0, 0, kLayoutSW64);   // all strides 0: reads the zero atom
       const unsigned long long tk0 = clock64();
-      unsigned long long m_te = 0, m_fu = 0;
+      unsigned long long m_te = 0, m_fu = 0, m_mma = 0, m_cm = 0, n_mma = 0;
       uint32_t ph = 0;
       int64_t tile_it = 0;
       int buf = 0;
@@ -349,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
             dcol = tbase + static_cast<uint32_t>(buf) * 256u;
             umma_f16(dcol, zdesc, zdesc, idesc_full, 0u, 0u, 0u, 0u, 0u);   // D = 0
           }
+          const unsigned long long tm0 = prof ? clock64() : 0;
           if (!(fl & kNoStep) && !(dbg & 1)) {
             // A: K-major, SW64 rows of 32 (SBO 512) or SW128 rows of 64 (SBO 1024); +32 B per K=16
             // B: MN-major SW64 boxes of 32 columns, 32 or 64 rows deep (LBO = box size); +1024 B per K=16
@@ -361,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
             if (nr == 1u && rs.y == kFullRun) {
               umma_f16(dcol, ad, bd, idesc_full, 1u, 0u, 0u, 0u, 0u);
               umma_f16(dcol, ad + 2, bd + 64, idesc_full, 1u, 0u, 0u, 0u, 0u);
+              if (prof) n_mma += 2;
               if (wide) {
                 umma_f16(dcol, ad + 4, bd + 128, idesc_full, 1u, 0u, 0u, 0u, 0u);
                 umma_f16(dcol, ad + 6, bd + 192, idesc_full, 1u, 0u, 0u, 0u, 0u);
@@ -380,13 +501,20 @@ __global__ void __launch_bounds__(kThreads, kCtas)
                 const uint64_t bj = bd + static_cast<uint64_t>(j0 * (box >> 4));
                 const uint32_t d = dcol + j0 * 32u;
                 for (int kk = 0; kk < nk; ++kk) umma_f16(d, ad + 2 * kk, bj + 64 * kk, idesc, 1u, m0, m1, m2, m3);
+                if (prof) n_mma += nk;
               }
             }
           }
+          const unsigned long long tm1 = prof ? clock64() : 0;
           umma_commit(&empty[st]);
           if (fl & kLast) {
             umma_commit(&tfull[buf]);
             ++tile_it;
+          }
+          if (prof) {
+            const unsigned long long tm2 = clock64();
+            m_mma += tm1 - tm0;
+            m_cm += tm2 - tm1;
           }
         }
         ph ^= 1;
@@ -395,6 +523,9 @@ __global__ void __launch_bounds__(kThreads, kCtas)
         prof[blockIdx.x * 16 + 2] = m_te;
         prof[blockIdx.x * 16 + 3] = m_fu;
         prof[blockIdx.x * 16 + 6] = clock64() - tk0;
+        prof[blockIdx.x * 16 + 12] = m_mma;
+        prof[blockIdx.x * 16 + 13] = m_cm;
+        prof[blockIdx.x * 16 + 14] = n_mma;
       }
     }
     __syncwarp();
@@ -409,6 +540,33 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     }
     const int t0 = lane & 3, t1 = lane >> 2;
     unsigned long long e_w = 0, e_d = 0;
+    // one zero-fill unit: 8 rows x 256 columns of an empty macro-tile; false when none is left
+    // units are dealt round-robin to the grid's epilogue warps (no claim atomics: tens of
+    // thousands of same-address atomics serialise in L2)
+    const int64_t n_units = n_empty * 16;
+    const int64_t u_stride = static_cast<int64_t>(gridDim.x) * kEpiWarps;
+    int64_t u_next = static_cast<int64_t>(blockIdx.x) * kEpiWarps + (warp - 4);
+    auto zero_unit = [&]() -> bool {
+      if (u_next >= n_units) return false;
+      const int64_t u = u_next;
+      u_next += u_stride;
+      const int64_t t = order[n_work + u / 16];
+      const int64_t r0 = (t / GN) * 128 + (u % 16) * 8, c0 = (t % GN) * 256;
+      // bulk (TMA-engine) stores of the 1 KB zero buffer: one instruction per row, so the
+      // zero-fill costs the SM a handful of issues instead of 16-byte stores from every lane
+      const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
+      const uint32_t bytes = static_cast<uint32_t>(ncol * 4) & ~15u;
+      if (lane == 0) {
+        for (int r = 0; r < 8; ++r) {
+          const int64_t row = r0 + r;
+          if (row >= M) break;
+          if (bytes) bulk_store_1d(C + row * ldc + c0, sZero, bytes);
+          for (int64_t cc = bytes / 4; cc < ncol; ++cc) C[row * ldc + c0 + cc] = 0.f;
+        }
+        bulk_commit_group();
+      }
+      return true;
+    };
     int tq_s = 0;
     uint32_t tq_ph = 0;
     for (int64_t it = 0;; ++it) {
@@ -424,10 +582,102 @@ __global__ void __launch_bounds__(kThreads, kCtas)
       const int64_t I = cur.t / GN, J = cur.t % GN;
       const int buf = static_cast<int>(it % kBufs);
       const unsigned long long te0 = prof ? clock64() : 0;
-      mbar_wait(&tfull[buf], static_cast<uint32_t>((it / kBufs) & 1));
+      if (!(dbg & 16)) {   // zero-fill empty tiles while waiting for the accumulator
+        const uint32_t par = static_cast<uint32_t>((it / kBufs) & 1);
+        while (!mbar_try_wait(&tfull[buf], par))
+          if (!zero_unit()) {
+            mbar_wait(&tfull[buf], par);
+            break;
+          }
+      } else {
+        mbar_wait(&tfull[buf], static_cast<uint32_t>((it / kBufs) & 1));
+      }
       const unsigned long long te1 = prof ? clock64() : 0;
       e_w += te1 - te0;
       tc_fence_after();
+      if (cur.part) {
+        // ---- stream-K partial tile: own partial -> scratch, ticket, last contributor combines
+        const int64_t w0 = wpre[cur.i], w1 = wpre[cur.i + 1];
+        const int64_t w_last = entry_w(ment[mstart[cur.t] + mcount[cur.t] - 1]);
+        const int64_t c_lo = sk_owner(w0, skW, skG), c_hi = sk_owner(w1 - w_last, skW, skG);
+        float* mine = sk_scratch + sk_slot(skC, c_lo, w0, skW, skG) * (128 * 256);
+#pragma unroll 1
+        for (int hh = 0; hh < 4; ++hh) {
+          const int lh = hh & 1;
+          const int c0 = half * 128 + (hh >> 1) * 64;
+          uint32_t v[32];
+          tmem_ld_16x256b_x8(tbase + ((static_cast<uint32_t>(q * 32 + 16 * lh)) << 16) + buf * 256 + c0, v);
+          tmem_wait_ld();
+          const int ra = q * 32 + 16 * lh + t1, rb = ra + 8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int col = c0 + 8 * i + 2 * t0;
+            __stcg(reinterpret_cast<float2*>(mine + ra * 256 + col),
+                   make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1])));
+            __stcg(reinterpret_cast<float2*>(mine + rb * 256 + col),
+                   make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);   // the accumulator is no longer needed
+        asm volatile("bar.sync 1, 256;" ::: "memory");   // all 8 epilogue warps wrote their part
+        if (warp == 4 && lane == 0) {
+          __threadfence();
+          const unsigned int old = atomicAdd(sk_ticket + cur.i, 1u);
+          const bool last = static_cast<int64_t>(old) == c_hi - c_lo;
+          if (last) sk_ticket[cur.i] = 0u;        // self-reset for the next launch
+          __threadfence();
+          *sk_flag = last ? 1u : 0u;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (*sk_flag) {
+          // partials summed in CTA order c_lo, c_lo+1, ... (deterministic): the first slot is
+          // sk_slot(c_lo), every later contributor's is 2c (its first chunk).  Coalesced:
+          // epilogue thread e handles float4 f = e + 256 m of the 128 x 256 tile.
+          const int64_t I0 = I * 128, J0 = J * 256;
+          const int nc = static_cast<int>(c_hi - c_lo + 1);
+          const float4* src0 = reinterpret_cast<const float4*>(sk_scratch + sk_slot(c_lo, c_lo, w0, skW, skG) * (128 * 256));
+          const float4* srcn = reinterpret_cast<const float4*>(sk_scratch + 2 * (c_lo + 1) * (128 * 256));
+          const int e = static_cast<int>(threadIdx.x) - 128;
+#pragma unroll 1
+          for (int m0 = 0; m0 < 32; m0 += 4) {
+            float4 acc[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc[m] = __ldcg(src0 + e + 256 * (m0 + m));
+            for (int n = 1; n < nc; ++n) {
+              const float4* src = srcn + static_cast<int64_t>(n - 1) * (2 * 128 * 256 / 4);
+              float4 x[4];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) x[m] = __ldcg(src + e + 256 * (m0 + m));
+#pragma unroll
+              for (int m = 0; m < 4; ++m) {
+                acc[m].x += x[m].x;
+                acc[m].y += x[m].y;
+                acc[m].z += x[m].z;
+                acc[m].w += x[m].w;
+              }
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const int f = e + 256 * (m0 + m);
+              const int64_t row = I0 + (f >> 6), gc = J0 + (f & 63) * 4;
+              if (row < M) {
+                float* dst = C + row * ldc + gc;
+                if (gc + 3 < N) {
+                  __stcs(reinterpret_cast<float4*>(dst), acc[m]);
+                } else {
+                  if (gc < N) dst[0] = acc[m].x;
+                  if (gc + 1 < N) dst[1] = acc[m].y;
+                  if (gc + 2 < N) dst[2] = acc[m].z;
+                }
+              }
+            }
+          }
+        }
+        if (prof) e_d += clock64() - te1;
+        continue;
+      }
 #pragma unroll 1
       for (int hh = 0; hh < 4; ++hh) {
         const int lh = hh & 1;                         // lanes [16*lh, 16*lh + 16) of the quadrant
@@ -457,6 +707,9 @@ __global__ void __launch_bounds__(kThreads, kCtas)
       if (lane == 0) mbar_arrive(&tempty[buf]);
       if (prof) e_d += clock64() - te1;
     }
+    while (zero_unit()) {
+    }
+    if (lane == 0) bulk_wait_group<0>();   // zero-fill stores complete before the CTA retires
     if (prof && warp == 4 && lane == 0) {
       prof[blockIdx.x * 16 + 4] = e_w;
       prof[blockIdx.x * 16 + 5] = e_d;
@@ -470,6 +723,72 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
     prof[blockIdx.x * 16 + 9] = g;
   }
+}
+
+// Stream-K weights: wt[i] = sum of entry_w over the entries of the tile at LPT position i
+// (one warp per position), then wpre = exclusive prefix of wt in place (one block, each
+// thread owns kPreR consecutive items), wpre[n] = total.  Empty tiles (the LPT tail) add 0.
+__global__ void __launch_bounds__(256) tile_weight_kernel(const int32_t* __restrict__ order,
+                                                          const int64_t* __restrict__ mstart,
+                                                          const int64_t* __restrict__ mcount,
+                                                          const uint4* __restrict__ ment, int64_t n,
+                                                          int64_t* __restrict__ wt) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t t = order[i], ms = mstart[t], cnt = mcount[t];
+  int64_t w = 0;
+  for (int64_t e = lane; e < cnt; e += 32) w += entry_w(ment[ms + e]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  if (lane == 0) wt[i] = w;
+}
+
+constexpr int kPreThreads = 1024, kPreR = 16;
+__global__ void __launch_bounds__(kPreThreads) lpt_prefix_kernel(int64_t n, int64_t* __restrict__ wpre) {
+  __shared__ int64_t s_warp[kPreThreads / 32];
+  __shared__ int64_t s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += static_cast<int64_t>(kPreThreads) * kPreR) {
+    const int64_t my0 = base + static_cast<int64_t>(threadIdx.x) * kPreR;
+    int64_t v[kPreR], tot = 0;
+#pragma unroll
+    for (int r = 0; r < kPreR; ++r) {
+      v[r] = my0 + r < n ? wpre[my0 + r] : 0;
+      tot += v[r];
+    }
+    int64_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t w = s_warp[lane];
+      int64_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_warp[lane] = wi - w;   // exclusive warp offsets
+    }
+    __syncthreads();
+    int64_t run = s_carry + s_warp[warp] + incl - tot;
+#pragma unroll
+    for (int r = 0; r < kPreR; ++r) {
+      if (my0 + r < n) wpre[my0 + r] = run;
+      run += v[r];
+    }
+    __syncthreads();
+    if (threadIdx.x == kPreThreads - 1) s_carry = run;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) wpre[n] = s_carry;
 }
 
 template <uint32_t kFmt, int kCtas, bool kWide>
@@ -503,16 +822,50 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
   const int64_t n_tiles = (p.row_end_macro - p.row_begin_macro) * p.GN;
   if (n_tiles <= 0) return SPAMM_OK;
   const int64_t slots = static_cast<int64_t>(p.num_sms) * kCtas;
-  const int grid = static_cast<int>(n_tiles < slots ? n_tiles : slots);
+  // stream-K (SPAMM_STREAMK=1) balances the k-step stream exactly but measured slower at the
+  // bench point (partial-tile combine and zero-fill tails); dynamic LPT is default
+  static const bool streamk = getenv("SPAMM_STREAMK") && atoi(getenv("SPAMM_STREAMK")) == 1;
+  // stream-K splits tiles, so it uses every slot even when there are fewer tiles than slots
+  const int grid = static_cast<int>(streamk ? slots : (n_tiles < slots ? n_tiles : slots));
   constexpr int kProfMax = 512;
   static unsigned long long* prof = nullptr;
   if (getenv("SPAMM_DEBUG_UMMA_PROF") && !prof) cudaMalloc(&prof, kProfMax * 16 * 8);
   if (prof && grid > kProfMax) return fail(SPAMM_E_UNSUPPORTED, "profiling supports at most 512 CTAs");
   if (prof) cudaMemsetAsync(prof, 0, kProfMax * 16 * 8, s);
-  SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
+  SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, 2 * sizeof(unsigned int), s));
   static const int dbg = getenv("SPAMM_DEBUG_UMMA_MODE") ? atoi(getenv("SPAMM_DEBUG_UMMA_MODE")) : 0;
+  if (streamk) {
+    const int64_t nmac = p.GM * p.GN;
+    if (p.sk_cap_tiles < nmac + 1 || p.sk_cap_slots < 2 * slots) {
+      if (p.sk_scratch) cudaFree(p.sk_scratch);
+      if (p.sk_ticket) cudaFree(p.sk_ticket);
+      if (p.sk_wpre) cudaFree(p.sk_wpre);
+      p.sk_scratch = nullptr;
+      p.sk_ticket = nullptr;
+      p.sk_wpre = nullptr;
+      p.sk_cap_tiles = p.sk_cap_slots = 0;
+      if (cudaMalloc(&p.sk_scratch, sizeof(float) * 128 * 256 * static_cast<size_t>(2 * slots)) != cudaSuccess ||
+          cudaMalloc(&p.sk_ticket, sizeof(unsigned int) * static_cast<size_t>(nmac + 1)) != cudaSuccess ||
+          cudaMalloc(&p.sk_wpre, sizeof(int64_t) * static_cast<size_t>(nmac + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SPAMM_E_NOMEM, "stream-K workspace allocation failed");
+      }
+      SPAMM_CUDA_TRY(cudaMemset(p.sk_ticket, 0, sizeof(unsigned int) * static_cast<size_t>(nmac + 1)));
+      p.sk_cap_tiles = nmac + 1;
+      p.sk_cap_slots = 2 * slots;
+    }
+    // LPT order of the multiplied macro-row range: weights, then their prefix
+    tile_weight_kernel<<<static_cast<unsigned>((n_tiles + 7) / 8), 256, 0, s>>>(p.order, p.mstart, p.Uw, p.macro_run,
+                                                                             n_tiles, p.sk_wpre);
+    lpt_prefix_kernel<<<1, kPreThreads, 0, s>>>(n_tiles, p.sk_wpre);
+    count_launch(2);
+    SPAMM_CUDA_TRY(cudaGetLastError());
+  }
   kern<<<grid, kThreads, kSmemBytes, s>>>(mp, use3d, p.mstart, p.Uw, p.macro_run, p.order,
-                                                                 n_tiles, p.GN, C, ldc, p.M, p.N, p.sched, prof, dbg);
+                                                                 n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
+                                                                 (streamk || (dbg & 32)) ? p.hist : nullptr,
+                                                                 streamk ? p.sk_wpre : nullptr, p.sk_scratch, p.sk_ticket,
+                                                                 prof, dbg);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (prof) {
@@ -545,7 +898,14 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
             "[umma prof] cycles/CTA: MMA thread %.0f (min %.0f max %.0f) tmem-empty wait %.0f stage-full wait %.0f | "
             "producer %.0f stage-empty wait %.0f | epilogue tmem-full wait %.0f drain %.0f\n",
             acc[6], mn, mx, acc[2], acc[3], acc[7], acc[1], acc[4], acc[5]);
-    fprintf(stderr, "[umma prof] producer claim %.0f\n", acc[11]);
+    fprintf(stderr, "[umma prof] producer claim %.0f | MMA-issue section %.0f commit %.0f MMAs/CTA %.0f\n", acc[11],
+            acc[12], acc[13], acc[14]);
+    if (getenv("SPAMM_DEBUG_UMMA_PROF_CTA")) {
+      for (int c = 0; c < grid; ++c)
+        fprintf(stderr, "[umma cta] %d mma %llu nmma %llu full %llu tempty %llu epi_wait %llu drain %llu start %.2f end %.2f\n", c,
+                h[c * 16 + 6], h[c * 16 + 14], h[c * 16 + 3], h[c * 16 + 2], h[c * 16 + 4], h[c * 16 + 5],
+                (h[c * 16 + 8] - g0) * 1e-3, (h[c * 16 + 9] - g0) * 1e-3);
+    }
   }
   return SPAMM_OK;
 }

@@ -68,6 +68,9 @@ struct NormJob {
   int64_t out_rs, out_cs;      // out[it*rs + kt*cs]
   int64_t r0, nrow;            // tile rows [r0, r0+nrow)
   int64_t ncb;                 // CTAs along the columns
+  int bpc;                     // column boxes per CTA (<= kBoxesPerCta; fewer for small grids)
+  double* out2;                // optional second map (A == B: nB^T from A's tiles), or nullptr
+  int64_t out2_rs, out2_cs;
 };
 
 // grid = (max ncb, nrowA + nrowB); blockIdx.y < nrowA -> job A else job B.
@@ -90,9 +93,9 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
   const CUtensorMap* tm = isA ? &tmA : &tmB;
   const int64_t it = j.r0 + (isA ? blockIdx.y : blockIdx.y - ja.nrow);
   if (static_cast<int64_t>(blockIdx.x) >= j.ncb) return;
-  const int64_t box0 = static_cast<int64_t>(blockIdx.x) * kBoxesPerCta;
+  const int64_t box0 = static_cast<int64_t>(blockIdx.x) * j.bpc;
   const int64_t nbox_total = (j.cols + kCols - 1) / kCols;
-  const int nbox = static_cast<int>(nbox_total - box0 < kBoxesPerCta ? nbox_total - box0 : kBoxesPerCta);
+  const int nbox = static_cast<int>(nbox_total - box0 < j.bpc ? nbox_total - box0 : j.bpc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
@@ -131,7 +134,11 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
   for (int t = threadIdx.x; t < nbox * TPB; t += kThreads) {
     const double tot = ((part[0][t] + part[1][t]) + part[2][t]) + part[3][t];
     const int64_t kt = box0 * TPB + t;
-    if (kt * 32 < j.cols) j.out[it * j.out_rs + kt * j.out_cs] = sqrt(tot);
+    if (kt * 32 < j.cols) {
+      const double nrm = sqrt(tot);
+      j.out[it * j.out_rs + kt * j.out_cs] = nrm;
+      if (j.out2) j.out2[it * j.out2_rs + kt * j.out2_cs] = nrm;
+    }
   }
 }
 
@@ -140,13 +147,30 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
                       int64_t bj0, int64_t bj1, cudaStream_t s, CUtensorMapDataType dt) {
   constexpr int kCols = kBoxBytesRow / sizeof(T);
   CUtensorMap tA{}, tB{};
-  NormJob ja{p.M, p.K, p.nA, p.BK, 1, ar0, ar1 - ar0, 0};
+  NormJob ja{p.M, p.K, p.nA, p.BK, 1, ar0, ar1 - ar0, 0, kBoxesPerCta, nullptr, 0, 0};
   // B column strip [bj0*32, bj1*32): treated as a (K x cols) matrix; tile row k, tile col j -> nBt[j*BK + k]
   const int64_t bcols = std::min<int64_t>(p.N, bj1 * kTile) - bj0 * kTile;
-  NormJob jb{p.K, bcols > 0 ? bcols : 0, p.nBt + bj0 * p.BK, 1, p.BK, 0, bj1 > bj0 ? p.BK : 0, 0};
-  const int64_t per_cta = static_cast<int64_t>(kBoxesPerCta) * kCols;
-  ja.ncb = ja.nrow > 0 ? (ja.cols + per_cta - 1) / per_cta : 0;
-  jb.ncb = jb.nrow > 0 ? (jb.cols + per_cta - 1) / per_cta : 0;
+  NormJob jb{p.K, bcols > 0 ? bcols : 0, p.nBt + bj0 * p.BK, 1, p.BK, 0, bj1 > bj0 ? p.BK : 0, 0, kBoxesPerCta, nullptr, 0, 0};
+  // B is A (same square matrix, same layout, full ranges): read it once.  Tile (r, c) of A is
+  // tile (k = r, j = c) of B, so its norm is also nB^T[c*BK + r] (C = A*A, e.g. matrix powers).
+  if (A == B && lda == ldb && p.M == p.K && p.K == p.N && ar0 == 0 && ar1 == p.BM && bj0 == 0 && bj1 == p.BN) {
+    ja.out2 = p.nBt;
+    ja.out2_rs = 1;
+    ja.out2_cs = p.BK;
+    jb.nrow = 0;
+  }
+  // boxes per CTA: 8 (128 KB streamed per CTA) unless that leaves fewer than ~4 CTAs per SM,
+  // then fewer so that small problems are not latency-bound on a handful of CTAs
+  int bpc = kBoxesPerCta;
+  auto ncb_of = [&](const NormJob& jj, int b) -> int64_t {
+    const int64_t per_cta = static_cast<int64_t>(b) * kCols;
+    return jj.nrow > 0 ? (jj.cols + per_cta - 1) / per_cta : 0;
+  };
+  while (bpc > 1 && ncb_of(ja, bpc) * ja.nrow + ncb_of(jb, bpc) * jb.nrow < 4 * static_cast<int64_t>(p.num_sms))
+    bpc >>= 1;
+  ja.bpc = jb.bpc = bpc;
+  ja.ncb = ncb_of(ja, bpc);
+  jb.ncb = ncb_of(jb, bpc);
   if (ja.nrow > 0)
     SPAMM_TRY(encode_tmap_2d(&tA, dt, sizeof(T), A, p.K, p.M, lda, kCols, 32, CU_TENSOR_MAP_SWIZZLE_NONE));
   if (jb.nrow > 0) {

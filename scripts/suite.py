@@ -2,7 +2,7 @@
 """Measurement suite over every BASELINE.json config on one GPU.
 
 For each workload and tau: per-stage device times (CUDA events recorded by the library,
-median over reps, L2 flushed by a 512 MB write before every rep), total time,
+median over reps, L2 flushed by a 512 MB write + 512 MB read before every rep), total time,
 dense-equivalent TFLOP/s (2MNK/t), kept TFLOP/s (2*32^3*P/t), the multiply's fraction of
 its roofline (BF16 burst peak from MEASURED_PEAKS.json; FP32 = 148 SMs x 128 FMA x 2 x max
 clock), the norm stage's HBM fraction, and cuBLAS dense GEMM (torch.matmul) on the same
@@ -41,11 +41,12 @@ def peaks():
 
 
 PK = None
-FLUSH = None
+FLUSH = FLUSH_RD = FLUSH_OUT = None
 
 
 def flush():
-    FLUSH.zero_()
+    FLUSH.zero_()                        # evict (write 512 MB) ...
+    torch.sum(FLUSH_RD, dim=0, out=FLUSH_OUT)   # ... then write the dirty lines back outside the timing
 
 
 def dev(x, prec):
@@ -102,7 +103,8 @@ def measure(name, A, B, prec, taus, reps, dense_ms=None):
             stages = {k: statistics.median(v) for k, v in st_ms.items()}
             kept_fl = 2.0 * T ** 3 * st["kept"]
             mul_peak = PK["fp32"] if prec == "fp32" else PK["bf16"]
-            norm_bytes = (M * K + K * N) * es
+            same = A.data_ptr() == B.data_ptr() and A.stride() == B.stride() and M == K == N
+            norm_bytes = (M * K + (0 if same else K * N)) * es   # A = B is read once (norms.cu)
             row = {"config": name, "precision": prec, "M": M, "N": N, "K": K, "tau": tau,
                    "kept": st["kept"], "valid_ratio": st["valid_ratio"], "ms": ms, "stages_ms": stages,
                    "tflops_dense_equiv": 2.0 * M * N * K / (ms / 1e3) / 1e12,
@@ -137,7 +139,7 @@ def cfg_toeplitz(name, kind, lam, c, N, taus, reps, precs, device_gen=False):
 
 
 def main():
-    global PK, FLUSH
+    global PK, FLUSH, FLUSH_RD, FLUSH_OUT
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4a,4b,5")
     ap.add_argument("--reps", type=int, default=5)
@@ -146,6 +148,8 @@ def main():
     args = ap.parse_args()
     PK = peaks()
     FLUSH = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    FLUSH_RD = torch.zeros(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    FLUSH_OUT = torch.empty((), dtype=torch.float32, device="cuda")
     precs = args.precs.split(",")
     cfgs = args.configs.split(",")
     res = {"peaks": PK, "device": torch.cuda.get_device_name(0), "rows": []}

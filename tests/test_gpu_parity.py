@@ -310,3 +310,22 @@ def test_sync_skipmap_path(sp, prec, shape):
     assert diff == 0
     err = _rel_fro(C, oracle.spamm(A, B, tau, T, nA, nB))
     assert err <= (2e-6 if prec == "fp32" else 1e-5), err
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("N", [256, 1000])
+def test_aliased_a_equals_b_norms(sp, prec, N):
+    """A and B the same buffer (C = A*A): the norm kernel reads it once and writes both maps;
+    they must be bit-identical to normalising a separate copy as B."""
+    A = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=51), prec)
+    Ad = _dev(A, prec)
+    Bd = Ad.clone()
+    p1 = sp.Plan(N, N, N, 0.0, prec)
+    p1.norms(Ad, Ad)
+    p2 = sp.Plan(N, N, N, 0.0, prec)
+    p2.norms(Ad, Bd)
+    a1, bt1 = sp.spamm_get_norms(p1.handle)
+    a2, bt2 = sp.spamm_get_norms(p2.handle)
+    assert torch.equal(a1, a2) and torch.equal(bt1, bt2)
+    assert torch.equal(bt1, a1.T)
+    np.testing.assert_allclose(a1.cpu().numpy(), oracle.tile_norms(A, T), rtol=1e-12, atol=0)
