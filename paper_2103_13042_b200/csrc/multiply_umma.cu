@@ -136,7 +136,7 @@ __device__ __forceinline__ int64_t find_entry(const uint4* __restrict__ ent, int
 }
 
 struct Maps {   // A (32- and 64-deep boxes); B as stacked 32-column boxes, 1..8 boxes, 32- or 64-deep
-  CUtensorMap a1, a2, b1[4], b2[4], b2d;
+  CUtensorMap a1, a2, b1[4], b2[4], b2d, b64, b64w;
 };
 
 template <uint32_t kFmt, int kCtas, bool kWide>
@@ -339,6 +339,12 @@ __global__ void __launch_bounds__(kThreads, kCtas)
             uint8_t* adst = smem + s * kStageBytes;
             if (dbg & 2) {
               mbar_arrive(&full[s]);   // debug: no loads
+            } else if (use3d == 2) {
+              // B in 64-column (128-byte-row) atoms: those covering the needed column tiles
+              const int c0 = __ffs(cols) - 1, c1 = 32 - __clz(cols);
+              const int na = ((c1 + 1) >> 1) - (c0 >> 1);
+              mbar_arrive_expect_tx(&full[s], (wide ? 2 : 1) * (8192 + 4096 * na));
+              tma_load_2d(adst, wide ? &mp.a2 : &mp.a1, &full[s], k0, I * 128);
             } else if (use3d) {
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
               mbar_arrive_expect_tx(&full[s], (wide ? 2 : 1) * (8192 + 2048 * len));
@@ -360,11 +366,17 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     }
   } else if (warp == 3) {
     // --------------------------------------------------------------- producer B
-    if (lane == 0)
-      for (int q = 0; q < 4; ++q) {
-        tma_prefetch_desc(&mp.b1[q]);
-        tma_prefetch_desc(&mp.b2[q]);
+    if (lane == 0) {
+      if (use3d == 2) {
+        tma_prefetch_desc(&mp.b64);
+        tma_prefetch_desc(&mp.b64w);
+      } else {
+        for (int q = 0; q < 4; ++q) {
+          tma_prefetch_desc(&mp.b1[q]);
+          tma_prefetch_desc(&mp.b2[q]);
+        }
       }
+    }
     int s = 0;
     uint32_t ph = 0;
     int tq_s = 0;
@@ -400,6 +412,14 @@ __global__ void __launch_bounds__(kThreads, kCtas)
             uint8_t* bdst = smem + s * kStageBytes + kASlot;
             mbar_wait(&empty[s], ph ^ 1);
             if (dbg & 2) {
+            } else if (use3d == 2) {
+              // atom a (columns [64a, 64a+64) of the macro-tile) lands at bdst + a * atom bytes;
+              // 2-D boxes [32|64 k x 64 n] SWIZZLE_128B, TMA zero fill beyond N
+              const int c0 = __ffs(cols) - 1, c1 = 32 - __clz(cols);
+              const int abytes = wide ? 8192 : 4096;
+              const CUtensorMap* bm = wide ? &mp.b64w : &mp.b64;
+              for (int a = c0 >> 1; a < ((c1 + 1) >> 1); ++a)
+                tma_load_2d(bdst + a * abytes, bm, &full[s], J * 256 + a * 64, k0);
             } else if (use3d) {
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
               const int box = wide ? 4096 : 2048;
@@ -475,16 +495,45 @@ __global__ void __launch_bounds__(kThreads, kCtas)
             const uint32_t a_addr = base_addr + st * kStageBytes, b_addr = a_addr + kASlot;
             const bool wide = kWide && (fl >> 31) != 0u;
             const uint64_t ad = wide ? smem_desc(a_addr, 16, 1024, kLayoutSW128) : smem_desc(a_addr, 16, 512, kLayoutSW64);
-            const uint32_t box = wide ? 4096u : 2048u;
-            const uint64_t bd = smem_desc(b_addr, box, 512, kLayoutSW64);
+            const bool b128 = use3d == 2;
+            // bmode 2: B atoms of 64 columns x 32|64 k rows, SW128 (LBO = atom bytes, SBO = 1024,
+            // +2048 B per K=16); bmode 0/1: 32-column SW64 boxes (LBO = box, SBO = 512, +1024 B)
+            const uint32_t box = b128 ? (wide ? 8192u : 4096u) : (wide ? 4096u : 2048u);
+            const uint64_t bd = b128 ? smem_desc(b_addr, box, 1024, kLayoutSW128) : smem_desc(b_addr, box, 512, kLayoutSW64);
+            const uint32_t kstep = b128 ? 128u : 64u;   // descriptor units (16 B) per K=16
             const uint32_t nr = (rs.x >> 16) & 15u;
             if (nr == 1u && rs.y == kFullRun) {
               umma_f16(dcol, ad, bd, idesc_full, 1u, 0u, 0u, 0u, 0u);
-              umma_f16(dcol, ad + 2, bd + 64, idesc_full, 1u, 0u, 0u, 0u, 0u);
+              umma_f16(dcol, ad + 2, bd + kstep, idesc_full, 1u, 0u, 0u, 0u, 0u);
               if (prof) n_mma += 2;
               if (wide) {
-                umma_f16(dcol, ad + 4, bd + 128, idesc_full, 1u, 0u, 0u, 0u, 0u);
-                umma_f16(dcol, ad + 6, bd + 192, idesc_full, 1u, 0u, 0u, 0u, 0u);
+                umma_f16(dcol, ad + 4, bd + 2 * kstep, idesc_full, 1u, 0u, 0u, 0u, 0u);
+                umma_f16(dcol, ad + 6, bd + 3 * kstep, idesc_full, 1u, 0u, 0u, 0u, 0u);
+              }
+            } else if (b128) {
+              const int nk = wide ? 4 : 2;
+              uint32_t cw = rs.y;
+              for (uint32_t rr = 0; rr < nr; ++rr) {
+                if (rr == 3) cw = rs.z;
+                if (rr == 6) cw = rs.w;
+                const uint32_t w = cw & 0x3FFu;
+                cw >>= 10;
+                uint32_t j0 = w & 7u, len = ((w >> 3) & 7u) + 1u;
+                const uint32_t pat = w >> 6;
+                const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;   // 0 keep, ~0 disable
+                const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
+                // a run may start mid-atom (odd j0: +64 B inside the 128-byte swizzled row) but
+                // the N walk only crosses atoms from an atom start: split odd starts of len > 1
+                while (len) {
+                  const uint32_t l = (j0 & 1u) ? 1u : len;
+                  const uint32_t idesc = idesc_base | (l << 19);
+                  const uint64_t bj = bd + (((j0 >> 1) * box + (j0 & 1u) * 64u) >> 4);
+                  const uint32_t d = dcol + j0 * 32u;
+                  for (int kk = 0; kk < nk; ++kk) umma_f16(d, ad + 2 * kk, bj + kstep * kk, idesc, 1u, m0, m1, m2, m3);
+                  if (prof) n_mma += nk;
+                  j0 += l;
+                  len -= l;
+                }
               }
             } else {
               const int nk = wide ? 4 : 2;
@@ -802,8 +851,17 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
   // B as stacked [32|64 k][32 n] boxes: dims {32 n, K, N/32} with strides {ldb, 32} elements
   // (a non-monotonic stride; verified by scripts/probe_tma3d.cu).  Only when N % 32 == 0:
   // the inner 32 columns of the last box must exist.
-  const int use3d = (p.N % 32) == 0;
-  if (use3d) {
+  // B layout: 1 (default) = stacked 32-column 3-D boxes (needs N % 32 == 0, else 0 = one 2-D
+  // 32-column box per needed tile); 2 = 64-column atoms with 128-byte rows (half the TMA
+  // requests per byte; parity-green but measured slower at the bench point: 198 vs 182 us,
+  // the extra columns of partially needed atoms and the split odd-start runs cost more)
+  static const int bmode_env = getenv("SPAMM_UMMA_BMODE") ? atoi(getenv("SPAMM_UMMA_BMODE")) : 1;
+  const int use3d = bmode_env == 2 ? 2 : (bmode_env == 1 && (p.N % 32) == 0 ? 1 : 0);
+  if (use3d == 2) {
+    SPAMM_TRY(encode_tmap_2d(&mp.b64, dt, 2, B, p.N, p.K, ldb, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B));
+    SPAMM_TRY(encode_tmap_2d(&mp.b64w, dt, 2, B, p.N, p.K, ldb, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B));
+  }
+  if (use3d == 1) {
     const uint32_t nbs[4] = {8, 4, 2, 1};
     for (int q = 0; q < 4; ++q) {
       SPAMM_TRY(encode_tmap_3d(&mp.b1[q], dt, B, 32, p.K, p.N / 32, static_cast<uint64_t>(ldb) * 2, 64, 32, 32,

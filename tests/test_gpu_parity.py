@@ -329,3 +329,21 @@ def test_aliased_a_equals_b_norms(sp, prec, N):
     assert torch.equal(a1, a2) and torch.equal(bt1, bt2)
     assert torch.equal(bt1, a1.T)
     np.testing.assert_allclose(a1.cpu().numpy(), oracle.tile_norms(A, T), rtol=1e-12, atol=0)
+
+
+def test_bf16_norms_special_values(sp):
+    """BF16 norms with subnormal, zero, Inf and NaN entries (the integer bf16->f64 fast path
+    must hand these to the exact conversion) vs the oracle."""
+    N = 256
+    A = synth.round_to_bf16(synth.random_matrix(N, N, seed=71))
+    A[3, 5] = np.float32(1e-40)      # bf16 subnormal (rounds to a subnormal bf16)
+    A[40, 70] = np.float32(-3e-39)
+    A[100, 200] = np.inf
+    A[200, 10] = np.nan
+    A[0:32, 32:64] = 0.0
+    A = synth.round_to_bf16(A)
+    plan = sp.Plan(N, N, N, 0.0, "bf16")
+    Bd = _dev(np.ones((N, N), np.float32), "bf16")
+    plan.norms(_dev(A, "bf16"), Bd)
+    got = sp.spamm_get_norms(plan.handle)[0].cpu().numpy()
+    np.testing.assert_allclose(got, oracle.tile_norms(A, T), rtol=1e-12, atol=0, equal_nan=True)
