@@ -74,10 +74,11 @@ def summarise_launches(path, tag):
     starts = [j for j, (_, k, _) in enumerate(recs) if "tile_norms" in k]
     if starts:
         step = recs[starts[-1]:]
-        tot = sum(v for _, k, v in step if "FillFunctor" not in k)
-        out.append("\n# share of one step (L2-flush fill excluded)")
+        flush = lambda k: "FillFunctor" in k or "reduce_kernel" in k   # noqa: E731  (L2 flush write + read)
+        tot = sum(v for _, k, v in step if not flush(k))
+        out.append("\n# share of one step (L2-flush kernels excluded)")
         for _, k, v in step:
-            if "FillFunctor" in k:
+            if flush(k):
                 continue
             out.append(f"{k.split('(')[0][:80]}: {v / 1e3:.1f} us ({100 * v / tot:.1f} %)")
     with open(os.path.join(ROOT, "profiles", f"{tag}_launches.txt"), "w") as f:
