@@ -166,7 +166,7 @@ def _config(args, prec):
 # --------------------------------------------------------------- GPU path ---
 def _device_inputs(N, prec, dev):
     A32 = synth.decay_matrix(N, "exp", LAM)
-    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[prec]
+    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp32x3": torch.float32}[prec]
     A = torch.from_numpy(A32).to(device=dev).to(dt)
     return A32, A
 
@@ -258,17 +258,22 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- roofline of the dominant kernel (device time inside the timed region)
     kept_flops = 2.0 * TILE ** 3 * st["kept"]
-    es = 4 if prec == "fp32" else 2
+    es = 4 if prec in ("fp32", "fp32x3") else 2
     mean = {k: statistics.mean(v) for k, v in stage.items()}
     dominant = max(mean, key=mean.get)
     traffic = _ncu_traffic(prec)
     if dominant == "multiply":
         peak = peaks["bf16_tflops"] if prec != "fp32" else _fp32_peak(peaks)
-        achieved = kept_flops / (mean["multiply"] / 1e3) / 1e12
-        roof = {"kernel": "spamm_mul_umma_kernel" if prec != "fp32" else "spamm_mul_simt_kernel",
+        # fp32x3 executes six BF16 products per kept pair on the tensor cores
+        mma_flops = kept_flops * (6 if prec == "fp32x3" else 1)
+        achieved = mma_flops / (mean["multiply"] / 1e3) / 1e12
+        kname = {"fp32": "spamm_mul_simt_kernel", "fp32x3": "spamm_mul_x3_kernel"}.get(prec, "spamm_mul_umma_kernel")
+        work = (f"6*2*32^3*kept = {mma_flops:.4g} BF16 MMA FLOP (kept={st['kept']})" if prec == "fp32x3"
+                else f"2*32^3*kept = {kept_flops:.4g} FLOP (kept={st['kept']})")
+        roof = {"kernel": kname,
                 "bound": "tensor" if prec != "fp32" else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic.get("multiply"),
-                "work_per_launch": f"2*32^3*kept = {kept_flops:.4g} FLOP (kept={st['kept']})",
+                "work_per_launch": work,
                 "peak_source": peaks["source"] + (" bf16 burst" if prec != "fp32" else
                                                   " FP32 CUDA-core 148 SM x 128 FMA x 2 x sm_max clock")}
     else:
@@ -338,7 +343,7 @@ def _ncu_traffic(prec):
 
 
 def _e2e(sp, A32, prec, N, tau, args, stream, flush, world, rank, comm):
-    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[prec]
+    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp32x3": torch.float32}[prec]
     host = torch.from_numpy(A32).to(dt)
     Ah, Bh = host.pin_memory(), host.clone().pin_memory()
     Ch = torch.empty((N, N), dtype=torch.float32).pin_memory()
@@ -371,8 +376,8 @@ def _sweep(sp, N, stream, flush):
     A32 = synth.decay_matrix(N, "exp", LAM)
     dev = torch.device("cuda", torch.cuda.current_device())
     cublas = {}
-    for prec in ("fp32", "bf16"):
-        dt = {"bf16": torch.bfloat16, "fp32": torch.float32}[prec]
+    for prec in ("fp32", "fp32x3", "bf16"):
+        dt = {"bf16": torch.bfloat16, "fp32": torch.float32, "fp32x3": torch.float32}[prec]
         A = torch.from_numpy(A32).to(device=dev).to(dt)
         C = torch.empty((N, N), dtype=torch.float32, device=dev)
         plan = sp.Plan(N, N, N, TAU_SWEEP[0], prec, flags=sp.SPAMM_FLAG_TIMING)
@@ -407,10 +412,13 @@ def _sweep(sp, N, stream, flush):
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
         gemm = lambda: torch.matmul(A, A)  # noqa: E731
-        ms_c = statistics.median(_timed(gemm, 3 if prec == "fp32" else 5, 2, flush, stream))
-        cublas[prec] = {"ms": ms_c, "tflops": 2.0 * N ** 3 / (ms_c / 1e3) / 1e12,
-                        "call": "torch.matmul (cuBLAS), " + ("FP32 SGEMM, TF32 off" if prec == "fp32"
-                                                            else "BF16 in, FP32 accumulate")}
+        if prec == "fp32x3":   # same FP32 inputs and accuracy class: compared with the SGEMM
+            ms_c = cublas["fp32"]["ms"]
+        else:
+            ms_c = statistics.median(_timed(gemm, 3 if prec == "fp32" else 5, 2, flush, stream))
+            cublas[prec] = {"ms": ms_c, "tflops": 2.0 * N ** 3 / (ms_c / 1e3) / 1e12,
+                            "call": "torch.matmul (cuBLAS), " + ("FP32 SGEMM, TF32 off" if prec == "fp32"
+                                                                else "BF16 in, FP32 accumulate")}
         for r in out:
             if r["precision"] == prec:
                 r["speedup_vs_cublas"] = ms_c / r["ms"]
@@ -439,7 +447,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--precision", choices=["bf16", "fp16", "fp32"], default="bf16")
+    ap.add_argument("--precision", choices=["bf16", "fp16", "fp32", "fp32x3"], default="bf16")
     ap.add_argument("--tau", type=float, default=TAU_HEADLINE)
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--ref-rows", type=int, default=16, help="oracle sample (tile rows) per reference step")

@@ -20,6 +20,7 @@
  *     aligned and ld*sizeof(elem) a multiple of 16 (TMA), ld >= number of columns.
  *     A host pointer returns SPAMM_E_INVALID (checked with cudaPointerGetAttributes).
  *   - Element types: SPAMM_FP32 -> float A, B (CUDA-core FP32 multiply);
+ *     SPAMM_FP32X3 -> float A, B (tensor cores on a 3 x bfloat16 split, FP32-accurate);
  *     SPAMM_BF16 / SPAMM_FP16 -> 16-bit A, B (tcgen05 tensor cores, FP32 accumulate).
  *     C is always float (ab_frag is FP32).
  *   - Ragged sizes are allowed: the result equals zero padding to a multiple of
@@ -56,7 +57,14 @@ typedef enum {
 typedef enum {
   SPAMM_FP32 = 0,  /* float inputs, CUDA-core FP32 FMA, two-level FP32 accumulation */
   SPAMM_BF16 = 1,  /* bfloat16 inputs, tcgen05.mma kind::f16, FP32 accumulation in TMEM */
-  SPAMM_FP16 = 2   /* float16 inputs, same tensor-core path as BF16 */
+  SPAMM_FP16 = 2,  /* float16 inputs, same tensor-core path as BF16 */
+  SPAMM_FP32X3 = 3 /* float inputs on the tensor cores: spamm_norms also
+                      splits A and B into three bfloat16 planes a = a0 + a1 + a2 (plan-owned,
+                      6 bytes per element), the multiply sums the six products a0b0 + a0b1 +
+                      a1b0 + a0b2 + a1b1 + a2b0 per kept pair with two-level FP32 accumulation
+                      (TMEM partials of 4 k-steps added in registers).  FP32-level accuracy;
+                      same norms, tau semantics and skip map as SPAMM_FP32.  Single GPU only
+                      (spamm_multiply_mgpu with nranks > 1 returns SPAMM_E_UNSUPPORTED). */
 } spamm_precision;
 
 /* plan flags */

@@ -68,7 +68,7 @@ spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void
 }
 
 // --------------------------------------------------------------- validation
-static size_t esize_of(spamm_precision p) { return p == SPAMM_FP32 ? 4 : 2; }
+static size_t esize_of(spamm_precision p) { return f32_inputs(p) ? 4 : 2; }
 
 static spamm_status check_matrix(const void* ptr, int64_t rows, int64_t cols, int64_t ld, size_t esize,
                                  const char* name) {
@@ -105,7 +105,8 @@ static spamm_status alloc(void** p, size_t bytes) {
 static void free_plan(Plan* p) {
   if (!p) return;
   void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_start, p->L, p->leaf_base, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent, p->macro_run,
-                  p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp, p->sk_scratch, p->sk_ticket, p->sk_wpre};
+                  p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp, p->sk_scratch, p->sk_ticket, p->sk_wpre,
+                  p->planes};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->mstart && p->mstart != p->macro_ptr) cudaFree(p->mstart);
@@ -158,7 +159,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   *out = nullptr;
   if (M <= 0 || N <= 0 || K <= 0) return fail(SPAMM_E_INVALID, "M, N, K must be positive");
   if (!tau_ok(tau)) return fail(SPAMM_E_INVALID, "tau must be finite and >= 0");
-  if (prec != SPAMM_FP32 && prec != SPAMM_BF16 && prec != SPAMM_FP16)
+  if (prec != SPAMM_FP32 && prec != SPAMM_BF16 && prec != SPAMM_FP16 && prec != SPAMM_FP32X3)
     return fail(SPAMM_E_INVALID, "unknown precision");
   if (tile != kTile) {
     if (tile == 64 || tile == 128) return fail(SPAMM_E_UNSUPPORTED, "only tile (LoNum) = 32 is implemented");
@@ -184,10 +185,10 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   const bool fixed_ok = !(flags & SPAMM_FLAG_SYNC_SKIPMAP) &&
                         sizeof(uint16_t) * static_cast<size_t>(BM * BN) * static_cast<size_t>(BK) <= kWorstCaseBudget;
   p->umma_variant = umma_variant_from_env();
-  p->pair = prec != SPAMM_FP32 && fixed_ok && N % 32 == 0 && p->umma_variant == 3;
-  if (prec != SPAMM_FP32 && !p->pair && p->umma_variant == 3) p->umma_variant = 0;
+  p->pair = !f32_inputs(prec) && fixed_ok && N % 32 == 0 && p->umma_variant == 3;
+  if (!f32_inputs(prec) && !p->pair && p->umma_variant == 3) p->umma_variant = 0;
   p->MI = p->pair ? kMacroI_pair : kMacroI;
-  p->MJ = prec == SPAMM_FP32 ? kMacroJ_simt : kMacroJ_umma;
+  p->MJ = f32_inputs(prec) ? kMacroJ_simt : kMacroJ_umma;
   p->GM = (BM + p->MI - 1) / p->MI;
   p->GN = (BN + p->MJ - 1) / p->MJ;
   p->device = dev;
@@ -235,7 +236,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     // (k, mask) entries: 8 bytes, or 16 bytes (k, mask_lo, mask_hi, 0) for 8 x 8 pair tiles
     st = alloc(reinterpret_cast<void**>(&p->macro_ent), (p->pair ? 16 : 8) * static_cast<size_t>(p->macro_cap));
     // tensor-path entries: a pair-path k-step with more than 6 runs takes two entries
-    if (st == SPAMM_OK && prec != SPAMM_FP32)
+    if (st == SPAMM_OK && !f32_inputs(prec))
       st = alloc(reinterpret_cast<void**>(&p->macro_run),
                  sizeof(uint4) * static_cast<size_t>(p->macro_cap) * (p->pair ? 2 : 1));
   }
@@ -262,10 +263,18 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     }
   }
   if (st == SPAMM_OK) {
-    if (p->fixed_regions && prec != SPAMM_FP32 && umma_variant_wide(p->umma_variant))
+    if (p->fixed_regions && !f32_inputs(prec) && umma_variant_wide(p->umma_variant))
       st = alloc(reinterpret_cast<void**>(&p->Uw), sizeof(int64_t) * static_cast<size_t>(nmac + 1));
     else
       p->Uw = p->U;
+  }
+  // FP32X3: the three bfloat16 planes of A and of B (leading dimensions rounded to 8 elements
+  // so every row is 16-byte aligned for TMA)
+  if (st == SPAMM_OK && prec == SPAMM_FP32X3) {
+    p->ldpa = (K + 7) / 8 * 8;
+    p->ldpb = (N + 7) / 8 * 8;
+    st = alloc(reinterpret_cast<void**>(&p->planes),
+               sizeof(uint16_t) * 3 * (static_cast<size_t>(M * p->ldpa) + static_cast<size_t>(K * p->ldpb)));
   }
   if (st == SPAMM_OK && cudaMallocHost(reinterpret_cast<void**>(&p->h_totals), 2 * sizeof(int64_t)) != cudaSuccess)
     st = fail(SPAMM_E_NOMEM, "cudaMallocHost failed");
@@ -363,7 +372,9 @@ spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int
   SPAMM_TRY(check_matrix(C, p.M, p.N, ldc, 4, "C"));
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[4], s));
-  if (p.prec == SPAMM_FP32) {
+  if (p.prec == SPAMM_FP32X3) {
+    SPAMM_TRY(launch_multiply_x3(p, C, ldc, s));
+  } else if (p.prec == SPAMM_FP32) {
     SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
                                    s));
   } else {

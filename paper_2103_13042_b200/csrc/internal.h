@@ -12,6 +12,9 @@ namespace spamm {
 
 constexpr int kTile = 32;   // LoNum; pinned by Table 1
 
+// precisions whose A, B are float (FP32 norms, FP32 skip-map grouping)
+inline bool f32_inputs(spamm_precision p) { return p == SPAMM_FP32 || p == SPAMM_FP32X3; }
+
 // Scheduling macro-tile shapes (in C tiles).  FP32 SIMT: 128x128 (one warp per C tile);
 // tensor path: 128x256 (one UMMA M=128 covers 4 tile rows, N up to 256 = 8 tile cols).
 constexpr int kMacroI = 4;
@@ -58,6 +61,11 @@ struct Plan {
   unsigned int* sk_ticket = nullptr; // [GM*GN] contributors arrived per LPT position (self-resetting)
   int64_t* sk_wpre = nullptr;        // [GM*GN + 1] exclusive prefix of Uw over the LPT order
   int64_t sk_cap_tiles = 0, sk_cap_slots = 0;
+  // SPAMM_FP32X3: bfloat16 split planes a = a0 + a1 + a2, written by the norm stage:
+  // A planes [3][M][ldpa], then B planes [3][K][ldpb] (unused when B is A)
+  uint16_t* planes = nullptr;
+  int64_t ldpa = 0, ldpb = 0;
+  bool b_is_a = false;           // the last spamm_norms saw B == A (planes of A serve both)
   bool fixed_regions = false;    // lists stored in worst-case fixed regions (single-pass skip map)
   int64_t* bucket_pos = nullptr; // [BK+2] descending bucket starts (consumed by emit)
   void* cub_tmp = nullptr;
@@ -112,6 +120,7 @@ int umma_variant_from_env();       // SPAMM_UMMA_VARIANT: 0 (default) 2 CTAs/SM 
 bool umma_variant_wide(int v);     // does the variant consume merged 64-deep k-steps?
 spamm_status launch_multiply_pair(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
+spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s);   // SPAMM_FP32X3
 spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 

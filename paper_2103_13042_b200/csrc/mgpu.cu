@@ -73,9 +73,11 @@ spamm_status spamm_multiply_mgpu(spamm_plan_t h, void* nccl_comm, int rank, int 
   if (nranks <= 0 || rank < 0 || rank >= nranks) return fail(SPAMM_E_INVALID, "bad rank / nranks");
   if (nranks > 1 && !nccl_comm) return fail(SPAMM_E_INVALID, "NCCL communicator is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
+  if (p.prec == SPAMM_FP32X3 && nranks > 1)   // its split planes come from full-range norms
+    return fail(SPAMM_E_UNSUPPORTED, "SPAMM_FP32X3 is single-GPU in this build");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
-  const size_t es = p.prec == SPAMM_FP32 ? 4 : 2;
+  const size_t es = f32_inputs(p.prec) ? 4 : 2;
 
   // 1. inputs from the root (Alg. 4 lines 4 and 7: B to every GPU, A rows)
   if ((flags & SPAMM_MGPU_INPUTS_ON_ROOT) && nranks > 1) {

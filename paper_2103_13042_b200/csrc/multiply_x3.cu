@@ -1,0 +1,341 @@
+// multiply_x3.cu -- stage 3 for SPAMM_FP32X3: FP32 inputs on the tensor cores (SURVEY.md
+// §8(f) f2), same skip semantics as every path: C[i,j] = sum_{kept k, ascending} A[i,k]B[k,j]
+// (PAPER.md:127), C in FP32.
+//
+// Each FP32 input is split by the norm stage into three bfloat16 planes, a = a0 + a1 + a2
+// (a0 = rn(a), a1 = rn(a - a0), a2 = rn(a - a0 - a1); exact to ~2^-24 |a|).  A kept tile
+// pair contributes the six products whose order is at most 2^-16 relative to a0 b0:
+//   a0b0 + a0b1 + a1b0 + a0b2 + a1b1 + a2b0      (dropped: a1b2, a2b1 ~2^-24, a2b2 ~2^-32)
+// so every product is FP32-accurate.  Accumulation is two-level: the tensor core's FP32
+// accumulator in TMEM only ever sums kChunk k-steps (6 x 2 MMAs each); the epilogue adds the
+// chunk partials into a per-thread FP32 running sum with IEEE adds, alternating between two
+// TMEM buffers so the next chunk's MMAs overlap the add.  (A single TMEM accumulation over
+// thousands of MMAs drifts by ~2^-24 per MMA: measured 4e-5 at K = 16384 on the BF16 path.)
+//
+// Layout: one CTA per SM (384 threads: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w4-11 epilogue), 128 x 128 macro-tiles (4 x 4 C tiles: the FP32 path's skip map, entries
+// (k, 16-bit mask)), a 4-deep ring of 48 KB stages holding A[3 planes][128 x 32] (K-major
+// SWIZZLE_64B, one 3-D TMA) and, per needed 32-column tile, B[3 planes][32 x 32] (MN-major
+// SWIZZLE_64B, one 3-D TMA each).  Per k-step the MMA thread decodes the 4 x 4 keep bits into
+// runs of adjacent C-tile columns with equal row patterns and issues, per run, 6 products x 2
+// tcgen05.mma (M = 128, N = 32*run, K = 16) with the disable-output-lane mask of the skipped
+// C-tile rows -- exact leaf-level skipping, as on the BF16 path.
+#include <cstring>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace spamm {
+namespace {
+
+using namespace sm100;
+
+constexpr int kStages = 4;
+constexpr int kAPlane = 128 * 32 * 2;              // 8 KB
+constexpr int kBBox = 32 * 32 * 2;                 // 2 KB
+constexpr int kBCol = 3 * kBBox;                   // one 32-column tile, 3 planes
+constexpr int kStageA = 3 * kAPlane;               // 24 KB
+constexpr int kStageBytes = kStageA + 4 * kBCol;   // 48 KB
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
+constexpr int kTQ = 4;
+constexpr int kChunk = 4;                          // k-steps per TMEM partial
+constexpr uint32_t kTmemCols = 256;                // 2 buffers x 128 columns
+constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 512 + 1024;
+constexpr uint32_t kFirst = 1u << 29, kLast = 1u << 30, kNoStep = 1u << 28, kEnd = 1u << 27;
+
+struct TileQ {
+  int64_t t, e0, e1;
+};
+
+struct X3Maps {
+  CUtensorMap a, b;   // 3-D: {cols, rows, plane}
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    spamm_mul_x3_kernel(const __grid_constant__ X3Maps mp, const int64_t* __restrict__ mstart,
+                        const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
+                        const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
+                        int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sZero = smem + kStages * kStageBytes;                  // 512-B zero atom (D = 0 MMA)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sZero + 512);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* tq_full = tempty + 2;
+  uint64_t* tq_empty = tq_full + kTQ;
+  uint4* srun = reinterpret_cast<uint4*>(tq_empty + kTQ);        // [kStages] k-step descriptors
+  TileQ* tq = reinterpret_cast<TileQ*>(srun + kStages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTQ);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 512 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
+    for (int q = 0; q < kTQ; ++q) {
+      mbar_init(&tq_full[q], 1);
+      mbar_init(&tq_empty[q], kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&mp.a);
+      tma_prefetch_desc(&mp.b);
+    }
+    int s = 0, tq_s = 0;
+    uint32_t ph = 0, tq_ph = 0;
+    auto claim = [&]() -> TileQ {
+      unsigned int idx = 0;
+      if (lane == 0) idx = atomicAdd(sched, 1u);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      TileQ ti{-1, 0, 0};
+      if (static_cast<int64_t>(idx) < n_tiles) {
+        ti.t = order[idx];
+        ti.e0 = mstart[ti.t];
+        ti.e1 = ti.e0 + mcount[ti.t];
+      }
+      return ti;
+    };
+    TileQ nxt = claim();
+    for (;;) {
+      const TileQ cur = nxt;
+      if (cur.t >= 0) nxt = claim();
+      if (lane == 0) {   // publish the tile (or the end marker) to the epilogue
+        mbar_wait(&tq_empty[tq_s], tq_ph ^ 1);
+        tq[tq_s] = cur;
+        mbar_arrive(&tq_full[tq_s]);
+      }
+      if (++tq_s == kTQ) {
+        tq_s = 0;
+        tq_ph ^= 1;
+      }
+      if (cur.t < 0 || cur.e1 == cur.e0) {   // end of stream / a tile without k-steps (C = 0)
+        if (lane == 0) {
+          mbar_wait(&empty[s], ph ^ 1);
+          srun[s] = make_uint4(0, 0, 0, cur.t < 0 ? kEnd : (kFirst | kLast | kNoStep));
+          mbar_arrive(&full[s]);
+        }
+        if (++s == kStages) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (cur.t < 0) break;
+        continue;
+      }
+      const int32_t I = static_cast<int32_t>(cur.t / GN), J = static_cast<int32_t>(cur.t % GN);
+      if (lane == 0) {
+        for (int64_t e = cur.e0; e < cur.e1; ++e) {
+          const uint2 en = ment[e];
+          const uint32_t mask = en.y & 0xFFFFu;
+          const uint32_t cols = (mask | (mask >> 4) | (mask >> 8) | (mask >> 12)) & 0xFu;   // needed C-tile columns
+          const int32_t k0 = static_cast<int32_t>(en.x) * 32;
+          mbar_wait(&empty[s], ph ^ 1);
+          srun[s] = make_uint4(en.x, mask, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
+          uint8_t* st = smem + s * kStageBytes;
+          mbar_arrive_expect_tx(&full[s], kStageA + kBCol * __popc(cols));
+          tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
+#pragma unroll
+          for (int lj = 0; lj < 4; ++lj)
+            if ((cols >> lj) & 1u) tma_load_3d(st + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+      // (s, ph) are only meaningful in lane 0, which issues every stage operation
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t base_addr = smem_u32(smem);
+      const uint64_t zdesc = smem_desc(smem_u32(sZero), 0, 0, kLayoutSW64);
+      const uint32_t idesc_zero = idesc_f16(1, 128, 128, 0, 1);
+      const uint32_t pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0};
+      uint32_t ph = 0, ub[2] = {0, 0};
+      int buf = 0;
+      int64_t kin = 0;   // k-steps of the current tile issued so far
+      bool fin = false;
+      while (!fin) {
+#pragma unroll 1
+        for (int st = 0; st < kStages; ++st) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint4 rs = srun[st];
+          const uint32_t fl = rs.w;
+          if (fl & kEnd) {
+            fin = true;
+            break;
+          }
+          if (fl & kFirst) kin = 0;
+          const uint32_t dcol = tbase + static_cast<uint32_t>(buf) * 128u;
+          if ((kin % kChunk) == 0) {   // chunk start: a drained buffer, zeroed
+            mbar_wait(&tempty[buf], ub[buf] & 1u);
+            tc_fence_after();
+            umma_f16(dcol, zdesc, zdesc, idesc_zero, 0u, 0u, 0u, 0u, 0u);
+          }
+          if (!(fl & kNoStep)) {
+            const uint32_t a_addr = base_addr + st * kStageBytes, b_addr = a_addr + kStageA;
+            const uint64_t ad = smem_desc(a_addr, 16, 512, kLayoutSW64);
+            const uint64_t bd = smem_desc(b_addr, kBCol, 512, kLayoutSW64);
+            const uint32_t mask = rs.y;
+            uint32_t j = 0;
+            while (j < 4) {
+              const uint32_t pat = ((mask >> j) & 1u) | (((mask >> (4 + j)) & 1u) << 1) |
+                                   (((mask >> (8 + j)) & 1u) << 2) | (((mask >> (12 + j)) & 1u) << 3);
+              uint32_t j1 = j + 1;
+              while (j1 < 4) {
+                const uint32_t p1 = ((mask >> j1) & 1u) | (((mask >> (4 + j1)) & 1u) << 1) |
+                                    (((mask >> (8 + j1)) & 1u) << 2) | (((mask >> (12 + j1)) & 1u) << 3);
+                if (p1 != pat) break;
+                ++j1;
+              }
+              if (pat) {
+                const uint32_t len = j1 - j;
+                const uint32_t idesc = idesc_f16(1, 128, 0, 0, 1) | ((len * 4u) << 17);   // N = 32 len
+                const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
+                const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
+                const uint32_t d = dcol + j * 32u;
+#pragma unroll
+                for (int p = 0; p < 6; ++p) {
+                  const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
+                  const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
+                  umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
+                  umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
+                }
+              }
+              j = j1;
+            }
+          }
+          umma_commit(&empty[st]);
+          ++kin;
+          if ((fl & kLast) || (kin % kChunk) == 0) {   // chunk complete: hand the buffer over
+            umma_commit(&tfull[buf]);
+            ++ub[buf];
+            buf ^= 1;
+          }
+        }
+        ph ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3;             // TMEM lane quadrant
+    const int half = (warp - 4) >> 2;   // columns [64*half, 64*half + 64)
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&tempty[0]);
+      mbar_arrive(&tempty[1]);
+    }
+    const int t0 = lane & 3, t1 = lane >> 2;
+    uint32_t eu[2] = {0, 0};
+    int buf = 0, tq_s = 0;
+    uint32_t tq_ph = 0;
+    for (;;) {
+      mbar_wait(&tq_full[tq_s], tq_ph);
+      const TileQ cur = tq[tq_s];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tq_empty[tq_s]);
+      if (++tq_s == kTQ) {
+        tq_s = 0;
+        tq_ph ^= 1;
+      }
+      if (cur.t < 0) break;
+      const int64_t U = cur.e1 - cur.e0;
+      const int64_t nch = U > 0 ? (U + kChunk - 1) / kChunk : 1;
+      float acc[64];
+      for (int64_t c = 0; c < nch; ++c) {
+        mbar_wait(&tfull[buf], eu[buf] & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int lh = 0; lh < 2; ++lh) {
+          uint32_t v[32];
+          tmem_ld_16x256b_x8(tbase + ((static_cast<uint32_t>(q * 32 + 16 * lh)) << 16) + buf * 128 + half * 64, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[32 * lh + i] = c == 0 ? __uint_as_float(v[i]) : acc[32 * lh + i] + __uint_as_float(v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        ++eu[buf];
+        buf ^= 1;
+      }
+      const int64_t I = cur.t / GN, J = cur.t % GN;
+#pragma unroll
+      for (int lh = 0; lh < 2; ++lh) {
+        const int64_t ra = I * 128 + q * 32 + 16 * lh + t1, rb = ra + 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int64_t col = J * 128 + half * 64 + 8 * i + 2 * t0;
+          const float v0 = acc[32 * lh + 4 * i], v1 = acc[32 * lh + 4 * i + 1];
+          const float v2 = acc[32 * lh + 4 * i + 2], v3 = acc[32 * lh + 4 * i + 3];
+          if (col + 1 < N) {
+            if (ra < M) __stcs(reinterpret_cast<float2*>(C + ra * ldc + col), make_float2(v0, v1));
+            if (rb < M) __stcs(reinterpret_cast<float2*>(C + rb * ldc + col), make_float2(v2, v3));
+          } else if (col < N) {
+            if (ra < M) C[ra * ldc + col] = v0;
+            if (rb < M) C[rb * ldc + col] = v2;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<kTmemCols>(tbase);
+}
+
+}  // namespace
+
+spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) {
+  if (!p.planes) return fail(SPAMM_E_STATE, "FP32X3 split planes missing (spamm_norms not run on this plan)");
+  const uint16_t* pA = p.planes;
+  const uint16_t* pB = p.b_is_a ? p.planes : p.planes + 3 * p.M * p.ldpa;
+  const int64_t ldb = p.b_is_a ? p.ldpa : p.ldpb;
+  X3Maps mp;
+  std::memset(&mp, 0, sizeof(mp));
+  SPAMM_TRY(encode_tmap_3d(&mp.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pA, p.K, p.M, 3,
+                           static_cast<uint64_t>(p.ldpa) * 2, static_cast<uint64_t>(p.M * p.ldpa) * 2, 32, 128, 3,
+                           CU_TENSOR_MAP_SWIZZLE_64B));
+  SPAMM_TRY(encode_tmap_3d(&mp.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pB, p.N, p.K, 3, static_cast<uint64_t>(ldb) * 2,
+                           static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 3, CU_TENSOR_MAP_SWIZZLE_64B));
+  static bool attr_set = false;
+  if (!attr_set) {
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(spamm_mul_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kSmemBytes)));
+    attr_set = true;
+  }
+  const int64_t n_tiles = (p.row_end_macro - p.row_begin_macro) * p.GN;
+  if (n_tiles <= 0) return SPAMM_OK;
+  const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
+  SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
+  spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, p.macro_ent, p.order, n_tiles, p.GN, C,
+                                                         ldc, p.M, p.N, p.sched);
+  count_launch();
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
+}
+
+}  // namespace spamm

@@ -71,7 +71,39 @@ struct NormJob {
   int bpc;                     // column boxes per CTA (<= kBoxesPerCta; fewer for small grids)
   double* out2;                // optional second map (A == B: nB^T from A's tiles), or nullptr
   int64_t out2_rs, out2_cs;
+  uint16_t* planes;            // SPAMM_FP32X3: 3 bfloat16 split planes [3][rows][pld] of this matrix, or nullptr
+  int64_t pld, pcol0;          // plane leading dimension; column offset of this job's strip in the planes
 };
+
+// a = a0 + a1 + a2 in bfloat16, each the RNE of the remaining residual (the residuals are
+// exact in float).  Non-finite a: a0 carries it, a1 = a2 = 0 (products stay Inf/NaN like GEMM).
+__device__ __forceinline__ void split3(float a, uint16_t& h0, uint16_t& h1, uint16_t& h2) {
+  const __nv_bfloat16 b0 = __float2bfloat16_rn(a);
+  const float r1 = a - __bfloat162float(b0);
+  const __nv_bfloat16 b1 = __float2bfloat16_rn(r1);
+  const float r2 = r1 - __bfloat162float(b1);
+  const __nv_bfloat16 b2 = __float2bfloat16_rn(r2);
+  const bool fin = isfinite(__bfloat162float(b0));
+  h0 = __bfloat16_as_ushort(b0);
+  h1 = fin ? __bfloat16_as_ushort(b1) : static_cast<uint16_t>(0);
+  h2 = fin ? __bfloat16_as_ushort(b2) : static_cast<uint16_t>(0);
+}
+template <typename T>
+__device__ __forceinline__ void write_planes(const NormJob&, const uint4&, int64_t, int64_t) {}
+template <>
+__device__ __forceinline__ void write_planes<float>(const NormJob& j, const uint4& raw, int64_t row, int64_t col) {
+  const float* f = reinterpret_cast<const float*>(&raw);
+  uint16_t h[3][4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) split3(f[e], h[0][e], h[1][e], h[2][e]);
+  const int64_t plane = j.rows * j.pld;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const uint2 v = make_uint2(static_cast<uint32_t>(h[q][0]) | (static_cast<uint32_t>(h[q][1]) << 16),
+                               static_cast<uint32_t>(h[q][2]) | (static_cast<uint32_t>(h[q][3]) << 16));
+    *reinterpret_cast<uint2*>(j.planes + q * plane + row * j.pld + j.pcol0 + col) = v;
+  }
+}
 
 // grid = (max ncb, nrowA + nrowB); blockIdx.y < nrowA -> job A else job B.
 template <typename T>
@@ -119,6 +151,10 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
     for (int r = 0; r < 8; ++r) {
       const uint4 raw = *reinterpret_cast<const uint4*>(box + (warp * 8 + r) * kBoxBytesRow + lane * 16);
       acc += sq16<T>(raw);
+      if (j.planes != nullptr) {   // FP32X3: the element's bfloat16 split (rows/cols of the padded planes)
+        const int64_t row = it * 32 + warp * 8 + r, col = (box0 + b) * kCols + lane * (16 / sizeof(T));
+        if (row < j.rows && col < j.pld - j.pcol0) write_planes<T>(j, raw, row, col);
+      }
     }
 #pragma unroll
     for (int o = LPT / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -147,13 +183,25 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
                       int64_t bj0, int64_t bj1, cudaStream_t s, CUtensorMapDataType dt) {
   constexpr int kCols = kBoxBytesRow / sizeof(T);
   CUtensorMap tA{}, tB{};
-  NormJob ja{p.M, p.K, p.nA, p.BK, 1, ar0, ar1 - ar0, 0, kBoxesPerCta, nullptr, 0, 0};
+  NormJob ja{p.M, p.K, p.nA, p.BK, 1, ar0, ar1 - ar0, 0, kBoxesPerCta, nullptr, 0, 0, nullptr, 0, 0};
+  if (p.prec == SPAMM_FP32X3 && p.planes) {
+    ja.planes = p.planes;
+    ja.pld = p.ldpa;
+  }
   // B column strip [bj0*32, bj1*32): treated as a (K x cols) matrix; tile row k, tile col j -> nBt[j*BK + k]
   const int64_t bcols = std::min<int64_t>(p.N, bj1 * kTile) - bj0 * kTile;
-  NormJob jb{p.K, bcols > 0 ? bcols : 0, p.nBt + bj0 * p.BK, 1, p.BK, 0, bj1 > bj0 ? p.BK : 0, 0, kBoxesPerCta, nullptr, 0, 0};
+  NormJob jb{p.K, bcols > 0 ? bcols : 0, p.nBt + bj0 * p.BK, 1, p.BK, 0, bj1 > bj0 ? p.BK : 0, 0, kBoxesPerCta, nullptr, 0, 0,
+             nullptr, 0, 0};
+  if (p.prec == SPAMM_FP32X3 && p.planes) {
+    jb.planes = p.planes + 3 * p.M * p.ldpa;
+    jb.pld = p.ldpb;
+    jb.pcol0 = bj0 * kTile;
+  }
   // B is A (same square matrix, same layout, full ranges): read it once.  Tile (r, c) of A is
   // tile (k = r, j = c) of B, so its norm is also nB^T[c*BK + r] (C = A*A, e.g. matrix powers).
+  const_cast<Plan&>(p).b_is_a = false;
   if (A == B && lda == ldb && p.M == p.K && p.K == p.N && ar0 == 0 && ar1 == p.BM && bj0 == 0 && bj1 == p.BN) {
+    const_cast<Plan&>(p).b_is_a = true;   // FP32X3: A's planes serve as B's
     ja.out2 = p.nBt;
     ja.out2_rs = 1;
     ja.out2_cs = p.BK;
@@ -200,6 +248,7 @@ spamm_status launch_norms2(const Plan& p, const void* A, int64_t lda, int64_t ar
                            int64_t ldb, int64_t bj0, int64_t bj1, cudaStream_t s) {
   switch (p.prec) {
     case SPAMM_FP32:
+    case SPAMM_FP32X3:
       return launch_t<float>(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
     case SPAMM_BF16:
       return launch_t<__nv_bfloat16>(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);

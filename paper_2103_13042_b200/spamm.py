@@ -18,13 +18,14 @@ LIB_PATH = os.path.join(_PKG, "libspamm.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "spamm.h")
 
 SPAMM_OK, SPAMM_E_INVALID, SPAMM_E_UNSUPPORTED, SPAMM_E_CUDA, SPAMM_E_NOMEM, SPAMM_E_NCCL, SPAMM_E_STATE = range(7)
-SPAMM_FP32, SPAMM_BF16, SPAMM_FP16 = 0, 1, 2
+SPAMM_FP32, SPAMM_BF16, SPAMM_FP16, SPAMM_FP32X3 = 0, 1, 2, 3
 SPAMM_FLAG_NONE, SPAMM_FLAG_TIMING, SPAMM_FLAG_SYNC_SKIPMAP = 0, 1, 2
 SPAMM_MUL_AUTO = 1
 SPAMM_MGPU_INPUTS_REPLICATED, SPAMM_MGPU_INPUTS_ON_ROOT, SPAMM_MGPU_GATHER_C = 0, 1, 2
 
-DTYPE_OF = {SPAMM_FP32: torch.float32, SPAMM_BF16: torch.bfloat16, SPAMM_FP16: torch.float16}
-PREC_OF = {"fp32": SPAMM_FP32, "bf16": SPAMM_BF16, "fp16": SPAMM_FP16}
+DTYPE_OF = {SPAMM_FP32: torch.float32, SPAMM_BF16: torch.bfloat16, SPAMM_FP16: torch.float16,
+            SPAMM_FP32X3: torch.float32}
+PREC_OF = {"fp32": SPAMM_FP32, "bf16": SPAMM_BF16, "fp16": SPAMM_FP16, "fp32x3": SPAMM_FP32X3}
 
 
 class SpammError(RuntimeError):
