@@ -10,6 +10,7 @@
  *     stage 1  spamm_norms          tile Frobenius norms, Eq. 2
  *     stage 2  spamm_build_skipmap  per-C-tile surviving k-lists
  *     stage 3  spamm_multiply       C[i,j] = sum_{kept k} A[i,k]B[k,j], alpha=1, beta=0
+ *                                   by default (spamm_set_scalars: C = alpha*SpAMM + beta*C)
  *   Multi-GPU row partitioning of C (Sec. 3.4, Alg. 4): spamm_multiply_mgpu.
  *
  * Conventions (every entry point):
@@ -178,6 +179,15 @@ spamm_status spamm_partition_rows(const int64_t* row_work, int64_t BM, int nrank
 spamm_status spamm_multiply_mgpu(spamm_plan_t p, void* nccl_comm, int rank, int nranks,
                                  const void* A, int64_t lda, const void* B, int64_t ldb,
                                  float* C, int64_t ldc, uint32_t flags, void* stream);
+
+/* General update C = alpha * SpAMM(A, B, tau) + beta * C (the problem statement's alpha and
+ * beta) for every later spamm_multiply / spamm_run /
+ * spamm_multiply_mgpu of this plan.  Defaults alpha = 1, beta = 0.  Applied in the multiply
+ * epilogue in FP32: C = fmaf(alpha, P, beta * C_old); with beta == 0 the old C is never read
+ * (BLAS convention: NaN there does not propagate).  Tiles without kept pairs get beta * C_old.
+ * alpha, beta must be finite (else SPAMM_E_INVALID).  The CTA-pair variant
+ * (SPAMM_UMMA_VARIANT=3) supports only the defaults (else SPAMM_E_UNSUPPORTED at multiply). */
+spamm_status spamm_set_scalars(spamm_plan_t p, double alpha, double beta);
 
 /* ------------------------------------------------------------ tau search --- */
 

@@ -36,7 +36,7 @@ import numpy as np
 __all__ = [
     "pad_to_tiles", "tile_norms", "keep_mask", "skipmap", "spamm", "spamm_tile",
     "spamm_recursive", "valid_ratio", "count_kept", "error_fnorm", "tile_error_bound",
-    "tau_search", "band_count", "dense_product", "macro_lists",
+    "tau_search", "band_count", "dense_product", "macro_lists", "spamm_axpby",
 ]
 
 
@@ -188,6 +188,17 @@ def spamm(A: np.ndarray, B: np.ndarray, tau: float, T: int,
             b = Bp[:, j * T:(j + 1) * T].reshape(BK, T, T)[ks].reshape(-1, T)
             C[i * T:(i + 1) * T, j * T:(j + 1) * T] = a @ b
     return C[:m, :n]
+
+
+def spamm_axpby(A: np.ndarray, B: np.ndarray, tau: float, T: int, alpha: float, beta: float,
+                C0: np.ndarray | None, nA: np.ndarray | None = None, nB: np.ndarray | None = None) -> np.ndarray:
+    """The problem statement in full, ``C = alpha*A*B + beta*C`` with A*B the SpAMM product
+    (the paper then fixes alpha = 1, beta = 0).  float64.  beta == 0 ignores C0
+    entirely (BLAS convention: NaN in C0 does not propagate)."""
+    P = spamm(A, B, tau, T, nA, nB)
+    if beta == 0.0:
+        return alpha * P
+    return alpha * P + beta * np.asarray(C0, dtype=np.float64)
 
 
 def spamm_tile(A: np.ndarray, B: np.ndarray, tau: float, T: int, i: int, j: int,

@@ -310,6 +310,15 @@ spamm_status spamm_set_tau(spamm_plan_t h, double tau) {
   return SPAMM_OK;
 }
 
+spamm_status spamm_set_scalars(spamm_plan_t h, double alpha, double beta) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  if (!std::isfinite(alpha) || !std::isfinite(beta)) return fail(SPAMM_E_INVALID, "alpha and beta must be finite");
+  Plan* p = reinterpret_cast<Plan*>(h);
+  p->alpha = alpha;
+  p->beta = beta;
+  return SPAMM_OK;
+}
+
 }  // extern "C"
 
 namespace spamm {

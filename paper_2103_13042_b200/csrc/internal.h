@@ -26,6 +26,7 @@ struct Plan {
   int64_t M = 0, N = 0, K = 0;
   int32_t tile = kTile;
   double tau = 0.0;
+  double alpha = 1.0, beta = 0.0;   // C = alpha * SpAMM(A, B) + beta * C (spamm_set_scalars)
   spamm_precision prec = SPAMM_FP32;
   uint32_t flags = 0;
   int64_t BM = 0, BK = 0, BN = 0;

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_simt_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
                           const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
-                          const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN) {
+                          const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, const Axpby ab) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* sA = reinterpret_cast<float*>(smem);
@@ -173,13 +173,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (m >= M) continue;
       float* crow = C + m * ldc + n0;
       if (n0 + 8 <= N) {
-        __stcs(reinterpret_cast<float4*>(crow), v0);
-        __stcs(reinterpret_cast<float4*>(crow + 4), v1);
+        __stcs(reinterpret_cast<float4*>(crow), axpby4(ab, v0, crow));
+        __stcs(reinterpret_cast<float4*>(crow + 4), axpby4(ab, v1, crow + 4));
       } else {
         const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (n0 + j < N) crow[j] = vv[j];
+          if (n0 + j < N) crow[j] = axpby1(ab, vv[j], crow + j);
       }
     }
   }
@@ -204,7 +204,8 @@ spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const fl
   if (n_tiles <= 0) return SPAMM_OK;
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
   spamm_mul_simt_kernel<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.mstart, p.U, p.macro_ent,
-                                                           p.order, n_tiles, p.GN);
+                                                           p.order, n_tiles, p.GN,
+                                                           Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)});
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

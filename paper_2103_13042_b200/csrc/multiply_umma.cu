@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
                           int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
                           const int64_t* __restrict__ n_empty_p, const int64_t* __restrict__ wpre,
                           float* __restrict__ sk_scratch, unsigned int* __restrict__ sk_ticket,
-                          unsigned long long* __restrict__ prof, int dbg) {
+                          const Axpby ab, unsigned long long* __restrict__ prof, int dbg) {
   using C_ = Cfg<kCtas, kWide>;
   // The LPT order lists macro-tiles by descending union length, so the tiles without any
   // kept pair (C = 0 there; often most of a banded product) are its tail.  Default
@@ -714,11 +714,11 @@ __global__ void __launch_bounds__(kThreads, kCtas)
               if (row < M) {
                 float* dst = C + row * ldc + gc;
                 if (gc + 3 < N) {
-                  __stcs(reinterpret_cast<float4*>(dst), acc[m]);
+                  __stcs(reinterpret_cast<float4*>(dst), axpby4(ab, acc[m], dst));
                 } else {
-                  if (gc < N) dst[0] = acc[m].x;
-                  if (gc + 1 < N) dst[1] = acc[m].y;
-                  if (gc + 2 < N) dst[2] = acc[m].z;
+                  if (gc < N) dst[0] = axpby1(ab, acc[m].x, dst);
+                  if (gc + 1 < N) dst[1] = axpby1(ab, acc[m].y, dst + 1);
+                  if (gc + 2 < N) dst[2] = axpby1(ab, acc[m].z, dst + 2);
                 }
               }
             }
@@ -740,14 +740,16 @@ __global__ void __launch_bounds__(kThreads, kCtas)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int64_t col = J * 256 + c0 + 8 * i + 2 * t0;
+          float* ca = C + ra * ldc + col;
+          float* cb = C + rb * ldc + col;
           if (col + 1 < N) {
-            if (ra < M) __stcs(reinterpret_cast<float2*>(C + ra * ldc + col),
-                               make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1])));
-            if (rb < M) __stcs(reinterpret_cast<float2*>(C + rb * ldc + col),
-                               make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])));
+            if (ra < M) __stcs(reinterpret_cast<float2*>(ca),
+                               axpby2(ab, make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1])), ca));
+            if (rb < M) __stcs(reinterpret_cast<float2*>(cb),
+                               axpby2(ab, make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])), cb));
           } else if (col < N) {
-            if (ra < M) C[ra * ldc + col] = __uint_as_float(v[4 * i]);
-            if (rb < M) C[rb * ldc + col] = __uint_as_float(v[4 * i + 2]);
+            if (ra < M) *ca = axpby1(ab, __uint_as_float(v[4 * i]), ca);
+            if (rb < M) *cb = axpby1(ab, __uint_as_float(v[4 * i + 2]), cb);
           }
         }
       }
@@ -882,7 +884,9 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
   const int64_t slots = static_cast<int64_t>(p.num_sms) * kCtas;
   // stream-K (SPAMM_STREAMK=1) balances the k-step stream exactly but measured slower at the
   // bench point (partial-tile combine and zero-fill tails); dynamic LPT is default
-  static const bool streamk = getenv("SPAMM_STREAMK") && atoi(getenv("SPAMM_STREAMK")) == 1;
+  static const bool streamk_env = getenv("SPAMM_STREAMK") && atoi(getenv("SPAMM_STREAMK")) == 1;
+  // (stream-K zero-fills empty tiles with bulk stores: only for beta == 0)
+  const bool streamk = streamk_env && p.beta == 0.0;
   // stream-K splits tiles, so it uses every slot even when there are fewer tiles than slots
   const int grid = static_cast<int>(streamk ? slots : (n_tiles < slots ? n_tiles : slots));
   constexpr int kProfMax = 512;
@@ -921,8 +925,9 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
   }
   kern<<<grid, kThreads, kSmemBytes, s>>>(mp, use3d, p.mstart, p.Uw, p.macro_run, p.order,
                                                                  n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
-                                                                 (streamk || (dbg & 32)) ? p.hist : nullptr,
+                                                                 (streamk || ((dbg & 32) && p.beta == 0.0)) ? p.hist : nullptr,
                                                                  streamk ? p.sk_wpre : nullptr, p.sk_scratch, p.sk_ticket,
+                                                                 Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                                                  prof, dbg);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());

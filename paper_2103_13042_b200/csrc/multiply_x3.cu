@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_x3_kernel(const __grid_constant__ X3Maps mp, const int64_t* __restrict__ mstart,
                         const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
                         const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
-                        int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched) {
+                        int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sZero = smem + kStages * kStageBytes;                  // 512-B zero atom (D = 0 MMA)
@@ -291,12 +291,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t col = J * 128 + half * 64 + 8 * i + 2 * t0;
           const float v0 = acc[32 * lh + 4 * i], v1 = acc[32 * lh + 4 * i + 1];
           const float v2 = acc[32 * lh + 4 * i + 2], v3 = acc[32 * lh + 4 * i + 3];
+          float* ca = C + ra * ldc + col;
+          float* cb = C + rb * ldc + col;
           if (col + 1 < N) {
-            if (ra < M) __stcs(reinterpret_cast<float2*>(C + ra * ldc + col), make_float2(v0, v1));
-            if (rb < M) __stcs(reinterpret_cast<float2*>(C + rb * ldc + col), make_float2(v2, v3));
+            if (ra < M) __stcs(reinterpret_cast<float2*>(ca), axpby2(ab, make_float2(v0, v1), ca));
+            if (rb < M) __stcs(reinterpret_cast<float2*>(cb), axpby2(ab, make_float2(v2, v3), cb));
           } else if (col < N) {
-            if (ra < M) C[ra * ldc + col] = v0;
-            if (rb < M) C[rb * ldc + col] = v2;
+            if (ra < M) *ca = axpby1(ab, v0, ca);
+            if (rb < M) *cb = axpby1(ab, v2, cb);
           }
         }
       }
@@ -332,7 +334,8 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
   SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
   spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, p.macro_ent, p.order, n_tiles, p.GN, C,
-                                                         ldc, p.M, p.N, p.sched);
+                                                         ldc, p.M, p.N, p.sched,
+                                                         Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)});
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;

@@ -285,5 +285,25 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
 }
 constexpr uint32_t kLayoutSW32 = 6u;
 
+// ----------------------------------------------------------- C = alpha*P + beta*C
+// (beta == 0 never reads C, so NaN/garbage there does not propagate -- BLAS rule)
+struct Axpby {
+  float alpha, beta;
+};
+__device__ __forceinline__ float axpby1(const Axpby& s, float p, const float* c) {
+  return s.beta == 0.f ? s.alpha * p : fmaf(s.alpha, p, s.beta * *c);
+}
+__device__ __forceinline__ float2 axpby2(const Axpby& s, float2 p, const float* c) {
+  if (s.beta == 0.f) return make_float2(s.alpha * p.x, s.alpha * p.y);
+  const float2 o = *reinterpret_cast<const float2*>(c);
+  return make_float2(fmaf(s.alpha, p.x, s.beta * o.x), fmaf(s.alpha, p.y, s.beta * o.y));
+}
+__device__ __forceinline__ float4 axpby4(const Axpby& s, float4 p, const float* c) {
+  if (s.beta == 0.f) return make_float4(s.alpha * p.x, s.alpha * p.y, s.alpha * p.z, s.alpha * p.w);
+  const float4 o = *reinterpret_cast<const float4*>(c);
+  return make_float4(fmaf(s.alpha, p.x, s.beta * o.x), fmaf(s.alpha, p.y, s.beta * o.y),
+                     fmaf(s.alpha, p.z, s.beta * o.z), fmaf(s.alpha, p.w, s.beta * o.w));
+}
+
 }  // namespace sm100
 }  // namespace spamm

@@ -75,6 +75,7 @@ def _load():
         "spamm_get_partition": [P, PI64, ctypes.c_int],
         "spamm_get_stats": [P, ctypes.POINTER(spamm_stats)],
         "spamm_count_kept": [P, D, PI64, P],
+        "spamm_set_scalars": [P, D, D],
         "spamm_tau_search": [P, D, D, I32, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I32), P],
     }
     for name, args in sig.items():
@@ -147,6 +148,11 @@ def spamm_plan_destroy(plan) -> None:
 
 def spamm_set_tau(plan, tau: float) -> None:
     _check(_lib.spamm_set_tau(plan, float(tau)))
+
+
+def spamm_set_scalars(plan, alpha: float, beta: float) -> None:
+    """C = alpha * SpAMM(A, B) + beta * C for later multiplies."""
+    _check(_lib.spamm_set_scalars(plan, float(alpha), float(beta)))
 
 
 # ----------------------------------------------------------------- stages ---
@@ -349,6 +355,9 @@ class Plan:
 
     def set_tau(self, tau):
         spamm_set_tau(self.handle, tau)
+
+    def set_scalars(self, alpha, beta):
+        spamm_set_scalars(self.handle, alpha, beta)
 
     def norms(self, A, B, stream=None):
         spamm_norms(self.handle, A, B, stream)

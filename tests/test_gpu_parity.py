@@ -348,3 +348,31 @@ def test_bf16_norms_special_values(sp):
     plan.norms(_dev(A, "bf16"), Bd)
     got = sp.spamm_get_norms(plan.handle)[0].cpu().numpy()
     np.testing.assert_allclose(got, oracle.tile_norms(A, T), rtol=1e-12, atol=0, equal_nan=True)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp32x3"])
+@pytest.mark.parametrize("alpha,beta", [(1.0, 0.0), (-0.5, 0.0), (2.0, 1.5), (1.0, -1.0), (0.0, 0.5)])
+def test_alpha_beta_update(sp, prec, alpha, beta):
+    """C = alpha*SpAMM(A, B) + beta*C vs oracle.spamm_axpby; beta = 0 must not
+    read C (a NaN-filled C stays out of the result)."""
+    M, N, K = 300, 257, 129
+    A = _rounded(synth.perturbed_decay_matrix(K, 0.95, seed=91, m=M), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=92, m=K), prec)
+    C0 = synth.random_matrix(M, N, seed=93)
+    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+    prods = np.unique(nA[:, :, None] * nB[None, :, :])
+    tau = float(0.5 * (prods[len(prods) // 2] + prods[len(prods) // 2 + 1]))
+    plan = sp.Plan(M, N, K, tau, prec)
+    plan.set_scalars(alpha, beta)
+    Cbuf = torch.full((M, -(-N // 4) * 4), float("nan"), dtype=torch.float32, device="cuda")
+    if beta != 0.0:
+        Cbuf[:, :N] = torch.from_numpy(C0).cuda()
+    plan.run(_dev(A, prec), _dev(B, prec), Cbuf[:, :N])
+    torch.cuda.synchronize()
+    got = Cbuf[:, :N].cpu().numpy()
+    ref = oracle.spamm_axpby(A, B, tau, T, alpha, beta, C0, nA, nB)
+    err = _rel_fro(got, ref)
+    assert err <= (1e-5 if prec != "bf16" else 2e-2), err
+    assert err <= 5e-6, err
+    with pytest.raises(sp.SpammError):
+        plan.set_scalars(float("nan"), 0.0)

@@ -319,3 +319,23 @@ def test_generators_deterministic_and_bf16_rne():
     np.testing.assert_array_equal(synth.fp32_to_bf16_bits(x), ref)
     np.testing.assert_array_equal(synth.round_to_bf16(x),
                                   torch.from_numpy(x).to(torch.bfloat16).float().numpy())
+
+
+# ------------------------------------------------------- alpha / beta ---
+def test_axpby_is_the_problem_statement_by_brute_force():
+    """C = alpha*A*B + beta*C at tau = 0, checked entry by entry with explicit
+    loops on a tiny ragged case; beta = 0 ignores a NaN-filled C0 (BLAS convention)."""
+    m, k, n = 5, 7, 3
+    A = synth.random_matrix(m, k, seed=81).astype(np.float64)
+    B = synth.random_matrix(k, n, seed=82).astype(np.float64)
+    C0 = synth.random_matrix(m, n, seed=83).astype(np.float64)
+    alpha, beta = -1.5, 0.25
+    got = oracle.spamm_axpby(A, B, 0.0, 2, alpha, beta, C0)
+    for i in range(m):
+        for j in range(n):
+            s = 0.0
+            for q in range(k):
+                s += A[i, q] * B[q, j]
+            assert abs(got[i, j] - (alpha * s + beta * C0[i, j])) < 1e-12
+    nanC = np.full((m, n), np.nan)
+    assert np.all(np.isfinite(oracle.spamm_axpby(A, B, 0.0, 2, 2.0, 0.0, nanC)))
