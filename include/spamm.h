@@ -77,6 +77,8 @@ typedef enum {
 /* spamm_multiply flags */
 #define SPAMM_MUL_AUTO            1u  /* run spamm_norms + spamm_build_skipmap first (spamm_run) */
 
+#define SPAMM_MUL_OUTPUT_NORMS    2u  /* spamm_multiply_chain: also write the tile norms of the result */
+
 /* spamm_multiply_mgpu flags (Sec. 3.4) */
 #define SPAMM_MGPU_INPUTS_REPLICATED 0u  /* every rank already holds full A and B           */
 #define SPAMM_MGPU_INPUTS_ON_ROOT    1u  /* rank 0 holds A and B; broadcast over NCCL first */
@@ -188,6 +190,30 @@ spamm_status spamm_multiply_mgpu(spamm_plan_t p, void* nccl_comm, int rank, int 
  * alpha, beta must be finite (else SPAMM_E_INVALID).  The CTA-pair variant
  * (SPAMM_UMMA_VARIANT=3) supports only the defaults (else SPAMM_E_UNSUPPORTED at multiply). */
 spamm_status spamm_set_scalars(spamm_plan_t p, double alpha, double beta);
+
+/* ---------------------------------------------------------- chained SpAMM --- */
+/* chains such as matrix powers X <- X*X (ergo's density-matrix purification,
+ * PAPER.md:320) without re-reading C to norm it.  spamm_multiply_chain is spamm_multiply
+ * (flags SPAMM_MUL_AUTO as there) whose epilogue additionally
+ *   - with C_low != NULL (BF16/FP16 plans only; device, row-major, leading dimension ldcl in
+ *     elements): writes C rounded (RNE) to the plan's input type -- the next product's operand;
+ *   - with SPAMM_MUL_OUTPUT_NORMS: writes the float64 tile norms of the written result into a
+ *     plan-owned map nC[BM][BN] (Eq. 2 of the values stored: C, or C_low's rounded values when
+ *     given -- reading R4), readable with spamm_get_output_norms.
+ * FP32X3 plans and the CTA-pair variant return SPAMM_E_UNSUPPORTED. */
+spamm_status spamm_multiply_chain(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
+                                  float* C, int64_t ldc, void* C_low, int64_t ldcl, uint32_t flags,
+                                  void* stream);
+
+/* Device pointer to nC[BM][BN] (row-major float64) of the last spamm_multiply_chain with
+ * SPAMM_MUL_OUTPUT_NORMS (else SPAMM_E_STATE). */
+spamm_status spamm_get_output_norms(spamm_plan_t p, const double** d_nC);
+
+/* Stage 1 from given maps instead of the matrices: nA[BM][BK] and nB[BK][BN] (row-major float64
+ * device arrays, e.g. another plan's output norms) are copied into the plan (nB transposed), which
+ * then behaves as after spamm_norms.  Stream-ordered.  FP32X3 plans: SPAMM_E_UNSUPPORTED (their
+ * norm stage also splits the inputs). */
+spamm_status spamm_set_norms(spamm_plan_t p, const double* nA, const double* nB, void* stream);
 
 /* ------------------------------------------------------------ tau search --- */
 

@@ -102,11 +102,35 @@ static spamm_status alloc(void** p, size_t bytes) {
   return SPAMM_OK;
 }
 
+__global__ void transpose_f64_kernel(const double* __restrict__ in, int64_t rows, int64_t cols,
+                                     double* __restrict__ out) {
+  __shared__ double t[32][33];
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = static_cast<int64_t>(blockIdx.y) * 32 + k;
+    if (r < rows && c < cols) t[k][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  const int64_t r2 = static_cast<int64_t>(blockIdx.y) * 32 + threadIdx.x;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c2 = static_cast<int64_t>(blockIdx.x) * 32 + k;
+    if (r2 < rows && c2 < cols) out[c2 * rows + r2] = t[threadIdx.x][k];
+  }
+}
+
+spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  transpose_f64_kernel<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out);
+  count_launch();
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
+}
+
 static void free_plan(Plan* p) {
   if (!p) return;
   void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_start, p->L, p->leaf_base, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent, p->macro_run,
                   p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp, p->sk_scratch, p->sk_ticket, p->sk_wpre,
-                  p->planes};
+                  p->planes, p->nC};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->mstart && p->mstart != p->macro_ptr) cudaFree(p->mstart);
@@ -424,6 +448,61 @@ spamm_status spamm_multiply(spamm_plan_t h, const void* A, int64_t lda, const vo
     SPAMM_TRY(do_skipmap(p, 0, p.GM, s));
   }
   return do_multiply(p, A, lda, B, ldb, C, ldc, s);
+}
+
+spamm_status spamm_multiply_chain(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
+                                  int64_t ldc, void* C_low, int64_t ldcl, uint32_t flags, void* stream) {
+  if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (C_low != nullptr) {
+    if (f32_inputs(p.prec)) return fail(SPAMM_E_INVALID, "C_low is for BF16/FP16 plans (FP32 C is the next input)");
+    SPAMM_TRY(check_matrix(C_low, p.M, p.N, ldcl, 2, "C_low"));
+  }
+  if (p.prec == SPAMM_FP32X3 || p.pair)
+    return fail(SPAMM_E_UNSUPPORTED, "chained outputs: FP32, BF16, FP16 (non-pair variants) only");
+  if ((flags & SPAMM_MUL_OUTPUT_NORMS) && !p.nC)
+    SPAMM_TRY(alloc(reinterpret_cast<void**>(&p.nC), sizeof(double) * static_cast<size_t>(p.BM * p.BN)));
+  if (flags & SPAMM_MUL_AUTO) {
+    SPAMM_TRY(do_norms(p, A, lda, B, ldb, s));
+    SPAMM_TRY(do_skipmap(p, 0, p.GM, s));
+  }
+  p.out_norms = (flags & SPAMM_MUL_OUTPUT_NORMS) != 0;
+  p.out_low = C_low;
+  p.out_ldl = ldcl;
+  const spamm_status st = do_multiply(p, A, lda, B, ldb, C, ldc, s);
+  p.nc_ready = st == SPAMM_OK && p.out_norms;
+  p.out_norms = false;
+  p.out_low = nullptr;
+  return st;
+}
+
+spamm_status spamm_get_output_norms(spamm_plan_t h, const double** d_nC) {
+  if (!h || !d_nC) return fail(SPAMM_E_INVALID, "plan or output is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  if (!p.nc_ready) return fail(SPAMM_E_STATE, "no spamm_multiply_chain with SPAMM_MUL_OUTPUT_NORMS on this plan");
+  *d_nC = p.nC;
+  return SPAMM_OK;
+}
+
+spamm_status spamm_set_norms(spamm_plan_t h, const double* nA, const double* nB, void* stream) {
+  if (!h || !nA || !nB) return fail(SPAMM_E_INVALID, "plan or norm map is NULL");
+  Plan& p = *reinterpret_cast<Plan*>(h);
+  if (p.prec == SPAMM_FP32X3) return fail(SPAMM_E_UNSUPPORTED, "SPAMM_FP32X3 needs spamm_norms (it also splits A, B)");
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, nA) != cudaSuccess || at.type != cudaMemoryTypeDevice ||
+      cudaPointerGetAttributes(&at, nB) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return fail(SPAMM_E_INVALID, "norm maps must be device pointers");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SPAMM_CUDA_TRY(cudaMemcpyAsync(p.nA, nA, sizeof(double) * static_cast<size_t>(p.BM * p.BK), cudaMemcpyDeviceToDevice, s));
+  SPAMM_TRY(launch_transpose_f64(nB, p.BK, p.BN, p.nBt, s));   // nB [BK][BN] -> nB^T [BN][BK]
+  p.norms_ready = true;
+  p.skipmap_ready = false;
+  p.b_is_a = false;
+  p.last_stream = s;
+  return SPAMM_OK;
 }
 
 spamm_status spamm_run(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,

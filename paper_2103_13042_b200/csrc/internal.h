@@ -27,6 +27,12 @@ struct Plan {
   int32_t tile = kTile;
   double tau = 0.0;
   double alpha = 1.0, beta = 0.0;   // C = alpha * SpAMM(A, B) + beta * C (spamm_set_scalars)
+  // chained SpAMM (spamm_multiply_chain): per-call outputs of the multiply epilogue
+  double* nC = nullptr;             // [BM][BN] tile norms of the last chained C (allocated on first use)
+  bool out_norms = false;
+  void* out_low = nullptr;          // rounded copy of C in the input precision, or nullptr
+  int64_t out_ldl = 0;
+  bool nc_ready = false;
   spamm_precision prec = SPAMM_FP32;
   uint32_t flags = 0;
   int64_t BM = 0, BK = 0, BN = 0;
@@ -126,6 +132,7 @@ spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const voi
                                   int64_t ldc, cudaStream_t s);
 
 size_t skipmap_cub_bytes(int64_t nleaf, int64_t nmac);
+spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s);
 
 // 3-D map: dims {inner, mid, outer} with byte strides {mid_stride, outer_stride}.
 spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,

@@ -518,6 +518,8 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
 
 spamm_status launch_multiply_pair(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s) {
+  if (p.out_norms || p.out_low)
+    return fail(SPAMM_E_UNSUPPORTED, "chained outputs are not implemented for the CTA-pair variant");
   if (p.alpha != 1.0 || p.beta != 0.0)
     return fail(SPAMM_E_UNSUPPORTED, "the CTA-pair variant (SPAMM_UMMA_VARIANT=3) implements alpha = 1, beta = 0 only");
   if (p.prec == SPAMM_BF16) return launch_fmt<1>(p, A, lda, B, ldb, C, ldc, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_simt_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
                           const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
-                          const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, const Axpby ab) {
+                          const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, const Axpby ab,
+                          double* __restrict__ nC, int64_t ldn, int64_t BM, int64_t BN) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* sA = reinterpret_cast<float*>(smem);
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // epilogue: rows I*128 + li*32 + g + 8*rr, cols J*128 + lj*32 + cg*8 .. +7
     const int64_t n0 = J * 128 + lj * 32 + cg * 8;
+    double tsq = 0.0;   // chained SpAMM: this lane's share of the tile's sum of squares
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
       const int64_t m = I * 128 + li * 32 + g + 8 * rr;
@@ -173,14 +175,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (m >= M) continue;
       float* crow = C + m * ldc + n0;
       if (n0 + 8 <= N) {
-        __stcs(reinterpret_cast<float4*>(crow), axpby4(ab, v0, crow));
-        __stcs(reinterpret_cast<float4*>(crow + 4), axpby4(ab, v1, crow + 4));
+        const float4 w0 = axpby4(ab, v0, crow), w1 = axpby4(ab, v1, crow + 4);
+        __stcs(reinterpret_cast<float4*>(crow), w0);
+        __stcs(reinterpret_cast<float4*>(crow + 4), w1);
+        if (nC != nullptr) {
+          const float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int j = 0; j < 8; ++j) tsq += static_cast<double>(ww[j]) * static_cast<double>(ww[j]);
+        }
       } else {
         const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (n0 + j < N) crow[j] = axpby1(ab, vv[j], crow + j);
+          if (n0 + j < N) {
+            const float w = axpby1(ab, vv[j], crow + j);
+            crow[j] = w;
+            tsq += static_cast<double>(w) * static_cast<double>(w);
+          }
       }
+    }
+    if (nC != nullptr) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) tsq += __shfl_xor_sync(0xffffffffu, tsq, o);
+      const int64_t ti = I * 4 + li, tj = J * 4 + lj;
+      if (lane == 0 && ti < BM && tj < BN) nC[ti * ldn + tj] = sqrt(tsq);
     }
   }
 }
@@ -205,7 +223,8 @@ spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const fl
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
   spamm_mul_simt_kernel<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.mstart, p.U, p.macro_ent,
                                                            p.order, n_tiles, p.GN,
-                                                           Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)});
+                                                           Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
+                                                           p.out_norms ? p.nC : nullptr, p.BN, p.BM, p.BN);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

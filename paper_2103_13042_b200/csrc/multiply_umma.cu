@@ -135,6 +135,16 @@ __device__ __forceinline__ int64_t find_entry(const uint4* __restrict__ ent, int
   return base < n ? base : n;
 }
 
+// Chained SpAMM outputs: the tile norms of the written C, and optionally a
+// copy of C rounded to the plan's input precision (the next product's operand); the norms are
+// then those of the rounded values (reading R4).
+struct ChainOut {
+  double* nC;       // [BM][ldn] or nullptr
+  int64_t ldn;
+  void* clow;       // bf16/fp16 copy of C or nullptr
+  int64_t ldl;
+};
+
 struct Maps {   // A (32- and 64-deep boxes); B as stacked 32-column boxes, 1..8 boxes, 32- or 64-deep
   CUtensorMap a1, a2, b1[4], b2[4], b2d, b64, b64w;
 };
@@ -147,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
                           int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
                           const int64_t* __restrict__ n_empty_p, const int64_t* __restrict__ wpre,
                           float* __restrict__ sk_scratch, unsigned int* __restrict__ sk_ticket,
-                          const Axpby ab, unsigned long long* __restrict__ prof, int dbg) {
+                          const Axpby ab, const ChainOut co, unsigned long long* __restrict__ prof, int dbg) {
   using C_ = Cfg<kCtas, kWide>;
   // The LPT order lists macro-tiles by descending union length, so the tiles without any
   // kept pair (C = 0 there; often most of a banded product) are its tail.  Default
@@ -727,6 +737,71 @@ __global__ void __launch_bounds__(kThreads, kCtas)
         if (prof) e_d += clock64() - te1;
         continue;
       }
+      if (co.nC != nullptr || co.clow != nullptr) {
+        // ---- chained output: C (alpha/beta applied), optional rounded copy, tile norms
+        double tsum[4] = {0.0, 0.0, 0.0, 0.0};   // tiles (I*4+q, J*8 + half*4 + t)
+#pragma unroll 1
+        for (int hh = 0; hh < 4; ++hh) {
+          const int lh = hh & 1;
+          const int c0 = half * 128 + (hh >> 1) * 64;
+          uint32_t v[32];
+          tmem_ld_16x256b_x8(tbase + ((static_cast<uint32_t>(q * 32 + 16 * lh)) << 16) + buf * 256 + c0, v);
+          tmem_wait_ld();
+          const int64_t ra = I * 128 + q * 32 + 16 * lh + t1;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int64_t col = J * 256 + c0 + 8 * i + 2 * t0;
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+              const int64_t row = ra + 8 * rr;
+              if (row >= M || col >= N) continue;
+              float* cp = C + row * ldc + col;
+              float2 x = make_float2(__uint_as_float(v[4 * i + 2 * rr]), __uint_as_float(v[4 * i + 2 * rr + 1]));
+              const bool two = col + 1 < N;
+              if (two) {
+                x = axpby2(ab, x, cp);
+                __stcs(reinterpret_cast<float2*>(cp), x);
+              } else {
+                x.x = axpby1(ab, x.x, cp);
+                x.y = 0.f;
+                *cp = x.x;
+              }
+              if (co.clow != nullptr) {   // round to the plan's input type; norms of what is stored
+                if (kFmt == 1) {
+                  __nv_bfloat16* lp = static_cast<__nv_bfloat16*>(co.clow) + row * co.ldl + col;
+                  const __nv_bfloat16 l0 = __float2bfloat16_rn(x.x), l1 = __float2bfloat16_rn(x.y);
+                  lp[0] = l0;
+                  if (two) lp[1] = l1;
+                  x = make_float2(__bfloat162float(l0), __bfloat162float(l1));
+                } else {
+                  __half* lp = static_cast<__half*>(co.clow) + row * co.ldl + col;
+                  const __half l0 = __float2half_rn(x.x), l1 = __float2half_rn(x.y);
+                  lp[0] = l0;
+                  if (two) lp[1] = l1;
+                  x = make_float2(__half2float(l0), __half2float(l1));
+                }
+              }
+              const double d0 = x.x, d1 = two ? static_cast<double>(x.y) : 0.0;
+              tsum[(hh >> 1) * 2 + (i >> 2)] += d0 * d0 + d1 * d1;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (co.nC != nullptr) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            double x = tsum[t];
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            const int64_t ti = I * 4 + q, tj = J * 8 + half * 4 + t;
+            if (lane == 0 && ti * 32 < M && tj * 32 < N) co.nC[ti * co.ldn + tj] = sqrt(x);
+          }
+        }
+        if (prof) e_d += clock64() - te1;
+        continue;
+      }
 #pragma unroll 1
       for (int hh = 0; hh < 4; ++hh) {
         const int lh = hh & 1;                         // lanes [16*lh, 16*lh + 16) of the quadrant
@@ -886,7 +961,8 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
   // bench point (partial-tile combine and zero-fill tails); dynamic LPT is default
   static const bool streamk_env = getenv("SPAMM_STREAMK") && atoi(getenv("SPAMM_STREAMK")) == 1;
   // (stream-K zero-fills empty tiles with bulk stores: only for beta == 0)
-  const bool streamk = streamk_env && p.beta == 0.0;
+  const bool chain = p.out_norms || p.out_low != nullptr;
+  const bool streamk = streamk_env && p.beta == 0.0 && !chain;
   // stream-K splits tiles, so it uses every slot even when there are fewer tiles than slots
   const int grid = static_cast<int>(streamk ? slots : (n_tiles < slots ? n_tiles : slots));
   constexpr int kProfMax = 512;
@@ -928,6 +1004,7 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
                                                                  (streamk || ((dbg & 32) && p.beta == 0.0)) ? p.hist : nullptr,
                                                                  streamk ? p.sk_wpre : nullptr, p.sk_scratch, p.sk_ticket,
                                                                  Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
+                                                                 ChainOut{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl},
                                                                  prof, dbg);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) {
   if (!p.planes) return fail(SPAMM_E_STATE, "FP32X3 split planes missing (spamm_norms not run on this plan)");
+  if (p.out_norms || p.out_low) return fail(SPAMM_E_UNSUPPORTED, "chained outputs are not implemented for SPAMM_FP32X3");
   const uint16_t* pA = p.planes;
   const uint16_t* pB = p.b_is_a ? p.planes : p.planes + 3 * p.M * p.ldpa;
   const int64_t ldb = p.b_is_a ? p.ldpa : p.ldpb;

@@ -20,6 +20,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "spamm.h")
 SPAMM_OK, SPAMM_E_INVALID, SPAMM_E_UNSUPPORTED, SPAMM_E_CUDA, SPAMM_E_NOMEM, SPAMM_E_NCCL, SPAMM_E_STATE = range(7)
 SPAMM_FP32, SPAMM_BF16, SPAMM_FP16, SPAMM_FP32X3 = 0, 1, 2, 3
 SPAMM_FLAG_NONE, SPAMM_FLAG_TIMING, SPAMM_FLAG_SYNC_SKIPMAP = 0, 1, 2
+SPAMM_MUL_AUTO, SPAMM_MUL_OUTPUT_NORMS = 1, 2
 SPAMM_MUL_AUTO = 1
 SPAMM_MGPU_INPUTS_REPLICATED, SPAMM_MGPU_INPUTS_ON_ROOT, SPAMM_MGPU_GATHER_C = 0, 1, 2
 
@@ -76,6 +77,9 @@ def _load():
         "spamm_get_stats": [P, ctypes.POINTER(spamm_stats)],
         "spamm_count_kept": [P, D, PI64, P],
         "spamm_set_scalars": [P, D, D],
+        "spamm_multiply_chain": [P, P, I64, P, I64, P, I64, P, I64, U32, P],
+        "spamm_get_output_norms": [P, PP],
+        "spamm_set_norms": [P, P, P, P],
         "spamm_tau_search": [P, D, D, I32, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I32), P],
     }
     for name, args in sig.items():
@@ -178,6 +182,31 @@ def spamm_run(plan, A, B, C, stream=None) -> None:
     b, ldb = _mat(B)
     c, ldc = _mat(C)
     _check(_lib.spamm_run(plan, a, lda, b, ldb, c, ldc, _stream(stream)))
+
+
+# ---------------------------------------------------------- chained SpAMM ---
+def spamm_multiply_chain(plan, A, B, C, C_low=None, flags: int = SPAMM_MUL_OUTPUT_NORMS, stream=None) -> None:
+    a, lda = _mat(A)
+    b, ldb = _mat(B)
+    c, ldc = _mat(C)
+    cl, ldcl = _mat(C_low)
+    _check(_lib.spamm_multiply_chain(plan, a, lda, b, ldb, c, ldc, cl, ldcl, int(flags), _stream(stream)))
+
+
+def spamm_get_output_norms(plan):
+    """nC [BM, BN] float64 copy of the last chained multiply's output tile norms."""
+    st = spamm_get_stats(plan)
+    d = ctypes.c_void_p()
+    _check(_lib.spamm_get_output_norms(plan, ctypes.byref(d)))
+    torch.cuda.synchronize()
+    return _view(d.value, (st["BM"], st["BN"]), "<f8", torch.float64)
+
+
+def spamm_set_norms(plan, nA, nB, stream=None) -> None:
+    """Stage 1 from device float64 maps nA [BM, BK] and nB [BK, BN] (contiguous)."""
+    nA, nB = nA.contiguous(), nB.contiguous()
+    _check(_lib.spamm_set_norms(plan, ctypes.c_void_p(nA.data_ptr()), ctypes.c_void_p(nB.data_ptr()),
+                                _stream(stream)))
 
 
 # -------------------------------------------------------------- tau search ---
@@ -376,6 +405,15 @@ class Plan:
 
     def stats(self):
         return spamm_get_stats(self.handle)
+
+    def multiply_chain(self, A, B, C, C_low=None, flags=SPAMM_MUL_OUTPUT_NORMS, stream=None):
+        spamm_multiply_chain(self.handle, A, B, C, C_low, flags, stream)
+
+    def output_norms(self):
+        return spamm_get_output_norms(self.handle)
+
+    def set_norms(self, nA, nB, stream=None):
+        spamm_set_norms(self.handle, nA, nB, stream)
 
     def count_kept(self, tau, stream=None):
         return spamm_count_kept(self.handle, tau, stream)

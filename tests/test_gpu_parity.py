@@ -376,3 +376,63 @@ def test_alpha_beta_update(sp, prec, alpha, beta):
     assert err <= 5e-6, err
     with pytest.raises(sp.SpammError):
         plan.set_scalars(float("nan"), 0.0)
+
+
+# ------------------------------------------------------------ chained SpAMM (f3) ---
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_chain_output_norms_and_low_copy(sp, prec):
+    """spamm_multiply_chain: C as spamm_multiply; C_low = RNE(C) to bf16; nC = tile norms (Eq. 2)
+    of the stored values (C_low's for BF16 plans, reading R4)."""
+    M, N, K = 300, 257, 129
+    A = _rounded(synth.perturbed_decay_matrix(K, 0.95, seed=101, m=M), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=102, m=K), prec)
+    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+    prods = np.unique(nA[:, :, None] * nB[None, :, :])
+    tau = float(0.5 * (prods[len(prods) // 3] + prods[len(prods) // 3 + 1]))
+    plan = sp.Plan(M, N, K, tau, prec)
+    Ad, Bd = _dev(A, prec), _dev(B, prec)
+    C = torch.empty((M, -(-N // 4) * 4), dtype=torch.float32, device="cuda")[:, :N]
+    Cl = torch.empty((M, -(-N // 8) * 8), dtype=torch.bfloat16, device="cuda")[:, :N] if prec == "bf16" else None
+    plan.multiply_chain(Ad, Bd, C, Cl, flags=sp.SPAMM_MUL_AUTO | sp.SPAMM_MUL_OUTPUT_NORMS)
+    torch.cuda.synchronize()
+    Cn = C.cpu().numpy()
+    assert _rel_fro(Cn, oracle.spamm(A, B, tau, T, nA, nB)) <= (2e-6 if prec == "fp32" else 1e-5)
+    stored = Cn
+    if prec == "bf16":
+        np.testing.assert_array_equal(Cl.cpu().float().numpy(), synth.round_to_bf16(Cn))
+        stored = Cl.cpu().float().numpy()
+    np.testing.assert_allclose(plan.output_norms().cpu().numpy(), oracle.tile_norms(stored, T), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_chain_matrix_square_twice(sp, prec):
+    """X -> X^2 -> X^4 by repeated SpAMM squaring, the second step's norm maps taken from the
+    first step's epilogue (spamm_set_norms), never from re-reading X^2.  Each step vs the
+    oracle on that step's actual input: skip map outside the tie band, C within the bar."""
+    N = 520
+    X = _rounded(synth.perturbed_decay_matrix(N, 0.9, seed=103), prec)
+    n1 = oracle.tile_norms(X, T)
+    tau = float(np.quantile(n1[:, :, None] * n1[None, :, :], 0.6))
+    dt = torch.float32 if prec == "fp32" else torch.bfloat16
+    p1 = sp.Plan(N, N, N, tau, prec)
+    Xd = _dev(X, prec)
+    X2 = torch.empty((N, N), dtype=torch.float32, device="cuda")
+    X2l = torch.empty((N, N), dtype=dt, device="cuda") if prec == "bf16" else None
+    p1.multiply_chain(Xd, Xd, X2, X2l, flags=sp.SPAMM_MUL_AUTO | sp.SPAMM_MUL_OUTPUT_NORMS)
+    nC = p1.output_norms()
+    X2in = X2 if prec == "fp32" else X2l
+    p2 = sp.Plan(N, N, N, tau * 1e-2, prec)
+    p2.set_norms(nC, nC)
+    p2.build_skipmap()
+    X4 = torch.empty((N, N), dtype=torch.float32, device="cuda")
+    p2.multiply(X2in, X2in, X4)
+    torch.cuda.synchronize()
+    X2h = X2in.cpu().float().numpy()
+    n2 = oracle.tile_norms(X2h, T)
+    np.testing.assert_allclose(nC.cpu().numpy(), n2, rtol=1e-12, atol=0)
+    diff, _ = _check_skipmap(sp, p2, n2, n2, tau * 1e-2)
+    err = _rel_fro(X4.cpu().numpy(), oracle.spamm(X2h, X2h, tau * 1e-2, T, n2, n2))
+    assert err <= (2e-6 if prec == "fp32" else 1e-5), err
+    with pytest.raises(sp.SpammError) as e:
+        sp.Plan(N, N, N, tau, "fp32x3").set_norms(nC, nC)
+    assert e.value.status == sp.SPAMM_E_UNSUPPORTED
