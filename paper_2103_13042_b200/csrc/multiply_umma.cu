@@ -149,7 +149,9 @@ struct Maps {   // A (32- and 64-deep boxes); B as stacked 32-column boxes, 1..8
   CUtensorMap a1, a2, b1[4], b2[4], b2d, b64, b64w;
 };
 
-template <uint32_t kFmt, int kCtas, bool kWide>
+// kGen: general epilogue (alpha/beta, chained outputs).  The plain instantiation (alpha = 1,
+// beta = 0, no chain outputs) keeps the register budget of 2 CTAs/SM free of spills.
+template <uint32_t kFmt, int kCtas, bool kWide, bool kGen>
 __global__ void __launch_bounds__(kThreads, kCtas)
     spamm_mul_umma_kernel(const __grid_constant__ Maps mp, int use3d, const int64_t* __restrict__ mstart,
                           const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
@@ -724,11 +726,11 @@ __global__ void __launch_bounds__(kThreads, kCtas)
               if (row < M) {
                 float* dst = C + row * ldc + gc;
                 if (gc + 3 < N) {
-                  __stcs(reinterpret_cast<float4*>(dst), axpby4(ab, acc[m], dst));
+                  __stcs(reinterpret_cast<float4*>(dst), kGen ? axpby4(ab, acc[m], dst) : acc[m]);
                 } else {
-                  if (gc < N) dst[0] = axpby1(ab, acc[m].x, dst);
-                  if (gc + 1 < N) dst[1] = axpby1(ab, acc[m].y, dst + 1);
-                  if (gc + 2 < N) dst[2] = axpby1(ab, acc[m].z, dst + 2);
+                  if (gc < N) dst[0] = kGen ? axpby1(ab, acc[m].x, dst) : acc[m].x;
+                  if (gc + 1 < N) dst[1] = kGen ? axpby1(ab, acc[m].y, dst + 1) : acc[m].y;
+                  if (gc + 2 < N) dst[2] = kGen ? axpby1(ab, acc[m].z, dst + 2) : acc[m].z;
                 }
               }
             }
@@ -737,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
         if (prof) e_d += clock64() - te1;
         continue;
       }
-      if (co.nC != nullptr || co.clow != nullptr) {
+      if (kGen && (co.nC != nullptr || co.clow != nullptr)) {
         // ---- chained output: C (alpha/beta applied), optional rounded copy, tile norms
         double tsum[4] = {0.0, 0.0, 0.0, 0.0};   // tiles (I*4+q, J*8 + half*4 + t)
 #pragma unroll 1
@@ -817,14 +819,14 @@ __global__ void __launch_bounds__(kThreads, kCtas)
           const int64_t col = J * 256 + c0 + 8 * i + 2 * t0;
           float* ca = C + ra * ldc + col;
           float* cb = C + rb * ldc + col;
+          const float2 pa = make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
+          const float2 pb = make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
           if (col + 1 < N) {
-            if (ra < M) __stcs(reinterpret_cast<float2*>(ca),
-                               axpby2(ab, make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1])), ca));
-            if (rb < M) __stcs(reinterpret_cast<float2*>(cb),
-                               axpby2(ab, make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])), cb));
+            if (ra < M) __stcs(reinterpret_cast<float2*>(ca), kGen ? axpby2(ab, pa, ca) : pa);
+            if (rb < M) __stcs(reinterpret_cast<float2*>(cb), kGen ? axpby2(ab, pb, cb) : pb);
           } else if (col < N) {
-            if (ra < M) *ca = axpby1(ab, __uint_as_float(v[4 * i]), ca);
-            if (rb < M) *cb = axpby1(ab, __uint_as_float(v[4 * i + 2]), cb);
+            if (ra < M) *ca = kGen ? axpby1(ab, pa.x, ca) : pa.x;
+            if (rb < M) *cb = kGen ? axpby1(ab, pb.x, cb) : pb.x;
           }
         }
       }
@@ -917,7 +919,7 @@ __global__ void __launch_bounds__(kPreThreads) lpt_prefix_kernel(int64_t n, int6
   if (threadIdx.x == 0) wpre[n] = s_carry;
 }
 
-template <uint32_t kFmt, int kCtas, bool kWide>
+template <uint32_t kFmt, int kCtas, bool kWide, bool kGen>
 spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                         cudaStream_t s, CUtensorMapDataType dt) {
   Maps mp;
@@ -948,7 +950,7 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
     }
   }
   constexpr size_t kSmemBytes = Cfg<kCtas, kWide>::kSmemBytes;
-  auto kern = spamm_mul_umma_kernel<kFmt, kCtas, kWide>;
+  auto kern = spamm_mul_umma_kernel<kFmt, kCtas, kWide, kGen>;
   static bool attr_set = false;
   if (!attr_set) {
     SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
@@ -1054,13 +1056,17 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
 template <uint32_t kFmt>
 spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                         cudaStream_t s, CUtensorMapDataType dt) {
+  if (p.alpha != 1.0 || p.beta != 0.0 || p.out_norms || p.out_low != nullptr) {   // general epilogue
+    if (umma_variant_wide(p.umma_variant)) return launch_cfg<kFmt, 2, true, true>(p, A, lda, B, ldb, C, ldc, s, dt);
+    return launch_cfg<kFmt, 2, false, true>(p, A, lda, B, ldb, C, ldc, s, dt);
+  }
   switch (p.umma_variant) {
     case 0:
-      return launch_cfg<kFmt, 2, false>(p, A, lda, B, ldb, C, ldc, s, dt);
+      return launch_cfg<kFmt, 2, false, false>(p, A, lda, B, ldb, C, ldc, s, dt);
     case 1:
-      return launch_cfg<kFmt, 2, true>(p, A, lda, B, ldb, C, ldc, s, dt);
+      return launch_cfg<kFmt, 2, true, false>(p, A, lda, B, ldb, C, ldc, s, dt);
     default:
-      return launch_cfg<kFmt, 1, true>(p, A, lda, B, ldb, C, ldc, s, dt);
+      return launch_cfg<kFmt, 1, true, false>(p, A, lda, B, ldb, C, ldc, s, dt);
   }
 }
 

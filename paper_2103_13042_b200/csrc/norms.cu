@@ -22,7 +22,9 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kThreads = 128;          // 4 warps x 8 rows of a 32-row box
+constexpr int kWarps = 8;              // warps per CTA, each reducing 32 / kWarps rows of a box
+constexpr int kRowsPerWarp = 32 / kWarps;
+constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 4;
 constexpr int kBoxBytesRow = 512;      // bytes per box row (256 BF16 / 128 FP32 columns)
 constexpr int kBoxBytes = 32 * kBoxBytesRow;   // 16 KB
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint8_t* ring = smem;
   __shared__ uint64_t full[kStages];
-  __shared__ double part[4][kBoxesPerCta * TPB];
+  __shared__ double part[kWarps][kBoxesPerCta * TPB];
 
   const bool isA = blockIdx.y < ja.nrow;
   const NormJob& j = isA ? ja : jb;
@@ -148,11 +150,11 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
     const uint8_t* box = ring + s * kBoxBytes;
     double acc = 0.0;                            // this lane's 16 bytes in the warp's 8 rows
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(box + (warp * 8 + r) * kBoxBytesRow + lane * 16);
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(box + (warp * kRowsPerWarp + r) * kBoxBytesRow + lane * 16);
       acc += sq16<T>(raw);
       if (j.planes != nullptr) {   // FP32X3: the element's bfloat16 split (rows/cols of the padded planes)
-        const int64_t row = it * 32 + warp * 8 + r, col = (box0 + b) * kCols + lane * (16 / sizeof(T));
+        const int64_t row = it * 32 + warp * kRowsPerWarp + r, col = (box0 + b) * kCols + lane * (16 / sizeof(T));
         if (row < j.rows && col < j.pld - j.pcol0) write_planes<T>(j, raw, row, col);
       }
     }
@@ -168,7 +170,9 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
   }
   __syncthreads();
   for (int t = threadIdx.x; t < nbox * TPB; t += kThreads) {
-    const double tot = ((part[0][t] + part[1][t]) + part[2][t]) + part[3][t];
+    double tot = part[0][t];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) tot += part[w][t];   // warp order: position independent
     const int64_t kt = box0 * TPB + t;
     if (kt * 32 < j.cols) {
       const double nrm = sqrt(tot);
