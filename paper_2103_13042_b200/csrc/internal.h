@@ -123,7 +123,7 @@ spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_
 spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 spamm_status launch_leaf_expand(Plan& p, cudaStream_t s);   // per-C-tile lists from macro lists
-int umma_variant_from_env();       // SPAMM_UMMA_VARIANT: 0 (default) 2 CTAs/SM 32-deep, 1 = 2 CTAs/SM 64-deep, 2 = 1 CTA/SM 64-deep, 3 = CTA pairs
+int umma_variant_from_env();       // SPAMM_UMMA_VARIANT: 0 (default) 2 CTAs/SM 32-deep, 1 = 2 CTAs/SM 64-deep, 2 = 1 CTA/SM 64-deep split issuers, 3 = CTA pairs, 4 = 1 CTA/SM 32-deep split issuers
 bool umma_variant_wide(int v);     // does the variant consume merged 64-deep k-steps?
 spamm_status launch_multiply_pair(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);

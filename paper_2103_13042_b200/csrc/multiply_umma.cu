@@ -53,7 +53,9 @@ struct Cfg {
   static constexpr int kASlot = kWide ? 128 * 64 * 2 : 128 * 32 * 2;    // A[128 x 64|32]
   static constexpr int kBSlot = kWide ? 64 * 256 * 2 : 32 * 256 * 2;    // B[64|32 x 256]
   static constexpr int kStageBytes = kASlot + kBSlot;
-  static constexpr int kStages = (kCtas == 2 && kWide) ? 2 : 4;
+  // kCtas == 1: one CTA per SM whose two MMA warps each own one 128-column half of the
+  // macro-tile (both consume every stage), two TMEM tiles (512 columns) and an 8-deep ring
+  static constexpr int kStages = kCtas == 2 ? (kWide ? 2 : 4) : (kWide ? 4 : 8);
   static constexpr int kBufs = kCtas == 2 ? 1 : 2;                       // TMEM accumulators
   static constexpr uint32_t kTmemCols = 256u * kBufs;
   static constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 1024 + 1536;
@@ -212,10 +214,10 @@ __global__ void __launch_bounds__(kThreads, kCtas)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kCtas == 1 ? 2 : 1);   // split issuers: both halves release a stage
     }
     for (int b = 0; b < kBufs; ++b) {
-      mbar_init(&tfull[b], 1);
+      mbar_init(&tfull[b], kCtas == 1 ? 2 : 1);
       mbar_init(&tempty[b], kEpiWarps);
     }
     for (int q = 0; q < kTQ; ++q) {
@@ -460,8 +462,11 @@ __global__ void __launch_bounds__(kThreads, kCtas)
         __syncwarp();
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (kCtas == 1 && warp == 2)) {
     // ------------------------------------------------------------- MMA issuer
+    // kCtas == 2: one issuer, full 256-column tile.  kCtas == 1: warp 1 issues columns
+    // [0, 128), warp 2 columns [128, 256) of every k-step (runs clipped to the half).
+    const int hsel = kCtas == 1 ? warp - 1 : 0;
     if (lane == 0) {
       constexpr uint32_t idesc_base = idesc_f16(kFmt, 128, 0, 0, 1);
       constexpr uint32_t idesc_full = idesc_base | (8u << 19);   // N = 256, no lane mask
@@ -497,8 +502,8 @@ __global__ void __launch_bounds__(kThreads, kCtas)
             mbar_wait(&tempty[buf], static_cast<uint32_t>((tile_it / kBufs) & 1));
             if (prof) m_te += clock64() - tw0;
             tc_fence_after();
-            dcol = tbase + static_cast<uint32_t>(buf) * 256u;
-            umma_f16(dcol, zdesc, zdesc, idesc_full, 0u, 0u, 0u, 0u, 0u);   // D = 0
+            dcol = tbase + static_cast<uint32_t>(buf) * 256u + (kCtas == 1 ? static_cast<uint32_t>(hsel) * 128u : 0u);
+            umma_f16(dcol, zdesc, zdesc, kCtas == 1 ? (idesc_base | (4u << 19)) : idesc_full, 0u, 0u, 0u, 0u, 0u);   // D = 0
           }
           const unsigned long long tm0 = prof ? clock64() : 0;
           if (!(fl & kNoStep) && !(dbg & 1)) {
@@ -514,7 +519,35 @@ __global__ void __launch_bounds__(kThreads, kCtas)
             const uint64_t bd = b128 ? smem_desc(b_addr, box, 1024, kLayoutSW128) : smem_desc(b_addr, box, 512, kLayoutSW64);
             const uint32_t kstep = b128 ? 128u : 64u;   // descriptor units (16 B) per K=16
             const uint32_t nr = (rs.x >> 16) & 15u;
-            if (nr == 1u && rs.y == kFullRun) {
+            if (kCtas == 1) {
+              // split issuer: this warp's half [4h, 4h + 4) of the column tiles
+              const uint32_t lo = 4u * static_cast<uint32_t>(hsel), hi = lo + 4u;
+              const int nk = wide ? 4 : 2;
+              if (nr == 1u && rs.y == kFullRun) {
+                const uint32_t idesc = idesc_base | (4u << 19);   // N = 128
+                const uint64_t bj = bd + static_cast<uint64_t>(lo * (box >> 4));
+                for (int kk = 0; kk < nk; ++kk) umma_f16(dcol, ad + 2 * kk, bj + 64 * kk, idesc, 1u, 0u, 0u, 0u, 0u);
+                if (prof) n_mma += nk;
+              } else {
+                uint32_t cw = rs.y;
+                for (uint32_t rr = 0; rr < nr; ++rr) {
+                  if (rr == 3) cw = rs.z;
+                  if (rr == 6) cw = rs.w;
+                  const uint32_t w = cw & 0x3FFu;
+                  cw >>= 10;
+                  const uint32_t r0 = w & 7u, r1 = r0 + ((w >> 3) & 7u) + 1u, pat = w >> 6;
+                  const uint32_t j0 = r0 > lo ? r0 : lo, j1 = r1 < hi ? r1 : hi;
+                  if (j1 <= j0) continue;
+                  const uint32_t idesc = idesc_base | ((j1 - j0) << 19);
+                  const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
+                  const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
+                  const uint64_t bj = bd + static_cast<uint64_t>(j0 * (box >> 4));
+                  const uint32_t d = dcol + (j0 - lo) * 32u;
+                  for (int kk = 0; kk < nk; ++kk) umma_f16(d, ad + 2 * kk, bj + 64 * kk, idesc, 1u, m0, m1, m2, m3);
+                  if (prof) n_mma += nk;
+                }
+              }
+            } else if (nr == 1u && rs.y == kFullRun) {
               umma_f16(dcol, ad, bd, idesc_full, 1u, 0u, 0u, 0u, 0u);
               umma_f16(dcol, ad + 2, bd + kstep, idesc_full, 1u, 0u, 0u, 0u, 0u);
               if (prof) n_mma += 2;
@@ -580,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
         }
         ph ^= 1;
       }
-      if (prof) {
+      if (prof && warp == 1) {
         prof[blockIdx.x * 16 + 2] = m_te;
         prof[blockIdx.x * 16 + 3] = m_fu;
         prof[blockIdx.x * 16 + 6] = clock64() - tk0;
@@ -935,7 +968,7 @@ spamm_status launch_cfg(Plan& p, const void* A, int64_t lda, const void* B, int6
   // requests per byte; parity-green but measured slower at the bench point: 198 vs 182 us,
   // the extra columns of partially needed atoms and the split odd-start runs cost more)
   static const int bmode_env = getenv("SPAMM_UMMA_BMODE") ? atoi(getenv("SPAMM_UMMA_BMODE")) : 1;
-  const int use3d = bmode_env == 2 ? 2 : (bmode_env == 1 && (p.N % 32) == 0 ? 1 : 0);
+  const int use3d = (bmode_env == 2 && kCtas == 2) ? 2 : (bmode_env >= 1 && (p.N % 32) == 0 ? 1 : 0);
   if (use3d == 2) {
     SPAMM_TRY(encode_tmap_2d(&mp.b64, dt, 2, B, p.N, p.K, ldb, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B));
     SPAMM_TRY(encode_tmap_2d(&mp.b64w, dt, 2, B, p.N, p.K, ldb, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B));
@@ -1065,6 +1098,8 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
       return launch_cfg<kFmt, 2, false, false>(p, A, lda, B, ldb, C, ldc, s, dt);
     case 1:
       return launch_cfg<kFmt, 2, true, false>(p, A, lda, B, ldb, C, ldc, s, dt);
+    case 4:
+      return launch_cfg<kFmt, 1, false, false>(p, A, lda, B, ldb, C, ldc, s, dt);
     default:
       return launch_cfg<kFmt, 1, true, false>(p, A, lda, B, ldb, C, ldc, s, dt);
   }
@@ -1075,9 +1110,9 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
 int umma_variant_from_env() {
   const char* v = getenv("SPAMM_UMMA_VARIANT");
   const int x = v ? atoi(v) : 0;
-  return x >= 0 && x <= 3 ? x : 0;
+  return x >= 0 && x <= 4 ? x : 0;
 }
-bool umma_variant_wide(int v) { return v != 0; }
+bool umma_variant_wide(int v) { return v == 1 || v == 2; }
 
 spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s) {
