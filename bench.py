@@ -267,7 +267,9 @@ def run_ours(args, rank, world, local_rank):
         # fp32x3 executes six BF16 products per kept pair on the tensor cores
         mma_flops = kept_flops * (6 if prec == "fp32x3" else 1)
         achieved = mma_flops / (mean["multiply"] / 1e3) / 1e12
-        kname = {"fp32": "spamm_mul_simt_kernel", "fp32x3": "spamm_mul_x3_kernel"}.get(prec, "spamm_mul_umma_kernel")
+        # BF16/FP16: 256 x 256 macro-tiles (macro_i = 8) run multiply_dual.cu, 128 x 256 multiply_umma.cu
+        tc_kernel = "spamm_mul_dual_kernel" if st.get("macro_i") == 8 else "spamm_mul_umma_kernel"
+        kname = {"fp32": "spamm_mul_simt_kernel", "fp32x3": "spamm_mul_x3_kernel"}.get(prec, tc_kernel)
         work = (f"6*2*32^3*kept = {mma_flops:.4g} BF16 MMA FLOP (kept={st['kept']})" if prec == "fp32x3"
                 else f"2*32^3*kept = {kept_flops:.4g} FLOP (kept={st['kept']})")
         roof = {"kernel": kname,

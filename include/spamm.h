@@ -187,8 +187,7 @@ spamm_status spamm_multiply_mgpu(spamm_plan_t p, void* nccl_comm, int rank, int 
  * spamm_multiply_mgpu of this plan.  Defaults alpha = 1, beta = 0.  Applied in the multiply
  * epilogue in FP32: C = fmaf(alpha, P, beta * C_old); with beta == 0 the old C is never read
  * (BLAS convention: NaN there does not propagate).  Tiles without kept pairs get beta * C_old.
- * alpha, beta must be finite (else SPAMM_E_INVALID).  The CTA-pair variant
- * (SPAMM_UMMA_VARIANT=3) supports only the defaults (else SPAMM_E_UNSUPPORTED at multiply). */
+ * alpha, beta must be finite (else SPAMM_E_INVALID). */
 spamm_status spamm_set_scalars(spamm_plan_t p, double alpha, double beta);
 
 /* ---------------------------------------------------------- chained SpAMM --- */
@@ -200,7 +199,7 @@ spamm_status spamm_set_scalars(spamm_plan_t p, double alpha, double beta);
  *   - with SPAMM_MUL_OUTPUT_NORMS: writes the float64 tile norms of the written result into a
  *     plan-owned map nC[BM][BN] (Eq. 2 of the values stored: C, or C_low's rounded values when
  *     given -- reading R4), readable with spamm_get_output_norms.
- * FP32X3 plans and the CTA-pair variant return SPAMM_E_UNSUPPORTED. */
+ * FP32X3 plans return SPAMM_E_UNSUPPORTED. */
 spamm_status spamm_multiply_chain(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
                                   float* C, int64_t ldc, void* C_low, int64_t ldcl, uint32_t flags,
                                   void* stream);

@@ -205,13 +205,13 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->BM = BM;
   p->BK = BK;
   p->BN = BN;
-  // the CTA-pair tensor path needs fixed list regions and whole 32-column B boxes
+  // the 256 x 256 two-issuer tensor path needs fixed list regions and whole 32-column B boxes
   const bool fixed_ok = !(flags & SPAMM_FLAG_SYNC_SKIPMAP) &&
                         sizeof(uint16_t) * static_cast<size_t>(BM * BN) * static_cast<size_t>(BK) <= kWorstCaseBudget;
   p->umma_variant = umma_variant_from_env();
-  p->pair = !f32_inputs(prec) && fixed_ok && N % 32 == 0 && p->umma_variant == 3;
-  if (!f32_inputs(prec) && !p->pair && p->umma_variant == 3) p->umma_variant = 0;
-  p->MI = p->pair ? kMacroI_pair : kMacroI;
+  p->dual = !f32_inputs(prec) && fixed_ok && N % 32 == 0 && p->umma_variant == 5;
+  if (!f32_inputs(prec) && !p->dual && p->umma_variant == 5) p->umma_variant = 0;
+  p->MI = p->dual ? kMacroI_dual : kMacroI;
   p->MJ = f32_inputs(prec) ? kMacroJ_simt : kMacroJ_umma;
   p->GM = (BM + p->MI - 1) / p->MI;
   p->GN = (BN + p->MJ - 1) / p->MJ;
@@ -257,12 +257,12 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   // macro lists: worst case GM*GN*BK entries (8 B each) -- small relative to A and B
   if (st == SPAMM_OK) {
     p->macro_cap = nmac * BK;
-    // (k, mask) entries: 8 bytes, or 16 bytes (k, mask_lo, mask_hi, 0) for 8 x 8 pair tiles
-    st = alloc(reinterpret_cast<void**>(&p->macro_ent), (p->pair ? 16 : 8) * static_cast<size_t>(p->macro_cap));
-    // tensor-path entries: a pair-path k-step with more than 6 runs takes two entries
+    // (k, mask) entries: 8 bytes, or 16 bytes (k, mask_lo, mask_hi, 0) for 8 x 8 macro-tiles
+    st = alloc(reinterpret_cast<void**>(&p->macro_ent), (p->dual ? 16 : 8) * static_cast<size_t>(p->macro_cap));
+    // tensor-path entries: one uint4 per k-step, two (one per 128-row half) for 8 x 8 macro-tiles
     if (st == SPAMM_OK && !f32_inputs(prec))
       st = alloc(reinterpret_cast<void**>(&p->macro_run),
-                 sizeof(uint4) * static_cast<size_t>(p->macro_cap) * (p->pair ? 2 : 1));
+                 sizeof(uint4) * static_cast<size_t>(p->macro_cap) * (p->dual ? 2 : 1));
   }
   // leaf lists: reserve the worst case unless it exceeds the budget or SYNC_SKIPMAP is set
   if (st == SPAMM_OK && !(flags & SPAMM_FLAG_SYNC_SKIPMAP)) {
@@ -411,8 +411,8 @@ spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int
     SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
                                    s));
   } else {
-    if (p.pair)
-      SPAMM_TRY(launch_multiply_pair(p, A, lda, B, ldb, C, ldc, s));
+    if (p.dual)
+      SPAMM_TRY(launch_multiply_dual(p, A, lda, B, ldb, C, ldc, s));
     else
       SPAMM_TRY(launch_multiply_umma(p, A, lda, B, ldb, C, ldc, s));
   }
@@ -459,8 +459,7 @@ spamm_status spamm_multiply_chain(spamm_plan_t h, const void* A, int64_t lda, co
     if (f32_inputs(p.prec)) return fail(SPAMM_E_INVALID, "C_low is for BF16/FP16 plans (FP32 C is the next input)");
     SPAMM_TRY(check_matrix(C_low, p.M, p.N, ldcl, 2, "C_low"));
   }
-  if (p.prec == SPAMM_FP32X3 || p.pair)
-    return fail(SPAMM_E_UNSUPPORTED, "chained outputs: FP32, BF16, FP16 (non-pair variants) only");
+  if (p.prec == SPAMM_FP32X3) return fail(SPAMM_E_UNSUPPORTED, "chained outputs: FP32, BF16, FP16 only");
   if ((flags & SPAMM_MUL_OUTPUT_NORMS) && !p.nC)
     SPAMM_TRY(alloc(reinterpret_cast<void**>(&p.nC), sizeof(double) * static_cast<size_t>(p.BM * p.BN)));
   if (flags & SPAMM_MUL_AUTO) {

@@ -18,7 +18,7 @@ inline bool f32_inputs(spamm_precision p) { return p == SPAMM_FP32 || p == SPAMM
 // Scheduling macro-tile shapes (in C tiles).  FP32 SIMT: 128x128 (one warp per C tile);
 // tensor path: 128x256 (one UMMA M=128 covers 4 tile rows, N up to 256 = 8 tile cols).
 constexpr int kMacroI = 4;
-constexpr int kMacroI_pair = 8;   // CTA-pair tensor path: 256 x 256 macro-tiles (8 x 8 C tiles)
+constexpr int kMacroI_dual = 8;   // default tensor path: 256 x 256 macro-tiles (8 x 8 C tiles), multiply_dual.cu
 constexpr int kMacroJ_simt = 4;
 constexpr int kMacroJ_umma = 8;
 
@@ -60,8 +60,8 @@ struct Plan {
   int64_t* hist = nullptr;       // = row_work + BM: [BK+2] histogram of macro union counts
   int64_t* totals = nullptr;     // = hist + BK + 2: [0] kept pairs, [1] macro entries
   int64_t* mstart = nullptr;     // [GM*GN] start of each macro-tile's entries (t*BK or macro_ptr)
-  int umma_variant = 0;          // tensor-path kernel: 0-2 multiply_umma.cu, 3 = CTA pairs (multiply_pair.cu)
-  bool pair = false;             // the CTA-pair path is in use (MI = 8, 16-byte macro entries)
+  int umma_variant = 5;          // tensor-path kernel: 0-2, 4 multiply_umma.cu, 5 multiply_dual.cu
+  bool dual = false;             // the two-issuer 256 x 256 path (variant 5, multiply_dual.cu): MI = 8, two 4 x 8 run entries per k-step
   int64_t* Uw = nullptr;         // [GM*GN] tensor-path entries per macro-tile (pairs merged) or = U
   // stream-K workspace of the tensor multiply (allocated on first use)
   float* sk_scratch = nullptr;       // [2 * grid][128 * 256] FP32 partial tiles
@@ -123,9 +123,9 @@ spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_
 spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 spamm_status launch_leaf_expand(Plan& p, cudaStream_t s);   // per-C-tile lists from macro lists
-int umma_variant_from_env();       // SPAMM_UMMA_VARIANT: 0 (default) 2 CTAs/SM 32-deep, 1 = 2 CTAs/SM 64-deep, 2 = 1 CTA/SM 64-deep split issuers, 3 = CTA pairs, 4 = 1 CTA/SM 32-deep split issuers
+int umma_variant_from_env();       // SPAMM_UMMA_VARIANT: 0 (default) 2 CTAs/SM 32-deep, 1 = 2 CTAs/SM 64-deep, 2 = 1 CTA/SM 64-deep split issuers, 4 = 1 CTA/SM 32-deep split issuers, 5 (default) = 256 x 256 tiles with two issuers (3, CTA pairs, was removed)
 bool umma_variant_wide(int v);     // does the variant consume merged 64-deep k-steps?
-spamm_status launch_multiply_pair(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
+spamm_status launch_multiply_dual(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s);   // SPAMM_FP32X3
 spamm_status launch_multiply_umma(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,

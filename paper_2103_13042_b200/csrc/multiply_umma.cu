@@ -1109,8 +1109,10 @@ spamm_status launch_fmt(Plan& p, const void* A, int64_t lda, const void* B, int6
 
 int umma_variant_from_env() {
   const char* v = getenv("SPAMM_UMMA_VARIANT");
-  const int x = v ? atoi(v) : 0;
-  return x >= 0 && x <= 4 ? x : 0;
+  // default 5: 256 x 256 macro-tiles with two MMA issuers (multiply_dual.cu; measured fastest at
+  // the bench point).  Plans whose shape it cannot serve fall back to 0 (api.cu).
+  const int x = v ? atoi(v) : 5;
+  return x >= 0 && x <= 5 ? x : 5;
 }
 bool umma_variant_wide(int v) { return v == 1 || v == 2; }
 

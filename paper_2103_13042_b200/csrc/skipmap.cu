@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kWarps = 8;
 
-// keep bits of one k-step of a macro-tile: bit li*MJ+lj; 64-bit for the 8 x 8 pair tiles
+// keep bits of one k-step of a macro-tile: bit li*MJ+lj; 64-bit for 8 x 8 macro-tiles
 template <int MI, int MJ>
 using mask_t = typename std::conditional<(MI * MJ > 32), unsigned long long, uint32_t>::type;
 
@@ -409,49 +409,6 @@ __device__ void last_cta_order(const LastArgs& la, int64_t* s_warp, unsigned lon
 // lists -- (k, keep mask) per k-step, which hold every keep bit -- are written here; the
 // per-C-tile k lists are expanded from them on request (leaf_expand_kernel).  Row work
 // and kept-pair counts are popcounts of the masks.
-// Runs of an 8 x 8 keep mask for the CTA-pair tensor path (multiply_pair.cu): adjacent
-// C-tile columns with the same non-zero 8-bit row pattern.  run = j0 | (len-1) << 3 |
-// pat << 6 (14 bits) in 16-bit slots, at most kPairRuns per entry; a k-step with more runs
-// is written as several entries for the same k (their MMAs accumulate).
-//   x = k | nruns << 16 | wide << 19,  y/z/w = runs 2q | 2q+1 << 16
-constexpr int kPairRuns = 6;
-__device__ __forceinline__ uint32_t col_pattern64(unsigned long long mask, int lj) {
-  // bits li*8 + lj (li = 0..7) -> bit li: the byte-spread bits are gathered by one multiply
-  const unsigned long long t = (mask >> lj) & 0x0101010101010101ull;
-  return static_cast<uint32_t>((t * 0x0102040810204080ull) >> 56) & 0xFFu;
-}
-__device__ __forceinline__ int pair_run_count(unsigned long long mask) {
-  int nr = 0;
-  uint32_t prev = 0u;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t pat = col_pattern64(mask, j);
-    nr += (pat != 0u && pat != prev) ? 1 : 0;
-    prev = pat;
-  }
-  return nr;
-}
-__device__ __forceinline__ uint4 encode_pair(uint32_t k, unsigned long long mask, uint32_t wide, int part) {
-  if (mask == ~0ull)   // all 8 x 8 pairs kept: one run j0 = 0, len = 8, pattern 0xFF
-    return make_uint4(k | (1u << 16) | (wide << 19), 0u | (7u << 3) | (0xFFu << 6), 0u, 0u);
-  uint32_t slot[kPairRuns] = {0u, 0u, 0u, 0u, 0u, 0u};
-  int nr = 0, n = 0;
-  int j = 0;
-  while (j < 8) {
-    const uint32_t pat = col_pattern64(mask, j);
-    int j1 = j + 1;
-    while (j1 < 8 && col_pattern64(mask, j1) == pat) ++j1;
-    if (pat) {
-      if (nr >= part * kPairRuns && nr < (part + 1) * kPairRuns)
-        slot[n++] = static_cast<uint32_t>(j) | (static_cast<uint32_t>(j1 - j - 1) << 3) | (pat << 6);
-      ++nr;
-    }
-    j = j1;
-  }
-  return make_uint4(k | (static_cast<uint32_t>(n) << 16) | (wide << 19), slot[0] | (slot[1] << 16),
-                    slot[2] | (slot[3] << 16), slot[4] | (slot[5] << 16));
-}
-
 constexpr int kFusedWarps = 8;
 constexpr int kKB = 32 * kFusedWarps;   // k per block: thread (w, lane) owns k = kb + 32 w + lane
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* src) {
@@ -470,8 +427,8 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
                       unsigned long long* __restrict__ hist, void* __restrict__ macro_ent_v,
                       uint4* __restrict__ macro_run, int64_t* __restrict__ Uw, int merge_ok, LastArgs la) {
   using M_ = mask_t<MI, MJ>;
-  constexpr bool kPair = MI * MJ > 32;    // 8 x 8 tiles: 64-bit masks, (k, mask_lo, mask_hi, 0) entries
-  constexpr int kRunStride = kPair ? 2 : 1;   // tensor-path region per macro-tile: kRunStride * BK entries
+  constexpr bool kMask64 = MI * MJ > 32;  // 8 x 8 tiles: 64-bit masks, (k, mask_lo, mask_hi, 0) entries
+  constexpr int kRunStride = kMask64 ? 2 : 1;   // tensor-path region per macro-tile: kRunStride * BK entries
   constexpr int W = kFusedWarps;
   constexpr int R = MI + MJ;              // norm rows per macro-tile: MI of A, MJ of B^T
   __shared__ uint32_t s_cm[W], s_cr[W], s_rw[W][MI];
@@ -544,7 +501,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
       rw[li] += static_cast<uint32_t>(__popcll(static_cast<unsigned long long>(mask >> (li * MJ)) & ((1ull << MJ) - 1ull)));
     const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
     // tensor-path entries: k-tiles 2p and 2p+1 with the same non-zero mask become one
-    // 64-deep k-step; the pair path splits k-steps with more than kPairRuns runs
+    // 64-deep k-step
     bool wide = false;
     uint32_t ne = 0;
     if (MJ == 8 && macro_run != nullptr) {
@@ -554,10 +511,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
       wide = merge_ok && even && mask != 0u && mnext == mask;
       const bool absorbed = merge_ok && !even && mask != 0u && mprev == mask;
       if (mask != 0u && !absorbed) {
-        if constexpr (kPair)
-          ne = static_cast<uint32_t>((pair_run_count(mask) + kPairRuns - 1) / kPairRuns);
-        else
-          ne = 1u;
+        ne = 1u;
       }
     }
     uint32_t ie = ne;   // inclusive warp scan of entry counts
@@ -581,7 +535,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
       tr += cr;
     }
     if (mask) {
-      if constexpr (kPair)
+      if constexpr (kMask64)
         reinterpret_cast<uint4*>(macro_ent_v)[mbase + om + __popc(any & lt)] =
             make_uint4(static_cast<uint32_t>(k), static_cast<uint32_t>(mask), static_cast<uint32_t>(mask >> 32), 0u);
       else
@@ -590,13 +544,15 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
     }
     for (uint32_t q = 0; q < ne; ++q) {
       const int64_t at = wbase + orr + (ie - ne) + q;
-      if constexpr (kPair)
-        macro_run[at] = encode_pair(static_cast<uint32_t>(k), mask, wide ? 1u : 0u, static_cast<int>(q));
-      else
+      if constexpr (kMask64) {   // 256 x 256 two-issuer path: the 4 x 8 runs of each half, entries 2 * at, +1
+        const int64_t at2 = wbase + 2 * (orr + (ie - ne) + q);
+        macro_run[at2] = encode_runs(static_cast<uint32_t>(k), static_cast<uint32_t>(mask), wide ? 1u : 0u);
+        macro_run[at2 + 1] = encode_runs(static_cast<uint32_t>(k), static_cast<uint32_t>(mask >> 32), wide ? 1u : 0u);
+      } else
         macro_run[at] = encode_runs(static_cast<uint32_t>(k), static_cast<uint32_t>(mask), wide ? 1u : 0u);
     }
     mbase += tm;
-    wbase += tr;
+    wbase += kMask64 ? 2 * tr : tr;
     if (kb + kKB >= BK) {   // last k block of the macro-tile: counts
 #pragma unroll
       for (int li = 0; li < MI; ++li) {
@@ -831,7 +787,7 @@ spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_
   }
   // row_work [BM], hist [BK+2] and totals [2] are contiguous in one allocation (see api.cu)
   SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 4), s));
-  if (p.MI == kMacroI_pair) return fused_t<kMacroI_pair, kMacroJ_umma>(p, gi0, gi1, s);
+  if (p.MI == kMacroI_dual) return fused_t<kMacroI_dual, kMacroJ_umma>(p, gi0, gi1, s);
   if (p.MJ == kMacroJ_umma) return fused_t<kMacroI, kMacroJ_umma>(p, gi0, gi1, s);
   return fused_t<kMacroI, kMacroJ_simt>(p, gi0, gi1, s);
 }
@@ -843,8 +799,8 @@ spamm_status launch_leaf_expand(Plan& p, cudaStream_t s) {
   const int64_t n_macro = (gi1 - gi0) * p.GN;
   if (n_macro <= 0) return SPAMM_OK;
   const int64_t blocks = (n_macro + kWarps - 1) / kWarps;
-  if (p.MI == kMacroI_pair)
-    leaf_expand_kernel<kMacroI_pair, kMacroJ_umma><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
+  if (p.MI == kMacroI_dual)
+    leaf_expand_kernel<kMacroI_dual, kMacroJ_umma><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
         p.BM, p.BK, p.BN, p.GN, gi0, n_macro, p.U, p.macro_ent, p.V, p.leaf_start, p.leaf_k);
   else if (p.MJ == kMacroJ_umma)
     leaf_expand_kernel<kMacroI, kMacroJ_umma><<<static_cast<unsigned>(blocks), kWarps * 32, 0, s>>>(
