@@ -133,10 +133,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
     int tq_s = 0;
     uint32_t tq_ph = 0;
     auto claim = [&]() -> DTile {
+      DTile d{-1, 0, 0};
       unsigned int idx = 0;
       if (lane == 0) idx = atomicAdd(sched, 1u);
       idx = __shfl_sync(0xffffffffu, idx, 0);
-      DTile d{-1, 0, 0};
       if (static_cast<int64_t>(idx) < n_work) {
         d.t = order[idx];
         d.e0 = mstart[d.t];
@@ -297,14 +297,20 @@ __global__ void __launch_bounds__(kDThreads, 1)
       uint32_t ph = 0;
       uint32_t tile_par = 0;
       bool fin = false;
-      unsigned long long c_full = 0, c_te = 0, c_mma = 0, c_cm = 0, n_st = 0;
+      unsigned long long c_full = 0, c_te = 0, c_mma = 0, c_cm = 0, n_st = 0, c_head = 0;
+      int st_in_tile = 0;
       const unsigned long long c_start = clock64();
       while (!fin) {
 #pragma unroll 1
         for (int st = 0; st < kDStages; ++st) {
           const unsigned long long ta = prof ? clock64() : 0;
           mbar_wait(&full[st], ph);
-          if (prof) c_full += clock64() - ta;
+          if (prof) {
+            const unsigned long long dw = clock64() - ta;
+            c_full += dw;
+            if (st_in_tile < 3) c_head += dw;
+            ++st_in_tile;
+          }
           tc_fence_after();
           uint4 rs;
           asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -363,6 +369,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
           if (fl & kLast) {
             umma_commit(&tfull[h]);
             tile_par ^= 1;
+            st_in_tile = 0;
           }
           if (prof) {
             const unsigned long long te = clock64();
@@ -381,6 +388,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
         pr[3] = c_mma;
         pr[4] = c_cm;
         pr[5] = n_st;
+        if (h == 0) prof[blockIdx.x * 16 + 13] = c_head;
       }
     }
     __syncwarp();
@@ -586,7 +594,8 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
       fprintf(stderr, "[dual prof] issuer %d cycles/CTA %.0f (min %.0f max %.0f): full-wait %.0f tmem-empty %.0f "
               "mma %.0f commit %.0f stages %.0f\n", h, a[6 * h], mn, mx, a[6 * h + 1], a[6 * h + 2], a[6 * h + 3],
               a[6 * h + 4], a[6 * h + 5]);
-    fprintf(stderr, "[dual prof] epilogue warp 4 tmem-full wait %.0f\n", a[12]);
+    fprintf(stderr, "[dual prof] epilogue warp 4 tmem-full wait %.0f; issuer 0 full-wait in a tile's first 3 stages %.0f\n",
+            a[12], a[13]);
   }
   return SPAMM_OK;
 }

@@ -11,6 +11,7 @@
 // tile's position, so equal tiles give bit-identical norms (Toeplitz inputs).  TMA's
 // out-of-bounds zero fill implements the zero padding of PAPER.md:99.  A and B are
 // normed by one launch.
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -25,11 +26,11 @@ using namespace sm100;
 constexpr int kWarps = 8;              // warps per CTA, each reducing 32 / kWarps rows of a box
 constexpr int kRowsPerWarp = 32 / kWarps;
 constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 4;
 constexpr int kBoxBytesRow = 512;      // bytes per box row (256 BF16 / 128 FP32 columns)
 constexpr int kBoxBytes = 32 * kBoxBytesRow;   // 16 KB
-constexpr int kBoxesPerCta = 8;        // column boxes walked by one CTA
-constexpr size_t kSmemBytes = 128 + static_cast<size_t>(kStages) * kBoxBytes + 1024;
+constexpr int kBoxesPerCta = 16;       // max column boxes walked by one CTA
+template <int S>
+constexpr size_t smem_bytes() { return 128 + static_cast<size_t>(S) * kBoxBytes + 1024; }
 
 template <typename T>
 __device__ __forceinline__ double sq16(const uint4& raw);
@@ -108,7 +109,7 @@ __device__ __forceinline__ void write_planes<float>(const NormJob& j, const uint
 }
 
 // grid = (max ncb, nrowA + nrowB); blockIdx.y < nrowA -> job A else job B.
-template <typename T>
+template <typename T, int kStages>
 __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_constant__ CUtensorMap tmA,
                                                               const __grid_constant__ CUtensorMap tmB, NormJob ja,
                                                               NormJob jb) {
@@ -187,14 +188,14 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
                       int64_t bj0, int64_t bj1, cudaStream_t s, CUtensorMapDataType dt) {
   constexpr int kCols = kBoxBytesRow / sizeof(T);
   CUtensorMap tA{}, tB{};
-  NormJob ja{p.M, p.K, p.nA, p.BK, 1, ar0, ar1 - ar0, 0, kBoxesPerCta, nullptr, 0, 0, nullptr, 0, 0};
+  NormJob ja{p.M, p.K, p.nA, p.BK, 1, ar0, ar1 - ar0, 0, 8, nullptr, 0, 0, nullptr, 0, 0};
   if (p.prec == SPAMM_FP32X3 && p.planes) {
     ja.planes = p.planes;
     ja.pld = p.ldpa;
   }
   // B column strip [bj0*32, bj1*32): treated as a (K x cols) matrix; tile row k, tile col j -> nBt[j*BK + k]
   const int64_t bcols = std::min<int64_t>(p.N, bj1 * kTile) - bj0 * kTile;
-  NormJob jb{p.K, bcols > 0 ? bcols : 0, p.nBt + bj0 * p.BK, 1, p.BK, 0, bj1 > bj0 ? p.BK : 0, 0, kBoxesPerCta, nullptr, 0, 0,
+  NormJob jb{p.K, bcols > 0 ? bcols : 0, p.nBt + bj0 * p.BK, 1, p.BK, 0, bj1 > bj0 ? p.BK : 0, 0, 8, nullptr, 0, 0,
              nullptr, 0, 0};
   if (p.prec == SPAMM_FP32X3 && p.planes) {
     jb.planes = p.planes + 3 * p.M * p.ldpa;
@@ -213,7 +214,11 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
   }
   // boxes per CTA: 8 (128 KB streamed per CTA) unless that leaves fewer than ~4 CTAs per SM,
   // then fewer so that small problems are not latency-bound on a handful of CTAs
-  int bpc = kBoxesPerCta;
+  // ring depth and boxes per CTA (experiments: SPAMM_NORM_STAGES 2..4, SPAMM_NORM_BPC 1..16)
+  // default 2 stages (33 KB): 6 CTAs per SM, so the N = 8192 grid runs in ~one wave (measured
+  // 29.3 vs 31.1 us with 4 stages, r01f)
+  const int stages = getenv("SPAMM_NORM_STAGES") ? std::min(4, std::max(2, atoi(getenv("SPAMM_NORM_STAGES")))) : 2;
+  int bpc = getenv("SPAMM_NORM_BPC") ? std::min(kBoxesPerCta, std::max(1, atoi(getenv("SPAMM_NORM_BPC")))) : 8;
   auto ncb_of = [&](const NormJob& jj, int b) -> int64_t {
     const int64_t per_cta = static_cast<int64_t>(b) * kCols;
     return jj.nrow > 0 ? (jj.cols + per_cta - 1) / per_cta : 0;
@@ -231,8 +236,12 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
   }
   static bool attr = false;
   if (!attr) {
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kSmemBytes)));
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem_bytes<2>())));
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem_bytes<3>())));
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem_bytes<4>())));
     attr = true;
   }
   const int64_t gx = std::max(ja.ncb, jb.ncb);
@@ -240,7 +249,12 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
   if (gx <= 0 || gy <= 0) return SPAMM_OK;
   if (gy > 65535) return fail(SPAMM_E_UNSUPPORTED, "more than 65535 tile rows in one norm launch");
   dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
-  tile_norms_kernel<T><<<grid, kThreads, kSmemBytes, s>>>(tA, tB, ja, jb);
+  if (stages == 2)
+    tile_norms_kernel<T, 2><<<grid, kThreads, smem_bytes<2>(), s>>>(tA, tB, ja, jb);
+  else if (stages == 3)
+    tile_norms_kernel<T, 3><<<grid, kThreads, smem_bytes<3>(), s>>>(tA, tB, ja, jb);
+  else
+    tile_norms_kernel<T, 4><<<grid, kThreads, smem_bytes<4>(), s>>>(tA, tB, ja, jb);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;

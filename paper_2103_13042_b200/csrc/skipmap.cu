@@ -258,15 +258,21 @@ __device__ __forceinline__ uint32_t col_pattern8(uint32_t mask, int lj) {
 __device__ __forceinline__ uint4 encode_runs(uint32_t k, uint32_t mask, uint32_t wide = 0u) {
   if (mask == 0xFFFFFFFFu)   // all 4 x 8 pairs kept: one run j0 = 0, len = 8, pattern 1111
     return make_uint4(k | (1u << 16) | (0xFFu << 24), 0u | (7u << 3) | (15u << 6), 0u, wide << 31);
+  // bit lj of bnd: column lj's 4-bit pattern differs from column lj+1's (any row byte differs);
+  // bit lj of nz: column lj has a kept pair.  Runs = maximal segments between boundaries
+  // whose columns are non-zero (same result as walking the columns, a fraction of the ops).
+  const uint32_t d = (mask ^ (mask >> 1)) & 0x7F7F7F7Fu;
+  const uint32_t bnd = (d | (d >> 8) | (d >> 16) | (d >> 24)) & 0x7Fu;
+  const uint32_t nz = (mask | (mask >> 8) | (mask >> 16) | (mask >> 24)) & 0xFFu;
   uint32_t words[3] = {0u, 0u, 0u};
   uint32_t nr = 0, cols = 0;
-  int j = 0;
+  uint32_t j = 0;
   while (j < 8) {
-    const uint32_t pat = col_pattern8(mask, j);
-    int j1 = j + 1;
-    while (j1 < 8 && col_pattern8(mask, j1) == pat) ++j1;
-    if (pat) {
-      const uint32_t run = static_cast<uint32_t>(j) | (static_cast<uint32_t>(j1 - j - 1) << 3) | (pat << 6);
+    const uint32_t b = bnd >> j;
+    const uint32_t j1 = b ? j + static_cast<uint32_t>(__ffs(b)) : 8u;
+    if ((nz >> j) & 1u) {
+      const uint32_t pat = col_pattern8(mask, static_cast<int>(j));
+      const uint32_t run = j | ((j1 - j - 1) << 3) | (pat << 6);
       words[nr / 3] |= run << (10 * (nr % 3));
       ++nr;
       cols |= ((1u << (j1 - j)) - 1u) << j;

@@ -1,0 +1,9 @@
+#!/bin/bash
+OUT=gpurun_out
+mkdir -p $OUT
+python -m paper_2103_13042_b200.build > /dev/null
+timeout 120 ./scripts/probe_tma_rings > $OUT/probe_tma_rings.log 2>&1; cat $OUT/probe_tma_rings.log
+timeout 900 python -m pytest tests/test_gpu_variants.py tests/test_gpu_parity.py -q -x 2>&1 | tail -2
+B="python bench.py --no-sweep --no-cpu-baseline --no-e2e --steps 200"
+for pf in 0 1; do echo "prefetch $pf"; SPAMM_DUAL_PREFETCH=$pf timeout 300 $B 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['stages_ms'], d['roofline']['frac'])"; done
+for pf in 0 1; do SPAMM_DUAL_PREFETCH=$pf SPAMM_DEBUG_UMMA_PROF=1 timeout 300 python bench.py --no-sweep --no-cpu-baseline --no-e2e --steps 3 --warmup 3 2>&1 | grep "prof\]" | tail -3; done
