@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
                           const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
-                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof) {
+                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait) {
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
   constexpr int kDStages = DCfg<kPack>::kStages, kDStageBytes = DCfg<kPack>::kStageBytes;
@@ -398,27 +398,27 @@ __global__ void __launch_bounds__(kDThreads, 1)
     const int h = (warp - 4) >> 2;       // accumulator half (C rows 128h ..)
     if (lane == 0) mbar_arrive(&tempty[h]);   // the accumulator starts empty
     const int t0 = lane & 3, t1 = lane >> 2;
-    // zero-fill units: 8 rows x 256 columns of an empty macro-tile, dealt round-robin
-    const int64_t n_units = n_empty * 32;
-    const int64_t u_stride = static_cast<int64_t>(gridDim.x) * 8;
-    int64_t u_next = static_cast<int64_t>(blockIdx.x) * 8 + (warp - 4);
+    // Zero-fill of the macro-tiles without kept pairs (the LPT tail of `order`), done LAST: an
+    // epilogue warp whose CTA has no more tiles claims 32-row units (32 KB of C) from a global
+    // counter, so the CTAs that finish their MMA work early absorb it (the slowest one takes
+    // none).  Done greedily at the start instead, the 141 MB of zero writes at the bench point
+    // compete with the operand loads' first DRAM touches (multiply 165 vs 152 us without them).
+    const int64_t n_units = n_empty * 8;
     auto zero_unit = [&]() -> bool {
-      if (u_next >= n_units) return false;
-      const int64_t u = u_next;
-      u_next += u_stride;
-      const int64_t t = order[n_work + u / 32];
-      const int64_t r0 = (t / GN) * 256 + (u % 32) * 8, c0 = (t % GN) * 256;
+      if (dbg & 1) return false;   // dbg 1: no zero-fill (timing experiments only)
+      unsigned int u32 = 0;
+      if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
+      const int64_t u = __shfl_sync(0xffffffffu, u32, 0);
+      if (u >= n_units) return false;
+      const int64_t t = order[n_work + u / 8];
+      const int64_t row = (t / GN) * 256 + (u % 8) * 32 + lane, c0 = (t % GN) * 256;
       const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
       const uint32_t bytes = static_cast<uint32_t>(ncol * 4) & ~15u;
-      if (lane == 0) {
-        for (int r = 0; r < 8; ++r) {
-          const int64_t row = r0 + r;
-          if (row >= M) break;
-          if (bytes) bulk_store_1d(C + row * ldc + c0, sZero, bytes);
-          for (int64_t cc = bytes / 4; cc < ncol; ++cc) C[row * ldc + c0 + cc] = 0.f;
-        }
-        bulk_commit_group();
+      if (row < M) {   // one row per lane: 32 bulk (TMA-engine) stores of the 1 KB zero buffer
+        if (bytes) bulk_store_1d(C + row * ldc + c0, sZero, bytes);
+        for (int64_t cc = bytes / 4; cc < ncol; ++cc) C[row * ldc + c0 + cc] = 0.f;
       }
+      bulk_commit_group();
       return true;
     };
     int tq_s = 0;
@@ -436,11 +436,11 @@ __global__ void __launch_bounds__(kDThreads, 1)
       if (cur.t < 0) break;
       const int64_t I = cur.t / GN, J = cur.t % GN;
       const unsigned long long tw = prof ? clock64() : 0;
-      while (!mbar_try_wait(&tfull[h], par))
-        if (!zero_unit()) {
-          mbar_wait(&tfull[h], par);
-          break;
-        }
+      // while the accumulator fills: at most zf_per_wait zero-fill units (spread over the kernel
+      // instead of a burst at its start), the remainder after the last tile
+      for (int z = 0; z < zf_per_wait && !mbar_try_wait(&tfull[h], par); ++z)
+        if (!zero_unit()) break;
+      mbar_wait(&tfull[h], par);
       par ^= 1;
       if (prof && warp == 4 && lane == 0) prof[blockIdx.x * 16 + 12] += clock64() - tw;
       tc_fence_after();
@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
           float* cb = C + rb * ldc + col;
           const float2 pa = make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
           const float2 pb = make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          if (dbg & 2) continue;   // dbg 2: no C stores (timing experiments only)
           if (col + 1 < N) {
             if (ra < M) __stcs(reinterpret_cast<float2*>(ca), pa);
             if (rb < M) __stcs(reinterpret_cast<float2*>(cb), pb);
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
     }
     while (zero_unit()) {
     }
-    if (lane == 0) bulk_wait_group<0>();
+    bulk_wait_group<0>();   // zero-fill stores complete before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
@@ -571,12 +572,18 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   // (beta * C_old, chained norms)
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
   SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, 2 * sizeof(unsigned int), s));
+  // SPAMM_DEBUG_DUAL_MODE: timing experiments that break the result (bit 1: no zero-fill of empty tiles,
+  // bit 2: no C stores)
+  const int dbg = getenv("SPAMM_DEBUG_DUAL_MODE") ? atoi(getenv("SPAMM_DEBUG_DUAL_MODE")) : 0;
+  // zero-fill units an epilogue warp may take while waiting for one accumulator (SPAMM_DUAL_ZF)
+  const int zf_per_wait = getenv("SPAMM_DUAL_ZF") ? atoi(getenv("SPAMM_DUAL_ZF")) : 0;   // measured best: all at the end (r01k)
   static unsigned long long* prof = nullptr;
   if (getenv("SPAMM_DEBUG_UMMA_PROF") && !prof) cudaMalloc(&prof, 1024 * 16 * 8);
   if (prof) cudaMemsetAsync(prof, 0, 1024 * 16 * 8, s);
   kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, kGen ? nullptr : p.hist, p.GN, C, ldc, p.M,
                                        p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                       DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl}, prof);
+                                       DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl}, prof, dbg,
+                                       zf_per_wait);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (prof) {
