@@ -59,6 +59,8 @@ struct DCfg {
 
 constexpr uint32_t kFullRun = 0u | (7u << 3) | (15u << 6);
 constexpr uint32_t kFirst = 1u << 29, kLast = 1u << 30, kNoStep = 1u << 28, kEnd = 1u << 27;
+// stage holds k-steps k, k+1 as 64-deep boxes: A [128 x 64] SW128 per half, B [64 x 32] per column
+constexpr uint32_t kWideSt = 1u << 25;
 
 struct DTile {
   int64_t t, e0, e1;   // macro-tile, k-step range [e0, e1) (in k-steps, entry pairs)
@@ -66,7 +68,9 @@ struct DTile {
 
 struct DMaps {
   CUtensorMap a1;      // A [128 x 32] boxes, SW64
+  CUtensorMap a2;      // A [128 x 64] boxes, SW128 (a stage of two consecutive k-steps)
   CUtensorMap b1[4];   // B stacked [32 k x 32 n] boxes, 8/4/2/1 boxes, SW64
+  CUtensorMap b2[4];   // B stacked [64 k x 32 n] boxes (two consecutive k-steps), SW64
 };
 
 struct DChain {
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
                           const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
-                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait) {
+                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait, int wide_ok) {
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
   constexpr int kDStages = DCfg<kPack>::kStages, kDStageBytes = DCfg<kPack>::kStageBytes;
@@ -127,7 +131,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------- producer A: tile claims, srun, A boxes
-    if (lane == 0) tma_prefetch_desc(&mp.a1);
+    if (lane == 0) {
+      tma_prefetch_desc(&mp.a1);
+      tma_prefetch_desc(&mp.a2);
+    }
     int s = 0;
     uint32_t ph = 0;
     int tq_s = 0;
@@ -184,14 +191,27 @@ __global__ void __launch_bounds__(kDThreads, 1)
             // (batches hold 32 k-steps, a multiple of kPack: a stage never spans two batches,
             // and only a tile's last stage can be partly empty)
             const int np = cnt - q < kPack ? cnt - q : kPack;
+            // two consecutive k-tiles: one 64-deep box per A half and per B column range
+            const bool wide = wide_ok && kPack == 2 && np == 2 &&
+                              (sent[2 * q + 2].x & 0xFFFFu) == (sent[2 * q].x & 0xFFFFu) + 1u;
             uint32_t tx = 0;
-            for (int j = 0; j < np; ++j) {
-              const uint32_t x0 = sent[2 * (q + j)].x, x1 = sent[2 * (q + j) + 1].x;
-              const uint32_t cols = (x0 >> 24) | (x1 >> 24);
+            if (wide) {
+              const uint32_t x00 = sent[2 * q].x, x01 = sent[2 * q + 1].x, x10 = sent[2 * q + 2].x,
+                             x11 = sent[2 * q + 3].x;
+              const uint32_t cols = (x00 | x01 | x10 | x11) >> 24;
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
-              tx += 8192u * ((((x0 >> 16) & 15u) != 0u ? 1u : 0u) + (((x1 >> 16) & 15u) != 0u ? 1u : 0u)) + 2048u * len;
+              const bool h0 = ((x00 | x10) >> 16) & 15u, h1 = ((x01 | x11) >> 16) & 15u;
+              tx = 16384u * ((h0 ? 1u : 0u) + (h1 ? 1u : 0u)) + 4096u * len;
+            } else {
+              for (int j = 0; j < np; ++j) {
+                const uint32_t x0 = sent[2 * (q + j)].x, x1 = sent[2 * (q + j) + 1].x;
+                const uint32_t cols = (x0 >> 24) | (x1 >> 24);
+                const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
+                tx += 8192u * ((((x0 >> 16) & 15u) != 0u ? 1u : 0u) + (((x1 >> 16) & 15u) != 0u ? 1u : 0u)) + 2048u * len;
+              }
             }
-            const uint32_t fl = (eb + q == cur.e0 ? kFirst : 0u) | (eb + q + np == cur.e1 ? kLast : 0u);
+            const uint32_t fl = (eb + q == cur.e0 ? kFirst : 0u) | (eb + q + np == cur.e1 ? kLast : 0u) |
+                                (wide ? kWideSt : 0u);
             mbar_wait(&empty[s], ph ^ 1);
             for (int j = 0; j < kPack; ++j) {
               uint4 e0 = make_uint4(0, 0, 0, 0), e1 = make_uint4(0, 0, 0, 0);
@@ -207,12 +227,21 @@ __global__ void __launch_bounds__(kDThreads, 1)
               srun[2 * (kPack * s + j) + 1] = e1;
             }
             mbar_arrive_expect_tx(&full[s], tx);
-            for (int j = 0; j < np; ++j) {
-              const uint32_t x0 = sent[2 * (q + j)].x, x1 = sent[2 * (q + j) + 1].x;
-              const int32_t k0 = static_cast<int32_t>(x0 & 0xFFFFu) * 32;
-              uint8_t* adst = smem + s * kDStageBytes + j * kDStepBytes;
-              if ((x0 >> 16) & 15u) tma_load_2d(adst, &mp.a1, &full[s], k0, I * 256);
-              if ((x1 >> 16) & 15u) tma_load_2d(adst + 8192, &mp.a1, &full[s], k0, I * 256 + 128);
+            if (wide) {
+              const uint32_t x00 = sent[2 * q].x, x01 = sent[2 * q + 1].x, x10 = sent[2 * q + 2].x,
+                             x11 = sent[2 * q + 3].x;
+              const int32_t k0 = static_cast<int32_t>(x00 & 0xFFFFu) * 32;
+              uint8_t* adst = smem + s * kDStageBytes;
+              if (((x00 | x10) >> 16) & 15u) tma_load_2d(adst, &mp.a2, &full[s], k0, I * 256);
+              if (((x01 | x11) >> 16) & 15u) tma_load_2d(adst + 16384, &mp.a2, &full[s], k0, I * 256 + 128);
+            } else {
+              for (int j = 0; j < np; ++j) {
+                const uint32_t x0 = sent[2 * (q + j)].x, x1 = sent[2 * (q + j) + 1].x;
+                const int32_t k0 = static_cast<int32_t>(x0 & 0xFFFFu) * 32;
+                uint8_t* adst = smem + s * kDStageBytes + j * kDStepBytes;
+                if ((x0 >> 16) & 15u) tma_load_2d(adst, &mp.a1, &full[s], k0, I * 256);
+                if ((x1 >> 16) & 15u) tma_load_2d(adst + 8192, &mp.a1, &full[s], k0, I * 256 + 128);
+              }
             }
             if (++s == kDStages) {
               s = 0;
@@ -226,7 +255,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
   } else if (warp == 3) {
     // ---------------------------------------------------------------- producer B
     if (lane == 0)
-      for (int q = 0; q < 4; ++q) tma_prefetch_desc(&mp.b1[q]);
+      for (int q = 0; q < 4; ++q) {
+        tma_prefetch_desc(&mp.b1[q]);
+        tma_prefetch_desc(&mp.b2[q]);
+      }
     int s = 0;
     uint32_t ph = 0;
     int tq_s = 0;
@@ -259,8 +291,24 @@ __global__ void __launch_bounds__(kDThreads, 1)
         if (lane == 0) {
           for (int q = 0; q < cnt; q += kPack) {
             const int np = cnt - q < kPack ? cnt - q : kPack;
+            const bool wide = wide_ok && kPack == 2 && np == 2 &&
+                              (sentB[2 * q + 2].x & 0xFFFFu) == (sentB[2 * q].x & 0xFFFFu) + 1u;
             mbar_wait(&empty[s], ph ^ 1);
-            for (int j = 0; j < np; ++j) {
+            if (wide) {
+              const uint32_t cols = (sentB[2 * q].x | sentB[2 * q + 1].x | sentB[2 * q + 2].x | sentB[2 * q + 3].x) >> 24;
+              const int32_t k0 = static_cast<int32_t>(sentB[2 * q].x & 0xFFFFu) * 32;
+              uint8_t* bdst = smem + s * kDStageBytes + 2 * kDASlot;
+              const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
+              if (len == 8) {
+                tma_load_3d(bdst, &mp.b2[0], &full[s], 0, k0, jb);
+              } else {
+                int off = c0;
+                if (len & 4) { tma_load_3d(bdst + off * 4096, &mp.b2[1], &full[s], 0, k0, jb + off); off += 4; }
+                if (len & 2) { tma_load_3d(bdst + off * 4096, &mp.b2[2], &full[s], 0, k0, jb + off); off += 2; }
+                if (len & 1) { tma_load_3d(bdst + off * 4096, &mp.b2[3], &full[s], 0, k0, jb + off); }
+              }
+            }
+            for (int j = 0; j < (wide ? 0 : np); ++j) {
               const uint32_t x0 = sentB[2 * (q + j)].x, x1 = sentB[2 * (q + j) + 1].x;
               const uint32_t cols = (x0 >> 24) | (x1 >> 24);
               const int32_t k0 = static_cast<int32_t>(x0 & 0xFFFFu) * 32;
@@ -297,7 +345,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
       uint32_t ph = 0;
       uint32_t tile_par = 0;
       bool fin = false;
-      unsigned long long c_full = 0, c_te = 0, c_mma = 0, c_cm = 0, n_st = 0, c_head = 0;
+      unsigned long long c_full = 0, c_te = 0, c_mma = 0, c_cm = 0, n_st = 0, c_head = 0, n_tiles_done = 0;
       int st_in_tile = 0;
       const unsigned long long c_start = clock64();
       while (!fin) {
@@ -337,12 +385,17 @@ __global__ void __launch_bounds__(kDThreads, 1)
                            : "r"(srun_addr + st * (32 * kPack) + 32 * j));
             const uint32_t nr = (rs.x >> 16) & 15u;
             if ((fl & kNoStep) || nr == 0u) continue;
-            // A: K-major SW64 rows of 32 (SBO 512), +32 B per K=16; half h at +8 KB
-            // B: MN-major SW64 boxes of 32 columns (LBO = 2048), +1024 B per K=16
-            const uint32_t a_addr = base_addr + st * kDStageBytes + j * kDStepBytes + 8192u * static_cast<uint32_t>(h);
-            const uint32_t b_addr = base_addr + st * kDStageBytes + j * kDStepBytes + kDASlot;
-            const uint64_t ad = smem_desc(a_addr, 16, 512, kLayoutSW64);
-            const uint64_t bd = smem_desc(b_addr, 2048, 512, kLayoutSW64);
+            // 32-deep slots: A K-major SW64 rows of 32 (SBO 512), +32 B per K=16, half h at +8 KB;
+            //   B MN-major SW64 boxes of 32 columns x 32 k (LBO = 2048), +1024 B per K=16.
+            // wide stage (k-steps k, k+1): A SW128 rows of 64 (SBO 1024), half h at +16 KB, k-step j
+            //   at +64 B; B boxes of 32 columns x 64 k (LBO = 4096) after 32 KB of A, k-step j at +2 KB.
+            const bool wst = (fl & kWideSt) != 0u;
+            const uint32_t st_addr = base_addr + st * kDStageBytes;
+            const uint64_t ad = wst ? smem_desc(st_addr + 16384u * static_cast<uint32_t>(h), 16, 1024, kLayoutSW128) + 4u * j
+                                    : smem_desc(st_addr + j * kDStepBytes + 8192u * static_cast<uint32_t>(h), 16, 512, kLayoutSW64);
+            const uint64_t bd = wst ? smem_desc(st_addr + 2 * kDASlot, 4096, 512, kLayoutSW64) + 128u * j
+                                    : smem_desc(st_addr + j * kDStepBytes + kDASlot, 2048, 512, kLayoutSW64);
+            const uint32_t bbox = wst ? 256u : 128u;   // descriptor units (16 B) per column box
             if (nr == 1u && rs.y == kFullRun) {
               umma_f16(dcol, ad, bd, idesc_full, 1u, 0u, 0u, 0u, 0u);
               umma_f16(dcol, ad + 2, bd + 64, idesc_full, 1u, 0u, 0u, 0u, 0u);
@@ -357,7 +410,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
                 const uint32_t idesc = idesc_base | (len << 19);
                 const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;   // 0 keep, ~0 disable
                 const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
-                const uint64_t bj = bd + static_cast<uint64_t>(j0 * 128u);          // 2048 B per column box
+                const uint64_t bj = bd + static_cast<uint64_t>(j0 * bbox);
                 const uint32_t d = dcol + j0 * 32u;
                 umma_f16(d, ad, bj, idesc, 1u, m0, m1, m2, m3);
                 umma_f16(d, ad + 2, bj + 64, idesc, 1u, m0, m1, m2, m3);
@@ -370,6 +423,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
             umma_commit(&tfull[h]);
             tile_par ^= 1;
             st_in_tile = 0;
+            ++n_tiles_done;
           }
           if (prof) {
             const unsigned long long te = clock64();
@@ -388,7 +442,13 @@ __global__ void __launch_bounds__(kDThreads, 1)
         pr[3] = c_mma;
         pr[4] = c_cm;
         pr[5] = n_st;
-        if (h == 0) prof[blockIdx.x * 16 + 13] = c_head;
+        if (h == 0) {
+          prof[blockIdx.x * 16 + 13] = c_head;
+          prof[blockIdx.x * 16 + 14] = n_tiles_done;
+          unsigned int smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          prof[blockIdx.x * 16 + 15] = smid;
+        }
       }
     }
     __syncwarp();
@@ -554,10 +614,14 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   DMaps mp;
   std::memset(&mp, 0, sizeof(mp));
   SPAMM_TRY(encode_tmap_2d(&mp.a1, dt, 2, A, p.K, p.M, lda, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B));
+  SPAMM_TRY(encode_tmap_2d(&mp.a2, dt, 2, A, p.K, p.M, lda, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B));
   const uint32_t nbs[4] = {8, 4, 2, 1};
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < 4; ++q) {
     SPAMM_TRY(encode_tmap_3d(&mp.b1[q], dt, B, 32, p.K, p.N / 32, static_cast<uint64_t>(ldb) * 2, 64, 32, 32, nbs[q],
                              CU_TENSOR_MAP_SWIZZLE_64B));
+    SPAMM_TRY(encode_tmap_3d(&mp.b2[q], dt, B, 32, p.K, p.N / 32, static_cast<uint64_t>(ldb) * 2, 64, 32, 64, nbs[q],
+                             CU_TENSOR_MAP_SWIZZLE_64B));
+  }
   auto kern = spamm_mul_dual_kernel<kFmt, kGen, kPack>;
   constexpr size_t kDSmem = DCfg<kPack>::kSmem;
   static bool attr_set = false;
@@ -575,6 +639,8 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   // SPAMM_DEBUG_DUAL_MODE: timing experiments that break the result (bit 1: no zero-fill of empty tiles,
   // bit 2: no C stores)
   const int dbg = getenv("SPAMM_DEBUG_DUAL_MODE") ? atoi(getenv("SPAMM_DEBUG_DUAL_MODE")) : 0;
+  // stages of two consecutive k-steps load 64-deep boxes (SPAMM_DUAL_WIDE=0 disables)
+  const bool wide_ok = !getenv("SPAMM_DUAL_WIDE") || atoi(getenv("SPAMM_DUAL_WIDE")) != 0;
   // zero-fill units an epilogue warp may take while waiting for one accumulator (SPAMM_DUAL_ZF)
   const int zf_per_wait = getenv("SPAMM_DUAL_ZF") ? atoi(getenv("SPAMM_DUAL_ZF")) : 0;   // measured best: all at the end (r01k)
   static unsigned long long* prof = nullptr;
@@ -583,7 +649,7 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, kGen ? nullptr : p.hist, p.GN, C, ldc, p.M,
                                        p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                        DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl}, prof, dbg,
-                                       zf_per_wait);
+                                       zf_per_wait, wide_ok && kPack == 2 ? 1 : 0);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (prof) {
@@ -603,6 +669,19 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
               a[6 * h + 4], a[6 * h + 5]);
     fprintf(stderr, "[dual prof] epilogue warp 4 tmem-full wait %.0f; issuer 0 full-wait in a tile's first 3 stages %.0f\n",
             a[12], a[13]);
+    if (getenv("SPAMM_DEBUG_UMMA_PROF_CTA")) {
+      double by_n[8] = {0}, cnt_n[8] = {0};
+      for (int c = 0; c < grid; ++c) {
+        const int nt = static_cast<int>(std::min<unsigned long long>(hp[c * 16 + 14], 7));
+        by_n[nt] += static_cast<double>(hp[c * 16]);
+        cnt_n[nt] += 1;
+      }
+      for (int n = 0; n < 8; ++n)
+        if (cnt_n[n] > 0) fprintf(stderr, "[dual cta] %d tiles: %.0f CTAs, mean issuer cycles %.0f\n", n, cnt_n[n], by_n[n] / cnt_n[n]);
+      for (int c = 0; c < grid; ++c)
+        fprintf(stderr, "[dual cta] cta %d sm %llu tiles %llu cycles %llu full %llu\n", c, hp[c * 16 + 15], hp[c * 16 + 14],
+                hp[c * 16], hp[c * 16 + 1]);
+    }
   }
   return SPAMM_OK;
 }
