@@ -129,7 +129,7 @@ spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, 
 static void free_plan(Plan* p) {
   if (!p) return;
   void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_start, p->L, p->leaf_base, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent, p->macro_run,
-                  p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp, p->sk_scratch, p->sk_ticket, p->sk_wpre,
+                  p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp, p->sk_scratch, p->sk_ticket, p->sk_wpre, p->split_cnt, p->split_scr,
                   p->planes, p->nC};
   for (void* q : ptrs)
     if (q) cudaFree(q);

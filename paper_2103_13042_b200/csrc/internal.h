@@ -61,6 +61,8 @@ struct Plan {
   int64_t* totals = nullptr;     // = hist + BK + 2: [0] kept pairs, [1] macro entries
   int64_t* mstart = nullptr;     // [GM*GN] start of each macro-tile's entries (t*BK or macro_ptr)
   int umma_variant = 5;          // tensor-path kernel: 0-2, 4 multiply_umma.cu, 5 multiply_dual.cu
+  unsigned int* split_cnt = nullptr;   // dual multiply k-split handshake counters (self-resetting)
+  float* split_scr = nullptr;          // dual multiply k-split partials
   bool dual = false;             // the two-issuer 256 x 256 path (variant 5, multiply_dual.cu): MI = 8, two 4 x 8 run entries per k-step
   int64_t* Uw = nullptr;         // [GM*GN] tensor-path entries per macro-tile (pairs merged) or = U
   // stream-K workspace of the tensor multiply (allocated on first use)

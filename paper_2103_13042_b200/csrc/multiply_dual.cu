@@ -45,8 +45,9 @@ using namespace sm100;
 constexpr int kDASlot = 256 * 32 * 2;                 // A[256 x 32] as two [128 x 32] SW64 boxes
 constexpr int kDBSlot = 32 * 256 * 2;                 // B[32 x 256] as eight [32 x 32] boxes
 constexpr int kDStepBytes = kDASlot + kDBSlot;        // one 32-deep k-step
-constexpr int kDThreads = 384;
+constexpr int kDThreads = 384;   // w0 A/claims, w1-2 MMA, w3 B, w4-11 epilogue
 constexpr int kDTQ = 4;                               // tile ring depth
+constexpr int64_t kMaxSplit = 148;                    // k-split tiles per launch (scratch: 256 KB each)
 // kPack k-steps of one macro-tile per ring stage (one wait / commit per stage for the issuers);
 // the ring holds 6 k-steps either way (192 KB)
 template <int kPack>
@@ -64,6 +65,8 @@ constexpr uint32_t kWideSt = 1u << 25;
 
 struct DTile {
   int64_t t, e0, e1;   // macro-tile, k-step range [e0, e1) (in k-steps, entry pairs)
+  int64_t part;        // 0 whole tile; 1 / 2 first / second half of a k-split tile (C = P1 + P2)
+  int64_t slot;        // k-split tiles: index into the handshake counters and the partial scratch
 };
 
 struct DMaps {
@@ -86,9 +89,19 @@ __global__ void __launch_bounds__(kDThreads, 1)
                           const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
-                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait, int wide_ok) {
+                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait, int wide_ok,
+                          unsigned int* __restrict__ split_cnt, float* __restrict__ split_scr, int64_t split_req) {
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
+  // k-split tail (plain epilogue only): split_req < 0 = the last (n_work mod grid) tiles
+  int64_t n_split = 0;
+  if (!kGen && split_cnt != nullptr) {
+    if (split_req >= 0)
+      n_split = split_req < n_work ? split_req : n_work;
+    else if (n_work > static_cast<int64_t>(gridDim.x))
+      n_split = n_work % static_cast<int64_t>(gridDim.x);
+    if (n_split > kMaxSplit) n_split = kMaxSplit;
+  }
   constexpr int kDStages = DCfg<kPack>::kStages, kDStageBytes = DCfg<kPack>::kStageBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -106,6 +119,15 @@ __global__ void __launch_bounds__(kDThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kDTQ);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // profiling timeline (globaltimer ns): [0] CTA start [1] prologue done [2] issuer 0 done
+  // [3] epilogue warp 4 last drain done [4] its zero-fill done [5] CTA end
+  unsigned long long* tl = prof ? prof + 1024 * 16 + blockIdx.x * 8 : nullptr;
+  auto stamp = [&](int i) {
+    unsigned long long g_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));
+    tl[i] = g_;
+  };
+  if (tl && threadIdx.x == 0) stamp(0);
   for (int i = threadIdx.x; i < 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
@@ -128,7 +150,31 @@ __global__ void __launch_bounds__(kDThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  if (tl && threadIdx.x == 0) stamp(1);
 
+  // Zero-fill of the macro-tiles without kept pairs (the LPT tail of `order`), done LAST: an
+  // epilogue warp whose CTA has no more tiles claims 32-row units (32 KB of C) from a global
+  // counter, so the CTAs that finish their MMA work early absorb it (the slowest one takes
+  // none).  Done greedily at the start instead, the 141 MB of zero writes at the bench point
+  // compete with the operand loads' first DRAM touches (multiply 165 vs 152 us without them).
+  const int64_t n_units = n_empty * 8;
+  auto zero_unit = [&]() -> bool {
+    if (dbg & 1) return false;   // dbg 1: no zero-fill (timing experiments only)
+    unsigned int u32 = 0;
+    if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
+    const int64_t u = __shfl_sync(0xffffffffu, u32, 0);
+    if (u >= n_units) return false;
+    const int64_t t = order[n_work + u / 8];
+    const int64_t row = (t / GN) * 256 + (u % 8) * 32 + lane, c0 = (t % GN) * 256;
+    const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
+    const uint32_t bytes = static_cast<uint32_t>(ncol * 4) & ~15u;
+    if (row < M) {   // one row per lane: 32 bulk (TMA-engine) stores of the 1 KB zero buffer
+      if (bytes) bulk_store_1d(C + row * ldc + c0, sZero, bytes);
+      for (int64_t cc = bytes / 4; cc < ncol; ++cc) C[row * ldc + c0 + cc] = 0.f;
+    }
+    bulk_commit_group();
+    return true;
+  };
   if (warp == 0) {
     // ------------------------------------------------- producer A: tile claims, srun, A boxes
     if (lane == 0) {
@@ -140,21 +186,32 @@ __global__ void __launch_bounds__(kDThreads, 1)
     int tq_s = 0;
     uint32_t tq_ph = 0;
     auto claim = [&]() -> DTile {
-      DTile d{-1, 0, 0};
+      DTile d{-1, 0, 0, 0, 0};
       unsigned int idx = 0;
       if (lane == 0) idx = atomicAdd(sched, 1u);
       idx = __shfl_sync(0xffffffffu, idx, 0);
-      if (static_cast<int64_t>(idx) < n_work) {
+      const int64_t n_whole = n_work - n_split;
+      if (static_cast<int64_t>(idx) < n_whole) {
         d.t = order[idx];
         d.e0 = mstart[d.t];
         d.e1 = d.e0 + mcount[d.t];
+      } else if (static_cast<int64_t>(idx) < n_whole + 2 * n_split) {
+        // the LPT tail's last n_split tiles in k-halves, both halves claimed back to back
+        const int64_t j = static_cast<int64_t>(idx) - n_whole;
+        d.t = order[n_whole + j / 2];
+        d.part = 1 + (j & 1);
+        d.slot = j / 2;
+        const int64_t e0 = mstart[d.t], cnt = mcount[d.t], mid = e0 + (cnt + 1) / 2;
+        d.e0 = d.part == 1 ? e0 : mid;
+        d.e1 = d.part == 1 ? mid : e0 + cnt;
       }
       return d;
     };
-    DTile nxt = claim();
+    // A tile is claimed when the previous one's loads have all been issued, not when it starts:
+    // claiming ahead assigns the LPT tail by start time instead of by finish time (the ring's
+    // three stages of issued loads hide the claim's latency).
+    DTile cur = claim();
     for (;;) {
-      const DTile cur = nxt;
-      if (cur.t >= 0) nxt = claim();
       if (lane == 0) {
         mbar_wait(&tq_empty[tq_s], tq_ph ^ 1);
         tq[tq_s] = cur;
@@ -176,6 +233,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
           ph ^= 1;
         }
         if (cur.t < 0) break;
+        cur = claim();
         continue;
       }
       const int32_t I = static_cast<int32_t>(cur.t / GN);
@@ -251,6 +309,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
         }
         __syncwarp();
       }
+      cur = claim();
     }
   } else if (warp == 3) {
     // ---------------------------------------------------------------- producer B
@@ -437,6 +496,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
       if (prof) {
         unsigned long long* pr = prof + blockIdx.x * 16 + h * 6;
         pr[0] = clock64() - c_start;
+        if (h == 0) stamp(2);
         pr[1] = c_full;
         pr[2] = c_te;
         pr[3] = c_mma;
@@ -458,29 +518,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
     const int h = (warp - 4) >> 2;       // accumulator half (C rows 128h ..)
     if (lane == 0) mbar_arrive(&tempty[h]);   // the accumulator starts empty
     const int t0 = lane & 3, t1 = lane >> 2;
-    // Zero-fill of the macro-tiles without kept pairs (the LPT tail of `order`), done LAST: an
-    // epilogue warp whose CTA has no more tiles claims 32-row units (32 KB of C) from a global
-    // counter, so the CTAs that finish their MMA work early absorb it (the slowest one takes
-    // none).  Done greedily at the start instead, the 141 MB of zero writes at the bench point
-    // compete with the operand loads' first DRAM touches (multiply 165 vs 152 us without them).
-    const int64_t n_units = n_empty * 8;
-    auto zero_unit = [&]() -> bool {
-      if (dbg & 1) return false;   // dbg 1: no zero-fill (timing experiments only)
-      unsigned int u32 = 0;
-      if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
-      const int64_t u = __shfl_sync(0xffffffffu, u32, 0);
-      if (u >= n_units) return false;
-      const int64_t t = order[n_work + u / 8];
-      const int64_t row = (t / GN) * 256 + (u % 8) * 32 + lane, c0 = (t % GN) * 256;
-      const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
-      const uint32_t bytes = static_cast<uint32_t>(ncol * 4) & ~15u;
-      if (row < M) {   // one row per lane: 32 bulk (TMA-engine) stores of the 1 KB zero buffer
-        if (bytes) bulk_store_1d(C + row * ldc + c0, sZero, bytes);
-        for (int64_t cc = bytes / 4; cc < ncol; ++cc) C[row * ldc + c0 + cc] = 0.f;
-      }
-      bulk_commit_group();
-      return true;
-    };
     int tq_s = 0;
     uint32_t tq_ph = 0;
     uint32_t par = 0;
@@ -505,6 +542,28 @@ __global__ void __launch_bounds__(kDThreads, 1)
       if (prof && warp == 4 && lane == 0) prof[blockIdx.x * 16 + 12] += clock64() - tw;
       tc_fence_after();
       const uint32_t tq_addr = tbase + 256u * static_cast<uint32_t>(h);
+      // k-split halves: per warp slice (32 rows x 256 columns), the first half to get here parks
+      // its partial in scratch; the second waits only for that write, adds (P1 + P2 = P2 + P1
+      // exactly, so the result does not depend on which half came first) and stores C
+      bool split_first = false;
+      unsigned int* scnt = nullptr;
+      float* sscr = nullptr;
+      if (cur.part != 0) {
+        const int slice = h * 4 + q;
+        scnt = split_cnt + (cur.slot * 8 + slice) * 2;
+        sscr = split_scr + (cur.slot * 8 + slice) * (32 * 256);
+        unsigned int old = 0;
+        if (lane == 0) old = atomicAdd(scnt, 1u);
+        split_first = __shfl_sync(0xffffffffu, old, 0) == 0u;
+        if (!split_first) {
+          if (lane == 0) {
+            const volatile unsigned int* d = scnt + 1;
+            while (*d == 0u) __nanosleep(64);
+          }
+          __syncwarp();
+          __threadfence();
+        }
+      }
       if (kGen) {
         double tsum[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // C tiles (I*8 + 4h + q, J*8 + c)
 #pragma unroll 1
@@ -586,9 +645,22 @@ __global__ void __launch_bounds__(kDThreads, 1)
           const int64_t col = J * 256 + c0 + 8 * i + 2 * t0;
           float* ca = C + ra * ldc + col;
           float* cb = C + rb * ldc + col;
-          const float2 pa = make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
-          const float2 pb = make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          float2 pa = make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
+          float2 pb = make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
           if (dbg & 2) continue;   // dbg 2: no C stores (timing experiments only)
+          if (cur.part != 0) {
+            const int r = 16 * lh + t1, cc = c0 + 8 * i + 2 * t0;   // within the warp's slice
+            float2* sa = reinterpret_cast<float2*>(sscr + r * 256 + cc);
+            float2* sb = reinterpret_cast<float2*>(sscr + (r + 8) * 256 + cc);
+            if (split_first) {
+              __stcg(sa, pa);
+              __stcg(sb, pb);
+              continue;
+            }
+            const float2 oa = __ldcg(sa), ob = __ldcg(sb);
+            pa = make_float2(oa.x + pa.x, oa.y + pa.y);
+            pb = make_float2(ob.x + pb.x, ob.y + pb.y);
+          }
           if (col + 1 < N) {
             if (ra < M) __stcs(reinterpret_cast<float2*>(ca), pa);
             if (rb < M) __stcs(reinterpret_cast<float2*>(cb), pb);
@@ -598,14 +670,30 @@ __global__ void __launch_bounds__(kDThreads, 1)
           }
         }
       }
+      if (cur.part != 0) {
+        if (split_first) {   // the partial is visible: release the second half
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicExch(scnt + 1, 1u);
+        } else {             // both halves are done with this slot: reset it for the next launch
+          __syncwarp();
+          if (lane == 0) {
+            scnt[0] = 0u;
+            scnt[1] = 0u;
+          }
+        }
+      }
     }
+    if (tl && warp == 4 && lane == 0) stamp(3);
     while (zero_unit()) {
     }
     bulk_wait_group<0>();   // zero-fill stores complete before the CTA retires
+    if (tl && warp == 4 && lane == 0) stamp(4);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tbase);
+  if (tl && threadIdx.x == 0) stamp(5);
 }
 
 template <uint32_t kFmt, bool kGen, int kPack>
@@ -639,21 +727,31 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   // SPAMM_DEBUG_DUAL_MODE: timing experiments that break the result (bit 1: no zero-fill of empty tiles,
   // bit 2: no C stores)
   const int dbg = getenv("SPAMM_DEBUG_DUAL_MODE") ? atoi(getenv("SPAMM_DEBUG_DUAL_MODE")) : 0;
+  // k-split of the LPT tail.s last tiles (SPAMM_DUAL_SPLIT=n tiles, -1 = n_work mod grid; default off)
+  const int64_t split_req = getenv("SPAMM_DUAL_SPLIT") ? atoll(getenv("SPAMM_DUAL_SPLIT")) : 0;   // measured slower (r01p)
+  if (!p.split_cnt) {   // [kMaxSplit][8 slices][arrived, done] counters + [kMaxSplit][8][32 x 256] partials
+    if (cudaMalloc(&p.split_cnt, sizeof(unsigned int) * kMaxSplit * 16) != cudaSuccess ||
+        cudaMalloc(&p.split_scr, sizeof(float) * kMaxSplit * 8 * 32 * 256) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SPAMM_E_NOMEM, "k-split workspace");
+    }
+    SPAMM_CUDA_TRY(cudaMemsetAsync(p.split_cnt, 0, sizeof(unsigned int) * kMaxSplit * 16, s));
+  }
   // stages of two consecutive k-steps load 64-deep boxes (SPAMM_DUAL_WIDE=0 disables)
   const bool wide_ok = !getenv("SPAMM_DUAL_WIDE") || atoi(getenv("SPAMM_DUAL_WIDE")) != 0;
   // zero-fill units an epilogue warp may take while waiting for one accumulator (SPAMM_DUAL_ZF)
   const int zf_per_wait = getenv("SPAMM_DUAL_ZF") ? atoi(getenv("SPAMM_DUAL_ZF")) : 0;   // measured best: all at the end (r01k)
   static unsigned long long* prof = nullptr;
-  if (getenv("SPAMM_DEBUG_UMMA_PROF") && !prof) cudaMalloc(&prof, 1024 * 16 * 8);
-  if (prof) cudaMemsetAsync(prof, 0, 1024 * 16 * 8, s);
+  if (getenv("SPAMM_DEBUG_UMMA_PROF") && !prof) cudaMalloc(&prof, 1024 * 24 * 8);
+  if (prof) cudaMemsetAsync(prof, 0, 1024 * 24 * 8, s);
   kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, kGen ? nullptr : p.hist, p.GN, C, ldc, p.M,
                                        p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                        DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl}, prof, dbg,
-                                       zf_per_wait, wide_ok && kPack == 2 ? 1 : 0);
+                                       zf_per_wait, wide_ok && kPack == 2 ? 1 : 0, p.split_cnt, p.split_scr, split_req);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (prof) {
-    static unsigned long long hp[1024 * 16];
+    static unsigned long long hp[1024 * 24];
     cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     double a[16] = {0};
@@ -669,6 +767,21 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
               a[6 * h + 4], a[6 * h + 5]);
     fprintf(stderr, "[dual prof] epilogue warp 4 tmem-full wait %.0f; issuer 0 full-wait in a tile's first 3 stages %.0f\n",
             a[12], a[13]);
+    {
+      const unsigned long long* t = hp + 1024 * 16;
+      unsigned long long g0 = ~0ull;
+      for (int c = 0; c < grid; ++c) g0 = std::min(g0, t[c * 8]);
+      double m[6] = {0}, mx[6] = {0};
+      for (int c = 0; c < grid; ++c)
+        for (int k = 0; k < 6; ++k) {
+          const double v = (static_cast<double>(t[c * 8 + k]) - static_cast<double>(g0)) * 1e-3;
+          m[k] += v / grid;
+          mx[k] = std::max(mx[k], v);
+        }
+      fprintf(stderr, "[dual tl] us from first CTA start (mean / max): start %.1f/%.1f prologue %.1f/%.1f issuer-done %.1f/%.1f "
+              "last-drain %.1f/%.1f zero-fill-done %.1f/%.1f cta-end %.1f/%.1f\n", m[0], mx[0], m[1], mx[1], m[2], mx[2],
+              m[3], mx[3], m[4], mx[4], m[5], mx[5]);
+    }
     if (getenv("SPAMM_DEBUG_UMMA_PROF_CTA")) {
       double by_n[8] = {0}, cnt_n[8] = {0};
       for (int c = 0; c < grid; ++c) {

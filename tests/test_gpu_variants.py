@@ -117,3 +117,25 @@ def test_dual_chain(sp, monkeypatch):
     np.testing.assert_array_equal(Cl.cpu().float().numpy(), synth.round_to_bf16(Cn))
     np.testing.assert_allclose(plan.output_norms().cpu().numpy(), oracle.tile_norms(Cl.cpu().float().numpy(), T),
                                rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("n_split", [1, 10, 1000])
+def test_dual_k_split(sp, monkeypatch, n_split):
+    """Variant 5 with the LPT tail's last tiles split into k-halves (C = P1 + P2, the second half's
+    epilogue adds onto the first's stores after a per-tile handshake); forced on a small grid."""
+    monkeypatch.setenv("SPAMM_UMMA_VARIANT", "5")
+    monkeypatch.setenv("SPAMM_DUAL_SPLIT", str(n_split))
+    M, N, K = 1000, 1024, 1536
+    prec = "bf16"
+    A = _rounded(synth.perturbed_decay_matrix(K, 0.995, seed=21, m=M), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.995, seed=22, m=K), prec)
+    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+    tau = _tau_at(nA, nB, 0.3)
+    plan = sp.Plan(M, N, K, tau, prec)
+    Ad, Bd = _dev(A, prec), _dev(B, prec)
+    ref = oracle.spamm(A, B, tau, T, nA, nB)
+    for _ in range(3):   # repeated launches: the handshake counters reset themselves
+        C = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+        plan.run(Ad, Bd, C)
+        torch.cuda.synchronize()
+        assert _rel_fro(C.cpu().numpy(), ref) <= 1e-5
