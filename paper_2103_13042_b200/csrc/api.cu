@@ -357,6 +357,8 @@ spamm_status do_norms_range(Plan& p, const void* A, int64_t lda, const void* B, 
   // A (M x K): tile row i, tile col k -> nA[i*BK + k];  B (K x N) column strip [bj0*T, bj1*T):
   // tile row k, tile col j -> nBt[j*BK + k]
   SPAMM_TRY(launch_norms2(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s));
+  p.ws_zeroed = p.zero_ws_next;
+  p.zero_ws_next = false;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[1], s));
   p.ev_norms = timing;
   p.norms_ready = true;
@@ -444,6 +446,7 @@ spamm_status spamm_multiply(spamm_plan_t h, const void* A, int64_t lda, const vo
   Plan& p = *reinterpret_cast<Plan*>(h);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (flags & SPAMM_MUL_AUTO) {
+    p.zero_ws_next = p.fixed_regions;   // the norm kernel zeroes the skip map's counters
     SPAMM_TRY(do_norms(p, A, lda, B, ldb, s));
     SPAMM_TRY(do_skipmap(p, 0, p.GM, s));
   }

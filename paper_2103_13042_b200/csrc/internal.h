@@ -63,6 +63,10 @@ struct Plan {
   int umma_variant = 5;          // tensor-path kernel: 0-2, 4 multiply_umma.cu, 5 multiply_dual.cu
   unsigned int* split_cnt = nullptr;   // dual multiply k-split handshake counters (self-resetting)
   float* split_scr = nullptr;          // dual multiply k-split partials
+  // workspace zeroing folded into the previous kernel of a spamm_run / AUTO call (saves a memset
+  // node per stage): the norm kernel zeroes row_work/hist/totals for the skip map, the skip map's
+  // last CTA zeroes the multiply's claim counters
+  bool zero_ws_next = false, ws_zeroed = false, sched_zeroed = false;
   bool dual = false;             // the two-issuer 256 x 256 path (variant 5, multiply_dual.cu): MI = 8, two 4 x 8 run entries per k-step
   int64_t* Uw = nullptr;         // [GM*GN] tensor-path entries per macro-tile (pairs merged) or = U
   // stream-K workspace of the tensor multiply (allocated on first use)

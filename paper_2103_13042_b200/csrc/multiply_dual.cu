@@ -723,7 +723,8 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   // plain epilogue the epilogue warps zero-fill those, otherwise they go through the pipeline
   // (beta * C_old, chained norms)
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
-  SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, 2 * sizeof(unsigned int), s));
+  if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, 2 * sizeof(unsigned int), s));
+  p.sched_zeroed = false;
   // SPAMM_DEBUG_DUAL_MODE: timing experiments that break the result (bit 1: no zero-fill of empty tiles,
   // bit 2: no C stores)
   const int dbg = getenv("SPAMM_DEBUG_DUAL_MODE") ? atoi(getenv("SPAMM_DEBUG_DUAL_MODE")) : 0;

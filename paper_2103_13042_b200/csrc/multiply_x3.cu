@@ -114,10 +114,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       return ti;
     };
-    TileQ nxt = claim();
+    // the next tile is claimed once the current one's loads are issued (LPT tail by finish time;
+    // claiming at tile start measured 163.5 vs 143.6 us on the 256 x 256 kernel, multiply_dual.cu)
+    TileQ cur = claim();
     for (;;) {
-      const TileQ cur = nxt;
-      if (cur.t >= 0) nxt = claim();
       if (lane == 0) {   // publish the tile (or the end marker) to the epilogue
         mbar_wait(&tq_empty[tq_s], tq_ph ^ 1);
         tq[tq_s] = cur;
@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph ^= 1;
         }
         if (cur.t < 0) break;
+        cur = claim();
         continue;
       }
       const int32_t I = static_cast<int32_t>(cur.t / GN), J = static_cast<int32_t>(cur.t % GN);
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // (s, ph) are only meaningful in lane 0, which issues every stage operation
       __syncwarp();
+      cur = claim();
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer

@@ -112,7 +112,7 @@ __device__ __forceinline__ void write_planes<float>(const NormJob& j, const uint
 template <typename T, int kStages>
 __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_constant__ CUtensorMap tmA,
                                                               const __grid_constant__ CUtensorMap tmB, NormJob ja,
-                                                              NormJob jb) {
+                                                              NormJob jb, int64_t* __restrict__ zws, int zn) {
   constexpr int V = 16 / sizeof(T);              // elements per 16-byte lane load
   constexpr int kCols = kBoxBytesRow / sizeof(T);  // columns per box
   constexpr int LPT = 32 / V;                    // lanes per 32-column tile
@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
   __shared__ uint64_t full[kStages];
   __shared__ double part[kWarps][kBoxesPerCta * TPB];
 
+  if (zws != nullptr && blockIdx.x == 0 && blockIdx.y == 0)   // the skip map's counters (spamm_run)
+    for (int i = threadIdx.x; i < zn; i += blockDim.x) zws[i] = 0;
   const bool isA = blockIdx.y < ja.nrow;
   const NormJob& j = isA ? ja : jb;
   const CUtensorMap* tm = isA ? &tmA : &tmB;
@@ -244,17 +246,19 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
                                         static_cast<int>(smem_bytes<4>())));
     attr = true;
   }
+  int64_t* zws = p.zero_ws_next ? p.row_work : nullptr;
+  const int zn = static_cast<int>(p.BM + p.BK + 4);
   const int64_t gx = std::max(ja.ncb, jb.ncb);
   const int64_t gy = ja.nrow + jb.nrow;
   if (gx <= 0 || gy <= 0) return SPAMM_OK;
   if (gy > 65535) return fail(SPAMM_E_UNSUPPORTED, "more than 65535 tile rows in one norm launch");
   dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
   if (stages == 2)
-    tile_norms_kernel<T, 2><<<grid, kThreads, smem_bytes<2>(), s>>>(tA, tB, ja, jb);
+    tile_norms_kernel<T, 2><<<grid, kThreads, smem_bytes<2>(), s>>>(tA, tB, ja, jb, zws, zn);
   else if (stages == 3)
-    tile_norms_kernel<T, 3><<<grid, kThreads, smem_bytes<3>(), s>>>(tA, tB, ja, jb);
+    tile_norms_kernel<T, 3><<<grid, kThreads, smem_bytes<3>(), s>>>(tA, tB, ja, jb, zws, zn);
   else
-    tile_norms_kernel<T, 4><<<grid, kThreads, smem_bytes<4>(), s>>>(tA, tB, ja, jb);
+    tile_norms_kernel<T, 4><<<grid, kThreads, smem_bytes<4>(), s>>>(tA, tB, ja, jb, zws, zn);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;

@@ -359,6 +359,7 @@ struct LastArgs {
   int64_t* totals;       // [0] kept pairs, [1] macro entries
   unsigned int* ticket;
   unsigned long long* tstamp;   // debug (SPAMM_DEBUG_SKIP_PROF): [0] first CTA start, [1] last CTA enter, [2] exit
+  unsigned int* sched;          // the multiply's claim counters [4], zeroed by the last CTA
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long g;
@@ -616,6 +617,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 4)
   if (la.tstamp && threadIdx.x == 0) la.tstamp[1] = gtimer();
   last_cta_order(la, s_warp, s_pos);
   if (threadIdx.x == 0) *la.ticket = 0u;
+  if (threadIdx.x < 4 && la.sched) la.sched[threadIdx.x] = 0u;
   if (la.tstamp) {
     __syncthreads();
     if (threadIdx.x == 0) la.tstamp[2] = gtimer();
@@ -692,7 +694,7 @@ spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
     const unsigned long long init[12] = {~0ull, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(tst, init, sizeof(init), cudaMemcpyHostToDevice, s);
   }
-  LastArgs la{p.hist, p.bucket_pos, p.BK + 1, p.U, p.L, p.order, gi0 * p.GN, gi1 * p.GN, p.totals, p.ticket, tst};
+  LastArgs la{p.hist, p.bucket_pos, p.BK + 1, p.U, p.L, p.order, gi0 * p.GN, gi1 * p.GN, p.totals, p.ticket, tst, p.sched};
   constexpr int dyn = 2 * (MI + MJ) * kKB * static_cast<int>(sizeof(double));
   static bool attr = false;
   if (!attr) {
@@ -792,7 +794,9 @@ spamm_status launch_skipmap_fused(Plan& p, int64_t gi0, int64_t gi1, cudaStream_
     SPAMM_CUDA_TRY(cudaMemsetAsync(p.L, 0, sizeof(int64_t) * (nmac + 1), s));
   }
   // row_work [BM], hist [BK+2] and totals [2] are contiguous in one allocation (see api.cu)
-  SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 4), s));
+  if (!p.ws_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 4), s));
+  p.ws_zeroed = false;
+  p.sched_zeroed = true;   // the last CTA zeroes the multiply's claim counters
   if (p.MI == kMacroI_dual) return fused_t<kMacroI_dual, kMacroJ_umma>(p, gi0, gi1, s);
   if (p.MJ == kMacroJ_umma) return fused_t<kMacroI, kMacroJ_umma>(p, gi0, gi1, s);
   return fused_t<kMacroI, kMacroJ_simt>(p, gi0, gi1, s);
