@@ -264,22 +264,27 @@ __device__ __forceinline__ uint4 encode_runs(uint32_t k, uint32_t mask, uint32_t
   const uint32_t d = (mask ^ (mask >> 1)) & 0x7F7F7F7Fu;
   const uint32_t bnd = (d | (d >> 8) | (d >> 16) | (d >> 24)) & 0x7Fu;
   const uint32_t nz = (mask | (mask >> 8) | (mask >> 16) | (mask >> 24)) & 0xFFu;
-  uint32_t words[3] = {0u, 0u, 0u};
-  uint32_t nr = 0, cols = 0;
+  // runs 0-2 -> w0, 3-5 -> w1, 6-7 -> w2, 10 bits each (explicit registers: a dynamically indexed
+  // array would live in local memory)
+  uint32_t w0 = 0u, w1 = 0u, w2 = 0u;
+  uint32_t nr = 0, cols = 0, sh = 0;
   uint32_t j = 0;
   while (j < 8) {
     const uint32_t b = bnd >> j;
     const uint32_t j1 = b ? j + static_cast<uint32_t>(__ffs(b)) : 8u;
     if ((nz >> j) & 1u) {
       const uint32_t pat = col_pattern8(mask, static_cast<int>(j));
-      const uint32_t run = j | ((j1 - j - 1) << 3) | (pat << 6);
-      words[nr / 3] |= run << (10 * (nr % 3));
+      const uint32_t run = (j | ((j1 - j - 1) << 3) | (pat << 6)) << sh;
+      if (nr < 3) w0 |= run;
+      else if (nr < 6) w1 |= run;
+      else w2 |= run;
       ++nr;
+      sh = sh == 20u ? 0u : sh + 10u;
       cols |= ((1u << (j1 - j)) - 1u) << j;
     }
     j = j1;
   }
-  return make_uint4(k | (nr << 16) | (cols << 24), words[0], words[1], words[2] | (wide << 31));
+  return make_uint4(k | (nr << 16) | (cols << 24), w0, w1, w2 | (wide << 31));
 }
 
 template <int MI, int MJ>
@@ -427,7 +432,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <int MI, int MJ>
-__global__ void __launch_bounds__(kFusedWarps * 32, 4)
+__global__ void __launch_bounds__(kFusedWarps * 32, (MI + MJ > 12) ? 3 : 4)
     skip_fused_kernel(const double* __restrict__ nA, const double* __restrict__ nBt, int64_t BM, int64_t BK,
                       int64_t BN, double tau, int64_t GN, int64_t gi0, int64_t n_macro, int64_t* __restrict__ U,
                       int64_t* __restrict__ Lm, unsigned long long* __restrict__ row_work,
@@ -687,7 +692,9 @@ __global__ void __launch_bounds__(kWarps * 32)
 template <int MI, int MJ>
 spamm_status fused_t(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
   const int64_t n_macro = (gi1 - gi0) * p.GN;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(n_macro, static_cast<int64_t>(p.num_sms) * 4));
+  // resident CTAs per SM: the staging buffer is 2 x (MI + MJ) x 256 doubles (48 KB for 4 x 8, 64 KB for 8 x 8)
+  constexpr int kPerSm = (MI + MJ > 12) ? 3 : 4;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(n_macro, static_cast<int64_t>(p.num_sms) * kPerSm));
   static unsigned long long* tst = nullptr;
   if (getenv("SPAMM_DEBUG_SKIP_PROF") && !tst) cudaMalloc(&tst, 128);
   if (tst) {
