@@ -14,7 +14,7 @@
 //   warp 0 (lane 0): tile claims (atomic counter over the LPT order) and the A boxes
 //            [128 x 32] of the halves that have runs (K-major SWIZZLE_64B, rows 128h..);
 //   warp 3 (lane 0): the contiguous range of needed B[32 x 32] boxes (3-D stacked map);
-//   warps 1, 2 (lane 0): MMA issuer of half h = warp - 1 (C-tile rows 4h .. 4h+3): per run of
+//   warps 1, 2 (one elected lane): MMA issuer of half h = warp - 1 (C-tile rows 4h .. 4h+3): per run of
 //            adjacent C-tile columns with the same row pattern, 2 x tcgen05.mma M=128 N=32*run
 //            K=16 whose disable-output-lane mask switches off the skipped C-tile rows -- the
 //            4 x 8 run encoding of multiply_umma.cu, one per half.  Two independent issuers
@@ -68,6 +68,15 @@ struct DTile {
   int64_t part;        // 0 whole tile; 1 / 2 first / second half of a k-split tile (C = P1 + P2)
   int64_t slot;        // k-split tiles: index into the handshake counters and the partial scratch
 };
+
+// warp-uniform copy of lane 0's value (lets the compiler keep MMA operands in uniform registers)
+__device__ __forceinline__ uint4 bcast4(uint4 v) {
+  v.x = __shfl_sync(0xffffffffu, v.x, 0);
+  v.y = __shfl_sync(0xffffffffu, v.y, 0);
+  v.z = __shfl_sync(0xffffffffu, v.z, 0);
+  v.w = __shfl_sync(0xffffffffu, v.w, 0);
+  return v;
+}
 
 struct DMaps {
   CUtensorMap a1;      // A [128 x 32] boxes, SW64
@@ -394,7 +403,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
   } else if (warp == 1 || warp == 2) {
     // ------------------------------------------------------------ MMA issuer of half h
     const int h = warp - 1;
-    if (lane == 0) {
+    // The whole warp runs the loop on broadcast (warp-uniform) values and one elected lane issues
+    // each tcgen05 op: with uniform operands the compiler moves them to uniform registers with a
+    // plain R2UR, where a lane-0-only loop gets an ELECT/R2UR.BROADCAST/BRA.U.ANY waterfall per MMA.
+    {
       constexpr uint32_t idesc_base = idesc_f16(kFmt, 128, 0, 0, 1);
       constexpr uint32_t idesc_full = idesc_base | (8u << 19);   // N = 256
       const uint32_t base_addr = smem_u32(smem);
@@ -423,6 +435,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
           asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                        : "=r"(rs.x), "=r"(rs.y), "=r"(rs.z), "=r"(rs.w)
                        : "r"(srun_addr + st * (32 * kPack)));
+          rs = bcast4(rs);
           const uint32_t fl = rs.w;
           if (fl & kEnd) {
             fin = true;
@@ -433,15 +446,17 @@ __global__ void __launch_bounds__(kDThreads, 1)
             mbar_wait(&tempty[h], tile_par);   // phase 0 = the epilogue's initial arrival
             if (prof) c_te += clock64() - tb;
             tc_fence_after();
-            umma_f16(dcol, zdesc, zdesc, idesc_full, 0u, 0u, 0u, 0u, 0u);   // D = 0
+            if (elect_one()) umma_f16(dcol, zdesc, zdesc, idesc_full, 0u, 0u, 0u, 0u, 0u);   // D = 0
           }
           const unsigned long long tc = prof ? clock64() : 0;
 #pragma unroll
           for (int j = 0; j < kPack; ++j) {
-            if (j > 0)
+            if (j > 0) {
               asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                            : "=r"(rs.x), "=r"(rs.y), "=r"(rs.z), "=r"(rs.w)
                            : "r"(srun_addr + st * (32 * kPack) + 32 * j));
+              rs = bcast4(rs);
+            }
             const uint32_t nr = (rs.x >> 16) & 15u;
             if ((fl & kNoStep) || nr == 0u) continue;
             // 32-deep slots: A K-major SW64 rows of 32 (SBO 512), +32 B per K=16, half h at +8 KB;
@@ -456,8 +471,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
                                     : smem_desc(st_addr + j * kDStepBytes + kDASlot, 2048, 512, kLayoutSW64);
             const uint32_t bbox = wst ? 256u : 128u;   // descriptor units (16 B) per column box
             if (nr == 1u && rs.y == kFullRun) {
-              umma_f16(dcol, ad, bd, idesc_full, 1u, 0u, 0u, 0u, 0u);
-              umma_f16(dcol, ad + 2, bd + 64, idesc_full, 1u, 0u, 0u, 0u, 0u);
+              if (elect_one()) {
+                umma_f16(dcol, ad, bd, idesc_full, 1u, 0u, 0u, 0u, 0u);
+                umma_f16(dcol, ad + 2, bd + 64, idesc_full, 1u, 0u, 0u, 0u, 0u);
+              }
             } else {
               uint32_t cw = rs.y;
               for (uint32_t rr = 0; rr < nr; ++rr) {
@@ -471,15 +488,17 @@ __global__ void __launch_bounds__(kDThreads, 1)
                 const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
                 const uint64_t bj = bd + static_cast<uint64_t>(j0 * bbox);
                 const uint32_t d = dcol + j0 * 32u;
-                umma_f16(d, ad, bj, idesc, 1u, m0, m1, m2, m3);
-                umma_f16(d, ad + 2, bj + 64, idesc, 1u, m0, m1, m2, m3);
+                if (elect_one()) {
+                  umma_f16(d, ad, bj, idesc, 1u, m0, m1, m2, m3);
+                  umma_f16(d, ad + 2, bj + 64, idesc, 1u, m0, m1, m2, m3);
+                }
               }
             }
           }
           const unsigned long long td = prof ? clock64() : 0;
-          umma_commit(&empty[st]);
+          if (elect_one()) umma_commit(&empty[st]);
           if (fl & kLast) {
-            umma_commit(&tfull[h]);
+            if (elect_one()) umma_commit(&tfull[h]);
             tile_par ^= 1;
             st_in_tile = 0;
             ++n_tiles_done;
@@ -493,7 +512,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
         }
         ph ^= 1;
       }
-      if (prof) {
+      if (prof && lane == 0) {
         unsigned long long* pr = prof + blockIdx.x * 16 + h * 6;
         pr[0] = clock64() - c_start;
         if (h == 0) stamp(2);

@@ -249,14 +249,15 @@ def test_errors_and_state(sp):
     assert e.value.status == sp.SPAMM_E_UNSUPPORTED
 
 
-def test_mgpu_single_rank_equals_single_gpu(sp):
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_mgpu_single_rank_equals_single_gpu(sp, prec):
     N = 640
-    A = synth.perturbed_decay_matrix(N, 0.95, seed=31)
-    B = synth.perturbed_decay_matrix(N, 0.95, seed=32)
+    A = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=31), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=32), prec)
     tau = 0.05
-    _, C1 = _run(sp, A, B, tau, "fp32")
-    plan = sp.Plan(N, N, N, tau, "fp32")
-    Ad, Bd = _dev(A, "fp32"), _dev(B, "fp32")
+    _, C1 = _run(sp, A, B, tau, prec)
+    plan = sp.Plan(N, N, N, tau, prec)
+    Ad, Bd = _dev(A, prec), _dev(B, prec)
     C = torch.zeros((N, N), device="cuda")
     sp.spamm_multiply_mgpu(plan.handle, None, 0, 1, Ad, Bd, C, 0)
     torch.cuda.synchronize()
