@@ -168,7 +168,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // the whole warp runs the loop on warp-uniform values; one elected lane issues each tcgen05
+    // op (uniform operands go to uniform registers without a per-MMA R2UR waterfall)
+    {
       const uint32_t base_addr = smem_u32(smem);
       const uint64_t zdesc = smem_desc(smem_u32(sZero), 0, 0, kLayoutSW64);
       const uint32_t idesc_zero = idesc_f16(1, 128, 128, 0, 1);
@@ -182,7 +184,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int st = 0; st < kStages; ++st) {
           mbar_wait(&full[st], ph);
           tc_fence_after();
-          const uint4 rs = srun[st];
+          uint4 rs = srun[st];
+          rs.x = __shfl_sync(0xffffffffu, rs.x, 0);
+          rs.y = __shfl_sync(0xffffffffu, rs.y, 0);
+          rs.w = __shfl_sync(0xffffffffu, rs.w, 0);
           const uint32_t fl = rs.w;
           if (fl & kEnd) {
             fin = true;
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if ((kin % kChunk) == 0) {   // chunk start: a drained buffer, zeroed
             mbar_wait(&tempty[buf], ub[buf] & 1u);
             tc_fence_after();
-            umma_f16(dcol, zdesc, zdesc, idesc_zero, 0u, 0u, 0u, 0u, 0u);
+            if (elect_one()) umma_f16(dcol, zdesc, zdesc, idesc_zero, 0u, 0u, 0u, 0u, 0u);
           }
           if (!(fl & kNoStep)) {
             const uint32_t a_addr = base_addr + st * kStageBytes, b_addr = a_addr + kStageA;
@@ -217,21 +222,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
                 const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
                 const uint32_t d = dcol + j * 32u;
+                if (elect_one()) {
 #pragma unroll
-                for (int p = 0; p < 6; ++p) {
-                  const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
-                  const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
-                  umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
-                  umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
+                  for (int p = 0; p < 6; ++p) {
+                    const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
+                    const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
+                    umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
+                    umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
+                  }
                 }
               }
               j = j1;
             }
           }
-          umma_commit(&empty[st]);
+          if (elect_one()) umma_commit(&empty[st]);
           ++kin;
           if ((fl & kLast) || (kin % kChunk) == 0) {   // chunk complete: hand the buffer over
-            umma_commit(&tfull[buf]);
+            if (elect_one()) umma_commit(&tfull[buf]);
             ++ub[buf];
             buf ^= 1;
           }

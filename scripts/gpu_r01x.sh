@@ -1,0 +1,6 @@
+#!/bin/bash
+OUT=gpurun_out
+mkdir -p $OUT
+python -m paper_2103_13042_b200.build > /dev/null
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "fp32x3" 2>&1 | tail -1
+timeout 300 python bench.py --precision fp32x3 --no-sweep --no-cpu-baseline --no-e2e --steps 50 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['stages_ms'], d['roofline']['frac'])"
