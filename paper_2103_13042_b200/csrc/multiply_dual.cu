@@ -253,25 +253,25 @@ __global__ void __launch_bounds__(kDThreads, 1)
           sent[2 * lane + 1] = ment[2 * (eb + lane) + 1];
         }
         __syncwarp();
-        if (lane == 0) {
+        {   // whole warp, warp-uniform values (see the issuers); one elected lane issues
+          auto X = [&](int e) -> uint32_t { return __shfl_sync(0xffffffffu, sent[e].x, 0); };
           for (int q = 0; q < cnt; q += kPack) {
             // (batches hold 32 k-steps, a multiple of kPack: a stage never spans two batches,
             // and only a tile's last stage can be partly empty)
             const int np = cnt - q < kPack ? cnt - q : kPack;
             // two consecutive k-tiles: one 64-deep box per A half and per B column range
             const bool wide = wide_ok && kPack == 2 && np == 2 &&
-                              (sent[2 * q + 2].x & 0xFFFFu) == (sent[2 * q].x & 0xFFFFu) + 1u;
+                              (X(2 * q + 2) & 0xFFFFu) == (X(2 * q) & 0xFFFFu) + 1u;
             uint32_t tx = 0;
             if (wide) {
-              const uint32_t x00 = sent[2 * q].x, x01 = sent[2 * q + 1].x, x10 = sent[2 * q + 2].x,
-                             x11 = sent[2 * q + 3].x;
+              const uint32_t x00 = X(2 * q), x01 = X(2 * q + 1), x10 = X(2 * q + 2), x11 = X(2 * q + 3);
               const uint32_t cols = (x00 | x01 | x10 | x11) >> 24;
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
               const bool h0 = ((x00 | x10) >> 16) & 15u, h1 = ((x01 | x11) >> 16) & 15u;
               tx = 16384u * ((h0 ? 1u : 0u) + (h1 ? 1u : 0u)) + 4096u * len;
             } else {
               for (int j = 0; j < np; ++j) {
-                const uint32_t x0 = sent[2 * (q + j)].x, x1 = sent[2 * (q + j) + 1].x;
+                const uint32_t x0 = X(2 * (q + j)), x1 = X(2 * (q + j) + 1);
                 const uint32_t cols = (x0 >> 24) | (x1 >> 24);
                 const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
                 tx += 8192u * ((((x0 >> 16) & 15u) != 0u ? 1u : 0u) + (((x1 >> 16) & 15u) != 0u ? 1u : 0u)) + 2048u * len;
@@ -280,7 +280,8 @@ __global__ void __launch_bounds__(kDThreads, 1)
             const uint32_t fl = (eb + q == cur.e0 ? kFirst : 0u) | (eb + q + np == cur.e1 ? kLast : 0u) |
                                 (wide ? kWideSt : 0u);
             mbar_wait(&empty[s], ph ^ 1);
-            for (int j = 0; j < kPack; ++j) {
+            const bool leader = elect_one();
+            for (int j = 0; j < kPack && leader; ++j) {
               uint4 e0 = make_uint4(0, 0, 0, 0), e1 = make_uint4(0, 0, 0, 0);
               if (j < np) {
                 e0 = sent[2 * (q + j)];
@@ -293,21 +294,24 @@ __global__ void __launch_bounds__(kDThreads, 1)
               srun[2 * (kPack * s + j)] = e0;
               srun[2 * (kPack * s + j) + 1] = e1;
             }
-            mbar_arrive_expect_tx(&full[s], tx);
+            if (elect_one()) mbar_arrive_expect_tx(&full[s], tx);
             if (wide) {
-              const uint32_t x00 = sent[2 * q].x, x01 = sent[2 * q + 1].x, x10 = sent[2 * q + 2].x,
-                             x11 = sent[2 * q + 3].x;
+              const uint32_t x00 = X(2 * q), x01 = X(2 * q + 1), x10 = X(2 * q + 2), x11 = X(2 * q + 3);
               const int32_t k0 = static_cast<int32_t>(x00 & 0xFFFFu) * 32;
               uint8_t* adst = smem + s * kDStageBytes;
-              if (((x00 | x10) >> 16) & 15u) tma_load_2d(adst, &mp.a2, &full[s], k0, I * 256);
-              if (((x01 | x11) >> 16) & 15u) tma_load_2d(adst + 16384, &mp.a2, &full[s], k0, I * 256 + 128);
+              if (elect_one()) {
+                if (((x00 | x10) >> 16) & 15u) tma_load_2d(adst, &mp.a2, &full[s], k0, I * 256);
+                if (((x01 | x11) >> 16) & 15u) tma_load_2d(adst + 16384, &mp.a2, &full[s], k0, I * 256 + 128);
+              }
             } else {
               for (int j = 0; j < np; ++j) {
-                const uint32_t x0 = sent[2 * (q + j)].x, x1 = sent[2 * (q + j) + 1].x;
+                const uint32_t x0 = X(2 * (q + j)), x1 = X(2 * (q + j) + 1);
                 const int32_t k0 = static_cast<int32_t>(x0 & 0xFFFFu) * 32;
                 uint8_t* adst = smem + s * kDStageBytes + j * kDStepBytes;
-                if ((x0 >> 16) & 15u) tma_load_2d(adst, &mp.a1, &full[s], k0, I * 256);
-                if ((x1 >> 16) & 15u) tma_load_2d(adst + 8192, &mp.a1, &full[s], k0, I * 256 + 128);
+                if (elect_one()) {
+                  if ((x0 >> 16) & 15u) tma_load_2d(adst, &mp.a1, &full[s], k0, I * 256);
+                  if ((x1 >> 16) & 15u) tma_load_2d(adst + 8192, &mp.a1, &full[s], k0, I * 256 + 128);
+                }
               }
             }
             if (++s == kDStages) {
@@ -356,39 +360,43 @@ __global__ void __launch_bounds__(kDThreads, 1)
           sentB[2 * lane + 1] = ment[2 * (eb + lane) + 1];
         }
         __syncwarp();
-        if (lane == 0) {
+        {   // whole warp, warp-uniform values; one elected lane issues
+          auto X = [&](int e) -> uint32_t { return __shfl_sync(0xffffffffu, sentB[e].x, 0); };
           for (int q = 0; q < cnt; q += kPack) {
             const int np = cnt - q < kPack ? cnt - q : kPack;
-            const bool wide = wide_ok && kPack == 2 && np == 2 &&
-                              (sentB[2 * q + 2].x & 0xFFFFu) == (sentB[2 * q].x & 0xFFFFu) + 1u;
+            const bool wide = wide_ok && kPack == 2 && np == 2 && (X(2 * q + 2) & 0xFFFFu) == (X(2 * q) & 0xFFFFu) + 1u;
             mbar_wait(&empty[s], ph ^ 1);
             if (wide) {
-              const uint32_t cols = (sentB[2 * q].x | sentB[2 * q + 1].x | sentB[2 * q + 2].x | sentB[2 * q + 3].x) >> 24;
-              const int32_t k0 = static_cast<int32_t>(sentB[2 * q].x & 0xFFFFu) * 32;
+              const uint32_t cols = (X(2 * q) | X(2 * q + 1) | X(2 * q + 2) | X(2 * q + 3)) >> 24;
+              const int32_t k0 = static_cast<int32_t>(X(2 * q) & 0xFFFFu) * 32;
               uint8_t* bdst = smem + s * kDStageBytes + 2 * kDASlot;
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
-              if (len == 8) {
-                tma_load_3d(bdst, &mp.b2[0], &full[s], 0, k0, jb);
-              } else {
-                int off = c0;
-                if (len & 4) { tma_load_3d(bdst + off * 4096, &mp.b2[1], &full[s], 0, k0, jb + off); off += 4; }
-                if (len & 2) { tma_load_3d(bdst + off * 4096, &mp.b2[2], &full[s], 0, k0, jb + off); off += 2; }
-                if (len & 1) { tma_load_3d(bdst + off * 4096, &mp.b2[3], &full[s], 0, k0, jb + off); }
+              if (elect_one()) {
+                if (len == 8) {
+                  tma_load_3d(bdst, &mp.b2[0], &full[s], 0, k0, jb);
+                } else {
+                  int off = c0;
+                  if (len & 4) { tma_load_3d(bdst + off * 4096, &mp.b2[1], &full[s], 0, k0, jb + off); off += 4; }
+                  if (len & 2) { tma_load_3d(bdst + off * 4096, &mp.b2[2], &full[s], 0, k0, jb + off); off += 2; }
+                  if (len & 1) { tma_load_3d(bdst + off * 4096, &mp.b2[3], &full[s], 0, k0, jb + off); }
+                }
               }
             }
             for (int j = 0; j < (wide ? 0 : np); ++j) {
-              const uint32_t x0 = sentB[2 * (q + j)].x, x1 = sentB[2 * (q + j) + 1].x;
+              const uint32_t x0 = X(2 * (q + j)), x1 = X(2 * (q + j) + 1);
               const uint32_t cols = (x0 >> 24) | (x1 >> 24);
               const int32_t k0 = static_cast<int32_t>(x0 & 0xFFFFu) * 32;
               uint8_t* bdst = smem + s * kDStageBytes + j * kDStepBytes + kDASlot;
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
-              if (len == 8) {
-                tma_load_3d(bdst, &mp.b1[0], &full[s], 0, k0, jb);
-              } else {
-                int off = c0;
-                if (len & 4) { tma_load_3d(bdst + off * 2048, &mp.b1[1], &full[s], 0, k0, jb + off); off += 4; }
-                if (len & 2) { tma_load_3d(bdst + off * 2048, &mp.b1[2], &full[s], 0, k0, jb + off); off += 2; }
-                if (len & 1) { tma_load_3d(bdst + off * 2048, &mp.b1[3], &full[s], 0, k0, jb + off); }
+              if (elect_one()) {
+                if (len == 8) {
+                  tma_load_3d(bdst, &mp.b1[0], &full[s], 0, k0, jb);
+                } else {
+                  int off = c0;
+                  if (len & 4) { tma_load_3d(bdst + off * 2048, &mp.b1[1], &full[s], 0, k0, jb + off); off += 4; }
+                  if (len & 2) { tma_load_3d(bdst + off * 2048, &mp.b1[2], &full[s], 0, k0, jb + off); off += 2; }
+                  if (len & 1) { tma_load_3d(bdst + off * 2048, &mp.b1[3], &full[s], 0, k0, jb + off); }
+                }
               }
             }
             if (++s == kDStages) {
