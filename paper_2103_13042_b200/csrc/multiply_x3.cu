@@ -142,27 +142,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       const int32_t I = static_cast<int32_t>(cur.t / GN), J = static_cast<int32_t>(cur.t % GN);
-      if (lane == 0) {
-        for (int64_t e = cur.e0; e < cur.e1; ++e) {
-          const uint2 en = ment[e];
-          const uint32_t mask = en.y & 0xFFFFu;
+      // 32 entries per warp load; the whole warp walks them on shuffled (warp-uniform) values and
+      // one elected lane issues the stage's operations (no per-entry dependent global load, no
+      // R2UR waterfall around the TMA instructions)
+      for (int64_t eb = cur.e0; eb < cur.e1; eb += 32) {
+        const int cnt = static_cast<int>(cur.e1 - eb < 32 ? cur.e1 - eb : 32);
+        const uint2 en_l = lane < cnt ? ment[eb + lane] : make_uint2(0u, 0u);
+        for (int q = 0; q < cnt; ++q) {
+          const uint32_t ex = __shfl_sync(0xffffffffu, en_l.x, q), ey = __shfl_sync(0xffffffffu, en_l.y, q);
+          const int64_t e = eb + q;
+          const uint32_t mask = ey & 0xFFFFu;
           const uint32_t cols = (mask | (mask >> 4) | (mask >> 8) | (mask >> 12)) & 0xFu;   // needed C-tile columns
-          const int32_t k0 = static_cast<int32_t>(en.x) * 32;
+          const int32_t k0 = static_cast<int32_t>(ex) * 32;
           mbar_wait(&empty[s], ph ^ 1);
-          srun[s] = make_uint4(en.x, mask, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
           uint8_t* st = smem + s * kStageBytes;
-          mbar_arrive_expect_tx(&full[s], kStageA + kBCol * __popc(cols));
-          tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
+          if (elect_one()) {
+            srun[s] = make_uint4(ex, mask, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
+            mbar_arrive_expect_tx(&full[s], kStageA + kBCol * __popc(cols));
+            tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
 #pragma unroll
-          for (int lj = 0; lj < 4; ++lj)
-            if ((cols >> lj) & 1u) tma_load_3d(st + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
+            for (int lj = 0; lj < 4; ++lj)
+              if ((cols >> lj) & 1u) tma_load_3d(st + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
+          }
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
           }
         }
       }
-      // (s, ph) are only meaningful in lane 0, which issues every stage operation
       __syncwarp();
       cur = claim();
     }
