@@ -14,3 +14,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"til
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:spamm_mul_x3 -s 3 -c 1 -o $OUT/prof_x3_final -f python bench.py --precision fp32x3 --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > /dev/null 2>&1
 ls -la $OUT/*final*
 for r in prof_dual_final prof_ns_final prof_x3_final; do ncu -i $OUT/$r.ncu-rep --page source --csv > $OUT/${r}_source.csv 2>/dev/null; done
+timeout 1200 python scripts/suite.py --reps 5 --out $OUT/suite_final.json > $OUT/suite_final.log 2>&1; tail -2 $OUT/suite_final.log
