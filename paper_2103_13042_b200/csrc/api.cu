@@ -206,8 +206,8 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->BK = BK;
   p->BN = BN;
   // the 256 x 256 two-issuer tensor path needs fixed list regions and whole 32-column B boxes
-  const bool fixed_ok = !(flags & SPAMM_FLAG_SYNC_SKIPMAP) &&
-                        sizeof(uint16_t) * static_cast<size_t>(BM * BN) * static_cast<size_t>(BK) <= kWorstCaseBudget;
+  // (the macro lists are always reserved at their worst case; the per-C-tile lists only on request)
+  const bool fixed_ok = !(flags & SPAMM_FLAG_SYNC_SKIPMAP);
   p->umma_variant = umma_variant_from_env();
   p->dual = !f32_inputs(prec) && fixed_ok && N % 32 == 0 && p->umma_variant == 5;
   if (!f32_inputs(prec) && !p->dual && p->umma_variant == 5) p->umma_variant = 0;
@@ -264,13 +264,13 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
       st = alloc(reinterpret_cast<void**>(&p->macro_run),
                  sizeof(uint4) * static_cast<size_t>(p->macro_cap) * (p->dual ? 2 : 1));
   }
-  // leaf lists: reserve the worst case unless it exceeds the budget or SYNC_SKIPMAP is set
+  // fixed regions (single-pass skip map into worst-case macro-list regions) unless SYNC_SKIPMAP;
+  // the per-C-tile lists (2 B per C tile and k: 17 GB at N = 65536) are reserved when first asked
+  // for (spamm_get_skipmap / spamm_get_counts), and eagerly when that is under kWorstCaseBudget
   if (st == SPAMM_OK && !(flags & SPAMM_FLAG_SYNC_SKIPMAP)) {
+    p->fixed_regions = true;
     const size_t worst = sizeof(uint16_t) * static_cast<size_t>(nleaf) * static_cast<size_t>(BK);
-    if (worst <= kWorstCaseBudget) {
-      st = ensure_leaf_capacity(*p, nleaf * BK);
-      p->fixed_regions = st == SPAMM_OK;
-    }
+    if (worst <= kWorstCaseBudget) st = ensure_leaf_capacity(*p, nleaf * BK);
   }
   // macro-tile t's entries start at t*BK (fixed regions) or at the scanned offset macro_ptr[t]
   if (st == SPAMM_OK) {
@@ -528,6 +528,7 @@ spamm_status spamm_get_norms(spamm_plan_t h, const double** dA, const double** d
 // expanded from them on first request (same stream, then synchronised).
 static spamm_status ensure_leaf_lists(spamm::Plan& p) {
   if (p.leaf_ready) return SPAMM_OK;
+  if (p.fixed_regions) SPAMM_TRY(ensure_leaf_capacity(p, p.BM * p.BN * p.BK));
   SPAMM_TRY(launch_leaf_expand(p, p.last_stream));
   SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
   p.leaf_ready = true;
