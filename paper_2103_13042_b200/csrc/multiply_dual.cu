@@ -47,7 +47,8 @@ constexpr int kDBSlot = 32 * 256 * 2;                 // B[32 x 256] as eight [3
 constexpr int kDStepBytes = kDASlot + kDBSlot;        // one 32-deep k-step
 constexpr int kDThreads = 384;   // w0 A/claims, w1-2 MMA, w3 B, w4-11 epilogue
 constexpr int kDTQ = 4;                               // tile ring depth
-constexpr int64_t kMaxSplit = 148;                    // k-split tiles per launch (scratch: 256 KB each)
+constexpr int64_t kMaxSplit = 148;
+constexpr int64_t kOrdS = 12;                         // blocked claim order: super-block side (tiles)                    // k-split tiles per launch (scratch: 256 KB each)
 // kPack k-steps of one macro-tile per ring stage (one wait / commit per stage for the issuers);
 // the ring holds 6 k-steps either way (192 KB)
 template <int kPack>
@@ -99,9 +100,13 @@ __global__ void __launch_bounds__(kDThreads, 1)
                           const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
                           const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait, int wide_ok,
-                          unsigned int* __restrict__ split_cnt, float* __restrict__ split_scr, int64_t split_req) {
+                          unsigned int* __restrict__ split_cnt, float* __restrict__ split_scr, int64_t split_req,
+                          int order_mode, int64_t t0) {
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
+  // claim order: LPT (descending k-steps), or blocked when every CTA gets many tiles (order_mode:
+  // 0 = blocked if n_work >= 16 x grid, 1 = LPT, 2 = blocked)
+  const bool row_order = order_mode == 2 || (order_mode == 0 && n_work >= 16 * static_cast<int64_t>(gridDim.x));
   // k-split tail (plain epilogue only): split_req < 0 = the last (n_work mod grid) tiles
   int64_t n_split = 0;
   if (!kGen && split_cnt != nullptr) {
@@ -200,6 +205,27 @@ __global__ void __launch_bounds__(kDThreads, 1)
       if (lane == 0) idx = atomicAdd(sched, 1u);
       idx = __shfl_sync(0xffffffffu, idx, 0);
       const int64_t n_whole = n_work - n_split;
+      if (row_order) {
+        // many tiles per CTA: balance comes for free, so claim in a blocked tile order (kOrdS x kOrdS
+        // super-blocks row-major, tiles row-major inside; empty tiles skipped): the ~grid tiles in
+        // flight then share A row blocks and B column blocks in L2
+        const int64_t GMr = n_tiles / GN, nsbc = (GN + kOrdS - 1) / kOrdS;
+        for (;;) {
+          if (static_cast<int64_t>(idx) >= ((GMr + kOrdS - 1) / kOrdS) * nsbc * kOrdS * kOrdS) return d;
+          const int64_t sb = idx / (kOrdS * kOrdS), w = idx % (kOrdS * kOrdS);
+          const int64_t li = (sb / nsbc) * kOrdS + w / kOrdS, lj = (sb % nsbc) * kOrdS + w % kOrdS;
+          const int64_t t = t0 + li * GN + lj;
+          const int64_t c = (li < GMr && lj < GN) ? mcount[t] : 0;
+          if (c > 0) {
+            d.t = t;
+            d.e0 = mstart[t];
+            d.e1 = d.e0 + c;
+            return d;
+          }
+          if (lane == 0) idx = atomicAdd(sched, 1u);
+          idx = __shfl_sync(0xffffffffu, idx, 0);
+        }
+      }
       if (static_cast<int64_t>(idx) < n_whole) {
         d.t = order[idx];
         d.e0 = mstart[d.t];
@@ -755,6 +781,8 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   // SPAMM_DEBUG_DUAL_MODE: timing experiments that break the result (bit 1: no zero-fill of empty tiles,
   // bit 2: no C stores)
   const int dbg = getenv("SPAMM_DEBUG_DUAL_MODE") ? atoi(getenv("SPAMM_DEBUG_DUAL_MODE")) : 0;
+  // tile claim order (SPAMM_DUAL_ORDER: 0 auto, 1 LPT, 2 blocked)
+  const int order_mode = getenv("SPAMM_DUAL_ORDER") ? atoi(getenv("SPAMM_DUAL_ORDER")) : 0;
   // k-split of the LPT tail.s last tiles (SPAMM_DUAL_SPLIT=n tiles, -1 = n_work mod grid; default off)
   const int64_t split_req = getenv("SPAMM_DUAL_SPLIT") ? atoll(getenv("SPAMM_DUAL_SPLIT")) : 0;   // measured slower (r01p)
   if (!p.split_cnt) {   // [kMaxSplit][8 slices][arrived, done] counters + [kMaxSplit][8][32 x 256] partials
@@ -775,7 +803,8 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, kGen ? nullptr : p.hist, p.GN, C, ldc, p.M,
                                        p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                        DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl}, prof, dbg,
-                                       zf_per_wait, wide_ok && kPack == 2 ? 1 : 0, p.split_cnt, p.split_scr, split_req);
+                                       zf_per_wait, wide_ok && kPack == 2 ? 1 : 0, p.split_cnt, p.split_scr, split_req,
+                                       order_mode, p.row_begin_macro * p.GN);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (prof) {
