@@ -215,8 +215,11 @@ __global__ void __launch_bounds__(kDThreads, 1)
           const int64_t sb = idx / (kOrdS * kOrdS), w = idx % (kOrdS * kOrdS);
           const int64_t li = (sb / nsbc) * kOrdS + w / kOrdS, lj = (sb % nsbc) * kOrdS + w % kOrdS;
           const int64_t t = t0 + li * GN + lj;
-          const int64_t c = (li < GMr && lj < GN) ? mcount[t] : 0;
-          if (c > 0) {
+          const bool in = li < GMr && lj < GN;
+          const int64_t c = in ? mcount[t] : 0;
+          // tiles without k-steps are zero-filled at the end, or (no zero-fill: alpha/beta, chained
+          // outputs) go through the pipeline like any tile
+          if (c > 0 || (in && n_empty_p == nullptr)) {
             d.t = t;
             d.e0 = mstart[t];
             d.e1 = d.e0 + c;

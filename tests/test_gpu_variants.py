@@ -139,3 +139,26 @@ def test_dual_k_split(sp, monkeypatch, n_split):
         plan.run(Ad, Bd, C)
         torch.cuda.synchronize()
         assert _rel_fro(C.cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("alpha,beta", [(1.0, 0.0), (2.0, 1.5)])
+def test_dual_blocked_order(sp, monkeypatch, alpha, beta):
+    """Variant 5 with the blocked (12 x 12 super-block) claim order forced (SPAMM_DUAL_ORDER=2;
+    automatic when every CTA gets >= 16 tiles): empty tiles are zero-filled (beta = 0) or go
+    through the pipeline (beta != 0)."""
+    monkeypatch.setenv("SPAMM_UMMA_VARIANT", "5")
+    monkeypatch.setenv("SPAMM_DUAL_ORDER", "2")
+    M, N, K = 1000, 1024, 1536
+    prec = "bf16"
+    A = _rounded(synth.perturbed_decay_matrix(K, 0.99, seed=41, m=M), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.99, seed=42, m=K), prec)
+    C0 = synth.random_matrix(M, N, seed=43)
+    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+    tau = _tau_at(nA, nB, 0.8)
+    plan = sp.Plan(M, N, K, tau, prec)
+    plan.set_scalars(alpha, beta)
+    C = torch.from_numpy(C0).cuda() if beta != 0.0 else torch.full((M, N), float("nan"), device="cuda")
+    plan.run(_dev(A, prec), _dev(B, prec), C)
+    torch.cuda.synchronize()
+    ref = oracle.spamm_axpby(A, B, tau, T, alpha, beta, C0, nA, nB)
+    assert _rel_fro(C.cpu().numpy(), ref) <= 5e-6
