@@ -209,7 +209,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   // (the macro lists are always reserved at their worst case; the per-C-tile lists only on request)
   const bool fixed_ok = !(flags & SPAMM_FLAG_SYNC_SKIPMAP);
   p->umma_variant = umma_variant_from_env();
-  p->dual = !f32_inputs(prec) && fixed_ok && N % 32 == 0 && p->umma_variant == 5;
+  p->dual = !f32_inputs(prec) && fixed_ok && p->umma_variant == 5;
   if (!f32_inputs(prec) && !p->dual && p->umma_variant == 5) p->umma_variant = 0;
   p->MI = p->dual ? kMacroI_dual : kMacroI;
   p->MJ = f32_inputs(prec) ? kMacroJ_simt : kMacroJ_umma;

@@ -84,6 +84,7 @@ struct DMaps {
   CUtensorMap a2;      // A [128 x 64] boxes, SW128 (a stage of two consecutive k-steps)
   CUtensorMap b1[4];   // B stacked [32 k x 32 n] boxes, 8/4/2/1 boxes, SW64
   CUtensorMap b2[4];   // B stacked [64 k x 32 n] boxes (two consecutive k-steps), SW64
+  CUtensorMap b2d1, b2d2;   // N % 32 != 0: plain 2-D B boxes [32 | 64 k x 32 n], SW64
 };
 
 struct DChain {
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
                           const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait, int wide_ok,
                           unsigned int* __restrict__ split_cnt, float* __restrict__ split_scr, int64_t split_req,
-                          int order_mode, int64_t t0) {
+                          int order_mode, int64_t t0, int use3d) {
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
   // claim order: LPT (descending k-steps), or blocked when every CTA gets many tiles (order_mode:
@@ -356,10 +357,14 @@ __global__ void __launch_bounds__(kDThreads, 1)
   } else if (warp == 3) {
     // ---------------------------------------------------------------- producer B
     if (lane == 0)
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 4 && use3d; ++q) {
         tma_prefetch_desc(&mp.b1[q]);
         tma_prefetch_desc(&mp.b2[q]);
       }
+    if (lane == 0 && !use3d) {
+      tma_prefetch_desc(&mp.b2d1);
+      tma_prefetch_desc(&mp.b2d2);
+    }
     int s = 0;
     uint32_t ph = 0;
     int tq_s = 0;
@@ -401,7 +406,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
               uint8_t* bdst = smem + s * kDStageBytes + 2 * kDASlot;
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
               if (elect_one()) {
-                if (len == 8) {
+                if (!use3d) {   // N % 32 != 0: one 2-D box per column tile (zero fill past N)
+                  for (int c = c0; c < c0 + len; ++c)
+                    tma_load_2d(bdst + c * 4096, &mp.b2d2, &full[s], (jb + c) * 32, k0);
+                } else if (len == 8) {
                   tma_load_3d(bdst, &mp.b2[0], &full[s], 0, k0, jb);
                 } else {
                   int off = c0;
@@ -418,7 +426,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
               uint8_t* bdst = smem + s * kDStageBytes + j * kDStepBytes + kDASlot;
               const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
               if (elect_one()) {
-                if (len == 8) {
+                if (!use3d) {
+                  for (int c = c0; c < c0 + len; ++c)
+                    tma_load_2d(bdst + c * 2048, &mp.b2d1, &full[s], (jb + c) * 32, k0);
+                } else if (len == 8) {
                   tma_load_3d(bdst, &mp.b1[0], &full[s], 0, k0, jb);
                 } else {
                   int off = c0;
@@ -760,11 +771,16 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   SPAMM_TRY(encode_tmap_2d(&mp.a1, dt, 2, A, p.K, p.M, lda, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_tmap_2d(&mp.a2, dt, 2, A, p.K, p.M, lda, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B));
   const uint32_t nbs[4] = {8, 4, 2, 1};
-  for (int q = 0; q < 4; ++q) {
-    SPAMM_TRY(encode_tmap_3d(&mp.b1[q], dt, B, 32, p.K, p.N / 32, static_cast<uint64_t>(ldb) * 2, 64, 32, 32, nbs[q],
-                             CU_TENSOR_MAP_SWIZZLE_64B));
-    SPAMM_TRY(encode_tmap_3d(&mp.b2[q], dt, B, 32, p.K, p.N / 32, static_cast<uint64_t>(ldb) * 2, 64, 32, 64, nbs[q],
-                             CU_TENSOR_MAP_SWIZZLE_64B));
+  if (p.N % 32 == 0) {   // stacked 3-D maps need whole 32-column boxes
+    for (int q = 0; q < 4; ++q) {
+      SPAMM_TRY(encode_tmap_3d(&mp.b1[q], dt, B, 32, p.K, p.N / 32, static_cast<uint64_t>(ldb) * 2, 64, 32, 32, nbs[q],
+                               CU_TENSOR_MAP_SWIZZLE_64B));
+      SPAMM_TRY(encode_tmap_3d(&mp.b2[q], dt, B, 32, p.K, p.N / 32, static_cast<uint64_t>(ldb) * 2, 64, 32, 64, nbs[q],
+                               CU_TENSOR_MAP_SWIZZLE_64B));
+    }
+  } else {
+    SPAMM_TRY(encode_tmap_2d(&mp.b2d1, dt, 2, B, p.N, p.K, ldb, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
+    SPAMM_TRY(encode_tmap_2d(&mp.b2d2, dt, 2, B, p.N, p.K, ldb, 32, 64, CU_TENSOR_MAP_SWIZZLE_64B));
   }
   auto kern = spamm_mul_dual_kernel<kFmt, kGen, kPack>;
   constexpr size_t kDSmem = DCfg<kPack>::kSmem;
@@ -807,7 +823,7 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
                                        p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                        DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl}, prof, dbg,
                                        zf_per_wait, wide_ok && kPack == 2 ? 1 : 0, p.split_cnt, p.split_scr, split_req,
-                                       order_mode, p.row_begin_macro * p.GN);
+                                       order_mode, p.row_begin_macro * p.GN, p.N % 32 == 0 ? 1 : 0);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (prof) {

@@ -18,8 +18,8 @@ pytestmark = pytest.mark.gpu
 
 # "5:1" = variant 5 with one k-step per ring stage (SPAMM_DUAL_PACK=1; default 2)
 VARIANTS = os.environ.get("SPAMM_TEST_VARIANTS", "0,1,2,4,5,5:1").split(",")
-# N % 32 == 0 for the 3-D stacked B boxes of variant 5 (other N fall back to variant 0)
-SHAPES = [(256, 256, 256), (300, 512, 129), (1000, 768, 600), (64, 256, 4096), (513, 1024, 300), (40, 32, 32)]
+SHAPES = [(256, 256, 256), (300, 512, 129), (1000, 768, 600), (64, 256, 4096), (513, 1024, 300), (40, 32, 32),
+          (300, 257, 129), (129, 1000, 384)]   # the last two: N % 32 != 0 (2-D B boxes, clipped stores)
 
 
 def _tau_at(nA, nB, q):
