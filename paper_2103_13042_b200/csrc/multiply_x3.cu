@@ -20,6 +20,7 @@
 // runs of adjacent C-tile columns with equal row patterns and issues, per run, 6 products x 2
 // tcgen05.mma (M = 128, N = 32*run, K = 16) with the disable-output-lane mask of the skipped
 // C-tile rows -- exact leaf-level skipping, as on the BF16 path.
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -56,7 +57,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_x3_kernel(const __grid_constant__ X3Maps mp, const int64_t* __restrict__ mstart,
                         const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
                         const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
-                        int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab) {
+                        int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab,
+                        int blocked, int64_t t0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sZero = smem + kStages * kStageBytes;                  // 512-B zero atom (D = 0 MMA)
@@ -107,6 +109,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) idx = atomicAdd(sched, 1u);
       idx = __shfl_sync(0xffffffffu, idx, 0);
       TileQ ti{-1, 0, 0};
+      if (blocked) {
+        // many tiles per CTA: a blocked order (12 x 12 super-blocks row-major, tiles row-major
+        // inside) so the tiles in flight share operand strips in L2 (as multiply_dual.cu)
+        const int64_t GMr = n_tiles / GN, nsbc = (GN + 11) / 12;
+        for (;;) {
+          if (static_cast<int64_t>(idx) >= ((GMr + 11) / 12) * nsbc * 144) return ti;
+          const int64_t sb = idx / 144, w = idx % 144;
+          const int64_t li = (sb / nsbc) * 12 + w / 12, lj = (sb % nsbc) * 12 + w % 12;
+          if (li < GMr && lj < GN) {
+            ti.t = t0 + li * GN + lj;
+            ti.e0 = mstart[ti.t];
+            ti.e1 = ti.e0 + mcount[ti.t];
+            return ti;
+          }
+          if (lane == 0) idx = atomicAdd(sched, 1u);
+          idx = __shfl_sync(0xffffffffu, idx, 0);
+        }
+      }
       if (static_cast<int64_t>(idx) < n_tiles) {
         ti.t = order[idx];
         ti.e0 = mstart[ti.t];
@@ -350,9 +370,13 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
   if (n_tiles <= 0) return SPAMM_OK;
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
   SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
+  // claim order: LPT, or blocked with >= 16 tiles per CTA (SPAMM_X3_ORDER: 0 auto, 1 LPT, 2 blocked)
+  const int om = getenv("SPAMM_X3_ORDER") ? atoi(getenv("SPAMM_X3_ORDER")) : 0;
+  const int blocked = om == 2 || (om == 0 && n_tiles >= 16 * static_cast<int64_t>(grid)) ? 1 : 0;
   spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, p.macro_ent, p.order, n_tiles, p.GN, C,
                                                          ldc, p.M, p.N, p.sched,
-                                                         Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)});
+                                                         Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
+                                                         blocked, p.row_begin_macro * p.GN);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
