@@ -89,23 +89,29 @@ __device__ __forceinline__ mask_t<MI, MJ> chunk_mask(const ChunkVals<MI, MJ>& v,
   if (__dmul_rn(amin, bmin) >= tau) return valid;
   M_ mask = 0u;
 #pragma unroll
-  for (int li = 0; li < MI; ++li)
+  for (int li = 0; li < MI; ++li) {
+    uint32_t row = 0u;   // 32-bit row bits, merged into the (possibly 64-bit) mask once per row
 #pragma unroll
     for (int lj = 0; lj < MJ; ++lj) {
       const double prod = __dmul_rn(v.a[li], v.b[lj]);
-      mask |= static_cast<M_>(!(prod < tau)) << (li * MJ + lj);
+      row |= static_cast<uint32_t>(!(prod < tau)) << lj;
     }
+    mask |= static_cast<M_>(row) << (li * MJ);
+  }
   return mask & valid;
 }
 // bit li*MJ+lj set iff C tile (I*MI+li, J*MJ+lj) exists
 template <int MI, int MJ>
 __device__ __forceinline__ mask_t<MI, MJ> valid_bits(int64_t BM, int64_t BN, int64_t I, int64_t J) {
-  mask_t<MI, MJ> v = 0u;
+  using M_ = mask_t<MI, MJ>;
+  const int64_t rr = BM - I * MI, cc = BN - J * MJ;   // C-tile rows / columns left in the grid
+  const int rv = rr >= MI ? MI : (rr > 0 ? static_cast<int>(rr) : 0);
+  const int cv = cc >= MJ ? MJ : (cc > 0 ? static_cast<int>(cc) : 0);
+  const M_ row = (static_cast<M_>(1u) << cv) - 1u;    // MJ <= 8: one row's column bits
+  M_ v = 0u;
 #pragma unroll
   for (int li = 0; li < MI; ++li)
-#pragma unroll
-    for (int lj = 0; lj < MJ; ++lj)
-      if (I * MI + li < BM && J * MJ + lj < BN) v |= static_cast<mask_t<MI, MJ>>(1u) << (li * MJ + lj);
+    if (li < rv) v |= row << (li * MJ);
   return v;
 }
 // Exclusive scan of n int64 values by one CTA; out has n+1 entries, out[n] = total.
