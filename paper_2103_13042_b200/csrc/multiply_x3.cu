@@ -58,7 +58,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
                         const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
                         int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab,
-                        int blocked, int64_t t0) {
+                        int order_mode, int64_t t0, const int64_t* __restrict__ n_empty_p) {
+  // claim order: LPT, or blocked when every CTA gets >= 16 tiles with k-steps (order_mode: 0 auto,
+  // 1 LPT, 2 blocked); the LPT order ends with the n_empty tiles without kept pairs
+  const int64_t n_work = n_tiles - (n_empty_p ? *n_empty_p : 0);
+  const bool blocked = order_mode == 2 || (order_mode == 0 && n_work >= 16 * static_cast<int64_t>(gridDim.x));
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sZero = smem + kStages * kStageBytes;                  // 512-B zero atom (D = 0 MMA)
@@ -370,13 +374,12 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
   if (n_tiles <= 0) return SPAMM_OK;
   const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
   SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
-  // claim order: LPT, or blocked with >= 16 tiles per CTA (SPAMM_X3_ORDER: 0 auto, 1 LPT, 2 blocked)
+  // claim order (SPAMM_X3_ORDER: 0 auto, 1 LPT, 2 blocked)
   const int om = getenv("SPAMM_X3_ORDER") ? atoi(getenv("SPAMM_X3_ORDER")) : 0;
-  const int blocked = om == 2 || (om == 0 && n_tiles >= 16 * static_cast<int64_t>(grid)) ? 1 : 0;
   spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, p.macro_ent, p.order, n_tiles, p.GN, C,
                                                          ldc, p.M, p.N, p.sched,
                                                          Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                                         blocked, p.row_begin_macro * p.GN);
+                                                         om, p.row_begin_macro * p.GN, p.hist);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
