@@ -804,7 +804,7 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   const int order_mode = getenv("SPAMM_DUAL_ORDER") ? atoi(getenv("SPAMM_DUAL_ORDER")) : 0;
   // k-split of the LPT tail.s last tiles (SPAMM_DUAL_SPLIT=n tiles, -1 = n_work mod grid; default off)
   const int64_t split_req = getenv("SPAMM_DUAL_SPLIT") ? atoll(getenv("SPAMM_DUAL_SPLIT")) : 0;   // measured slower (r01p)
-  if (!p.split_cnt) {   // [kMaxSplit][8 slices][arrived, done] counters + [kMaxSplit][8][32 x 256] partials
+  if (split_req != 0 && !p.split_cnt) {   // [kMaxSplit][8 slices][arrived, done] counters + [kMaxSplit][8][32 x 256] partials
     if (cudaMalloc(&p.split_cnt, sizeof(unsigned int) * kMaxSplit * 16) != cudaSuccess ||
         cudaMalloc(&p.split_scr, sizeof(float) * kMaxSplit * 8 * 32 * 256) != cudaSuccess) {
       cudaGetLastError();
