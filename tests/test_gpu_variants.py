@@ -162,3 +162,19 @@ def test_dual_blocked_order(sp, monkeypatch, alpha, beta):
     torch.cuda.synchronize()
     ref = oracle.spamm_axpby(A, B, tau, T, alpha, beta, C0, nA, nB)
     assert _rel_fro(C.cpu().numpy(), ref) <= 5e-6
+
+
+def test_fp32x3_blocked_order(sp, monkeypatch):
+    """FP32X3 multiply with the blocked claim order forced (SPAMM_X3_ORDER=2; automatic with >= 16
+    tiles with k-steps per CTA): every tile, with or without k-steps, is claimed exactly once."""
+    monkeypatch.setenv("SPAMM_X3_ORDER", "2")
+    M, N, K = 1000, 1000, 1536
+    A = synth.perturbed_decay_matrix(K, 0.99, seed=51, m=M)
+    B = synth.perturbed_decay_matrix(N, 0.99, seed=52, m=K)
+    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+    tau = _tau_at(nA, nB, 0.8)
+    plan = sp.Plan(M, N, K, tau, "fp32x3")
+    C = torch.full((M, N), float("nan"), device="cuda")
+    plan.run(_dev(A, "fp32x3"), _dev(B, "fp32x3"), C)
+    torch.cuda.synchronize()
+    assert _rel_fro(C.cpu().numpy(), oracle.spamm(A, B, tau, T, nA, nB)) <= 1e-5
