@@ -25,7 +25,12 @@ the Sec. 3.5.2 tau search.
 
 Parity pins: every function here is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_pins.py`` (paper tables, closed forms, brute force); none is
-"parity unpinned".
+"parity unpinned".  ``spamm_tile`` (reference of every sampled full-size tile check):
+hand-enumerated N=4 tiles, tau=0 = the plain product's block on ragged edges, a tile with
+one kept k = that block product, and agreement with ``spamm``; ``band_count``: products
+placed by hand inside/outside the 1e-6 band; ``tile_error_bound``: hand values and
+equality with the true error for aligned rank-one tiles (where the bound is tight);
+``macro_lists``: a hand-enumerated 8 x 8 (64-bit mask) case with a ragged second group.
 """
 from __future__ import annotations
 

@@ -339,3 +339,167 @@ def test_axpby_is_the_problem_statement_by_brute_force():
             assert abs(got[i, j] - (alpha * s + beta * C0[i, j])) < 1e-12
     nanC = np.full((m, n), np.nan)
     assert np.all(np.isfinite(oracle.spamm_axpby(A, B, 0.0, 2, 2.0, 0.0, nanC)))
+
+
+# ------------------------------------------------- spamm_tile (sampled checks) ---
+def _hand_n4():
+    """The N=4, T=2 inputs of test_hand_enumerated_skip_set_n4_t2 (tiles c*E11)."""
+    nA = [[3.0, 1.0], [2.0, 0.5]]
+    nB = [[1.0, 4.0], [0.25, 2.0]]
+    A = np.zeros((4, 4))
+    B = np.zeros((4, 4))
+    for i in range(2):
+        for k in range(2):
+            A[2 * i, 2 * k] = nA[i][k]
+            B[2 * i, 2 * k] = nB[i][k]
+    return A, B
+
+
+def test_spamm_tile_hand_enumerated_n4():
+    """oracle.spamm_tile (the reference of every sampled full-size tile check)
+    reproduces the hand-enumerated C tiles of the N=4, T=2 case: C00=3, C01=14, C10=2, C11=8
+    at E11, zero elsewhere."""
+    A, B = _hand_n4()
+    na, nb = oracle.tile_norms(A, 2), oracle.tile_norms(B, 2)
+    exp = {(0, 0): 3.0, (0, 1): 14.0, (1, 0): 2.0, (1, 1): 8.0}
+    for (i, j), v in exp.items():
+        t = oracle.spamm_tile(A, B, 2.0, 2, i, j, na, nb)
+        want = np.zeros((2, 2))
+        want[0, 0] = v
+        np.testing.assert_array_equal(t, want)
+
+
+@pytest.mark.parametrize("shape", [(100, 70, 45), (33, 129, 64), (64, 64, 96)])
+def test_spamm_tile_tau0_is_dense_tile_ragged(shape):
+    """tau = 0 keeps every pair, so each C tile -- including the partial edge tiles of ragged
+    shapes (zero padding) -- is the corresponding block of the plain product."""
+    m, k, n = shape
+    A = synth.random_matrix(m, k, seed=31)
+    B = synth.random_matrix(k, n, seed=32)
+    nA, nB = oracle.tile_norms(A, 32), oracle.tile_norms(B, 32)
+    full = A.astype(np.float64) @ B.astype(np.float64)
+    for i in range(nA.shape[0]):
+        for j in range(nB.shape[1]):
+            t = oracle.spamm_tile(A, B, 0.0, 32, i, j, nA, nB)
+            ref = full[i * 32:(i + 1) * 32, j * 32:(j + 1) * 32]
+            assert t.shape == ref.shape
+            np.testing.assert_allclose(t, ref, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_spamm_tile_single_kept_pair_is_block_product(seed):
+    """A C tile with exactly one kept k is that one block product A[i,k] B[k,j] (numpy
+    matmul of the raw blocks); a tile with none is exactly zero.  Ragged shape, edge tiles."""
+    m, k, n = 97, 150, 70
+    A = synth.perturbed_decay_matrix(k, 0.9, seed=40 + seed, m=m)
+    B = synth.perturbed_decay_matrix(n, 0.9, seed=50 + seed, m=k)
+    nA, nB = oracle.tile_norms(A, 32), oracle.tile_norms(B, 32)
+    p = nA[:, :, None] * nB[None, :, :]
+    checked_one = checked_none = 0
+    for tau in np.unique(p)[::7]:
+        keep = ~(p < tau)
+        for i in range(nA.shape[0]):
+            for j in range(nB.shape[1]):
+                ks = np.nonzero(keep[i, :, j])[0]
+                t = oracle.spamm_tile(A, B, float(tau), 32, i, j, nA, nB)
+                if ks.size == 0:
+                    assert np.all(t == 0.0)
+                    checked_none += 1
+                elif ks.size == 1:
+                    kk = int(ks[0])
+                    a = A[i * 32:(i + 1) * 32, kk * 32:(kk + 1) * 32].astype(np.float64)
+                    b = B[kk * 32:(kk + 1) * 32, j * 32:(j + 1) * 32].astype(np.float64)
+                    np.testing.assert_allclose(t, a @ b, rtol=1e-14, atol=1e-15)
+                    checked_one += 1
+    assert checked_one > 0 and checked_none > 0
+
+
+@pytest.mark.parametrize("shape", [(100, 70, 45), (300, 257, 129)])
+def test_spamm_tile_agrees_with_spamm_ragged(shape):
+    """Every tile of oracle.spamm_tile equals the same tile of oracle.spamm (two independent
+    loops over the same definition) at several tau, incl. the partial edge tiles."""
+    m, k, n = shape
+    A = synth.perturbed_decay_matrix(k, 0.95, seed=61, m=m)
+    B = synth.perturbed_decay_matrix(n, 0.95, seed=62, m=k)
+    nA, nB = oracle.tile_norms(A, 32), oracle.tile_norms(B, 32)
+    prods = np.sort((nA[:, :, None] * nB[None, :, :]).ravel())
+    for q in (0.1, 0.5, 0.9):
+        tau = float(prods[int(q * (len(prods) - 1))])
+        C = oracle.spamm(A, B, tau, 32, nA, nB)
+        for i in range(nA.shape[0]):
+            for j in range(nB.shape[1]):
+                t = oracle.spamm_tile(A, B, tau, 32, i, j, nA, nB)
+                np.testing.assert_allclose(t, C[i * 32:(i + 1) * 32, j * 32:(j + 1) * 32], rtol=1e-13, atol=1e-14)
+
+
+# --------------------------------------------------------------- band_count ---
+def test_band_count_hand_enumerated():
+    """Tie band of the north_star (products within 1e-6 relative of tau).  Products placed by
+    hand at tau(1 + d): row 0 (nA = 1) gives d = +1e-7, -5e-7 (inside), +3e-6, and three far
+    values (outside); row 1 (nA = 2, exact doubling) turns column 3 into tau(1 - 2e-7) (inside)
+    and everything else far from tau.  Expected count: 3."""
+    tau = 1.7
+    nA = np.array([[1.0], [2.0]])
+    nB = np.array([[tau * (1 + 1e-7), tau * (1 - 5e-7), tau * (1 + 3e-6),
+                    tau / 2 * (1 - 2e-7), tau / 2 * (1 + 5e-6), tau * 10]])
+    assert oracle.band_count(nA, nB, tau) == 3
+    assert oracle.band_count(nA, nB, tau, rel=1e-8) == 0
+    assert oracle.band_count(nA, nB, tau, rel=4e-6) == 4       # + tau(1 + 3e-6)
+    assert oracle.band_count(nA, nB, tau, rel=6e-6) == 5       # + 2 * tau/2 (1 + 5e-6)
+
+
+# -------------------------------------------------------- tile_error_bound ---
+def test_tile_error_bound_hand_values():
+    """sqrt(sum_ij (sum_{skipped k} nA nB)^2) on hand-computed maps.
+    1x3x1: products 4, 10, 18; tau 11 skips 4 and 10 -> 14; tau 0 -> 0; tau 100 -> 32.
+    2x2x2: nA = [[1,2],[3,4]], nB = [[1,.5],[2,3]]; products (i,k,j) 1 .5 4 6 3 1.5 8 12;
+    tau 5 skips (0,0,0)=1 (0,1,0)=4 | (0,0,1)=.5 | (1,0,0)=3 | (1,0,1)=1.5
+    -> sqrt(5^2 + .5^2 + 3^2 + 1.5^2) = sqrt(36.5)."""
+    nA = np.array([[1.0, 2.0, 3.0]])
+    nB = np.array([[4.0], [5.0], [6.0]])
+    assert oracle.tile_error_bound(nA, nB, 11.0) == 14.0
+    assert oracle.tile_error_bound(nA, nB, 0.0) == 0.0
+    assert oracle.tile_error_bound(nA, nB, 100.0) == 32.0
+    nA2 = np.array([[1.0, 2.0], [3.0, 4.0]])
+    nB2 = np.array([[1.0, 0.5], [2.0, 3.0]])
+    assert oracle.tile_error_bound(nA2, nB2, 5.0) == pytest.approx(math.sqrt(36.5), rel=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_tile_error_bound_is_tight_for_aligned_rank_one_tiles(seed):
+    """If every tile is c * E11 with c >= 0, each skipped product is (nA nB) E11 and they all
+    add at the same entry, so the triangle inequality and sub-multiplicativity are equalities:
+    ||E||_F equals the bound exactly (up to rounding).  A wrong (looser or tighter) bound fails."""
+    rng = np.random.default_rng(seed)
+    T, BD = 4, 6
+    A = np.zeros((BD * T, BD * T))
+    B = np.zeros((BD * T, BD * T))
+    A[::T, ::T] = rng.uniform(0.0, 2.0, (BD, BD))
+    B[::T, ::T] = rng.uniform(0.0, 2.0, (BD, BD))
+    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
+    for q in (0.2, 0.5, 0.8):
+        tau = float(np.quantile(nA[:, :, None] * nB[None, :, :], q))
+        err = oracle.error_fnorm(A, B, oracle.spamm(A, B, tau, T, nA, nB))
+        assert err == pytest.approx(oracle.tile_error_bound(nA, nB, tau), rel=1e-12)
+
+
+# ------------------------------------------------------ macro_lists (8 x 8) ---
+def test_macro_lists_8x8_hand_enumerated():
+    """The 8 x 8 grouping of the default tensor path (64-bit masks, bit li*8 + lj), tau = 1:
+    k=0: every tile row and column has norm 1 -> all 64 bits;  k=1: only (3,1)x(1,5) -> bit 29;
+    k=2: nA[7,2] = 2, nA[0,2] = .25, nB[2,0] = 2, nB[2,7] = 1 -> kept (7,0)=4 and (7,7)=2 (bits
+    56, 63); (0,0)=.5 and (0,7)=.25 skipped.  Rows 8, 9 form a second, ragged group: k=0 -> bits
+    0-15; k=1: nA[9,1] = 1 -> bit 13; k=2 nothing."""
+    nA = np.zeros((10, 3))
+    nB = np.zeros((3, 8))
+    nA[:, 0] = 1.0
+    nB[0, :] = 1.0
+    nA[3, 1] = 1.0
+    nA[9, 1] = 1.0
+    nB[1, 5] = 1.0
+    nA[7, 2], nA[0, 2] = 2.0, 0.25
+    nB[2, 0], nB[2, 7] = 2.0, 1.0
+    ml = oracle.macro_lists(nA, nB, 1.0, 8, 8)
+    assert ml["ptr"].tolist() == [0, 3, 5]
+    assert ml["entries"].tolist() == [[0, 2 ** 64 - 1], [1, 1 << 29], [2, (1 << 63) | (1 << 56)],
+                                      [0, 0xFFFF], [1, 1 << 13]]
