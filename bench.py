@@ -1,25 +1,31 @@
 #!/usr/bin/env python
-"""SpAMM hot-path benchmark (BASELINE.json metric: SpAMM time & effective TFLOP/s vs tau,
-speedup vs cuBLAS GEMM) on BASELINE.json configs[1]: N=8192 exponential-decay matrices
-a_ij = 0.99^|i-j|, tile 32, tau sweep 1e-10..1e-2, FP32 and BF16 paths.
+"""SpAMM hot-path benchmark.  BASELINE.json metric: "SpAMM time & effective TFLOP/s vs tau at
+1/2/4/8 B200; speedup vs cuBLAS GEMM", quoted on configs[4]:
 
-One STEP = one whole SpAMM call through the C ABI (spamm_run): tile norms of A and B ->
-skip map -> masked multiply into C, at the headline point (BF16 tcgen05 path,
-tau = 1e-6).  Inputs are resident in HBM; L2 (126 MB) is flushed by writing a 512 MB
-buffer and then reading another 512 MB buffer before every timed step, outside the
-step's CUDA events.
+  N = 65536 exponential-decay matrices a_ij = 0.999^|i-j|, A = B (C = A*A, the
+  paper's a_ij = b_ij workloads), tile 32, headline tau = 1e-6, BF16 tcgen05 path (FP32 C),
+  work-balanced row-block sharding at N GPUs (Sec. 3.4).
 
-  python bench.py [--gpus N --steps K --warmup W]            # our CUDA path
-  python bench.py --impl reference [...]                      # the CPU float64 oracle arm
+One STEP = one whole SpAMM through the C ABI: tile norms of A and B -> skip map -> masked
+multiply into C (spamm_run; spamm_multiply_mgpu on N > 1 GPUs, C rows sharded by work).
+Inputs are resident in HBM (8.6 GB, larger than the 126 MB L2, so no flush is needed between
+steps; smaller sweep sizes flush L2 before every timed step).
 
-Multi-GPU (torchrun, one rank per GPU): the same problem is row-partitioned across
-ranks with spamm_multiply_mgpu (Sec. 3.4 of the paper), strong scaling, max over ranks.
+  python bench.py [--gpus N --steps K --warmup W]       # our CUDA path (spawns N ranks itself
+                                                         # when not started by torchrun)
+  python bench.py --impl reference [...]                 # the float64 CPU oracle arm
+
+The JSON line also carries: per-stage times, kept (non-skipped) TFLOP/s, the roofline of the
+dominant kernel, a tau sweep at N = 65536 / 16384 (north_star's single-GPU target) / 8192 with
+cuBLAS on the same box, an end-to-end number through the public API with host buffers, the
+CPU-oracle baseline, clocks during the timed region and the count of our kernel launches.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,23 +40,36 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-N_DEFAULT = 8192
-LAM = 0.99
+N_DEFAULT = 65536
+LAM_DEFAULT = 0.999
 TAU_HEADLINE = 1e-6
-TAU_SWEEP = [1e-10, 1e-9, 1e-8, 1e-7, 1e-6, 1e-5, 1e-4, 1e-3, 1e-2]
+TAU5 = [1e-10, 1e-8, 1e-6, 1e-4, 1e-2]
+TAU9 = [1e-10, 1e-9, 1e-8, 1e-7, 1e-6, 1e-5, 1e-4, 1e-3, 1e-2]
 TILE = 32
-ORACLE_SAMPLE_TILE_ROWS = 64     # bounded CPU sample: 64 middle tile rows (2048 rows) of C
+L2_BYTES = 126 * 1024 * 1024
+METRIC = "SpAMM effective TFLOP/s (dense-equivalent 2N^3/t), configs[4]"
+DT = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp32x3": torch.float32}
 
 
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
+           "source": "fallback (B200_PROFILING.md)"}
     if os.path.exists(p):
         d = json.load(open(p))
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
-                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
-                "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "source": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
-            "source": "fallback (B200_PROFILING.md)"}
+        out = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+               "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+               "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "source": "measured (MEASURED_PEAKS.json)"}
+    # FP32 CUDA-core FFMA peak: measured by scripts/probe_ffma.cu on this pool's B200s
+    f = os.path.join(ROOT, "profiles", "ffma_peak.json")
+    if os.path.exists(f):
+        d = json.load(open(f))
+        out["fp32_tflops"] = d["tflops"]
+        out["fp32_source"] = f"measured FFMA peak ({d.get('how', 'scripts/probe_ffma.cu')})"
+    else:
+        out["fp32_tflops"] = 148 * 128 * 2 * out["sm_max_mhz"] * 1e6 / 1e12
+        out["fp32_source"] = "theoretical 148 SM x 128 FFMA x 2 x sm_max clock"
+    return out
 
 
 # ------------------------------------------------------------------ clocks ---
@@ -69,7 +88,7 @@ class ClockSampler:
         os.close(fd)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -78,7 +97,7 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
+        time.sleep(0.1)
         self.proc.terminate()
         self.proc.wait()
         sm, mx, reasons = [], None, set()
@@ -101,74 +120,101 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU oracle ---
-def _cpu_threads():
+def _cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     try:
         from threadpoolctl import threadpool_info
         n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
-        return int(max(n)) if n else os.cpu_count()
+        threads = int(max(n)) if n else os.cpu_count()
     except Exception:
-        return os.cpu_count()
+        threads = os.cpu_count()
+    return threads, model
 
 
-def oracle_sample(N: int, prec: str, tau: float, rows: int = ORACLE_SAMPLE_TILE_ROWS):
-    """Time the float64 oracle (as it stands) on a bounded sample: C rows of `rows` middle
-    tile rows of the same workload (their A rows times the full B; includes the norm
-    maps of the sample's A rows and of all of B).  Returns (seconds, dense-equivalent flops)."""
-    import oracle
-    A = synth.decay_matrix(N, "exp", LAM)
+def _table(N, lam, prec):
+    t = synth.decay_table("exp", N, lam).astype(np.float32)
     if prec == "bf16":
-        A = synth.round_to_bf16(A)
-    BM = N // TILE
-    r0 = (BM - rows) // 2
-    As = A[r0 * TILE:(r0 + rows) * TILE]
+        t = synth.round_to_bf16(t)
+    elif prec == "fp16":
+        t = synth.round_to_fp16(t)
+    return t
+
+
+def oracle_sample(N, lam, prec, tau, rows=8, cols=96, seed=0):
+    """The float64 oracle (as it stands) on a bounded sample of the workload: the C tiles of
+    `rows` middle tile rows x `cols` random tile columns, i.e. oracle.spamm(A[rows, :], B[:, cols])
+    -- norms of exactly those operand strips (all of K) and every kept product of those C tiles,
+    the same arithmetic those tiles get in the full problem.  Returns (seconds, dense-equivalent
+    flops of the sample, description)."""
+    import oracle
+    table = _table(N, lam, prec)
+    BD = N // TILE
+    r0 = (BD - rows) // 2
+    js = np.sort(np.random.default_rng(seed).choice(BD, size=cols, replace=False))
+    As = synth.toeplitz_block(table, r0 * TILE, (r0 + rows) * TILE, 0, N)
+    Bs = np.concatenate([synth.toeplitz_block(table, 0, N, j * TILE, (j + 1) * TILE) for j in js], axis=1)
     t0 = time.perf_counter()
-    C = oracle.spamm(As, A, tau, TILE)
+    C = oracle.spamm(As, Bs, tau, TILE)
     dt = time.perf_counter() - t0
-    assert C.shape == (rows * TILE, N)
-    return dt, 2.0 * rows * TILE * N * N
+    assert C.shape == (rows * TILE, cols * TILE)
+    desc = (f"{rows} middle tile rows x {cols} random tile columns of C ({rows * TILE} x {cols * TILE} of {N} x {N}), "
+            f"full K: float64 numpy oracle.spamm incl. the operand strips' norm maps")
+    return dt, 2.0 * rows * TILE * cols * TILE * N, desc
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle arm (rank 0 only; other ranks exit without work)."""
+    """--impl reference: the oracle arm on rank 0 (other ranks exit without work)."""
     if rank != 0:
         return
-    prec = args.precision
-    for _ in range(args.warmup):
-        oracle_sample(args.n, prec, args.tau, rows=args.ref_rows)
-    times, flops = [], 0.0
-    for _ in range(args.steps):
-        dt, flops = oracle_sample(args.n, prec, args.tau, rows=args.ref_rows)
+    for w in range(args.warmup):
+        oracle_sample(args.n, args.lam, args.precision, args.tau, seed=100 + w)
+    times, flops, desc = [], 0.0, ""
+    for s in range(args.steps):
+        dt, flops, desc = oracle_sample(args.n, args.lam, args.precision, args.tau, seed=s)
         times.append(dt)
     ms = 1e3 * statistics.mean(times)
     value = flops / (ms / 1e3) / 1e12
-    sample = (f"{args.ref_rows} middle tile rows ({args.ref_rows * TILE} of {args.n} rows of C) x full B, "
-              f"float64 numpy oracle incl. norm maps")
-    cores = _cpu_threads()
+    threads, model = _cpu_info()
     line = {
-        "impl": "reference", "metric": "SpAMM effective TFLOP/s (dense-equivalent 2MNK/t)", "value": value,
-        "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config(args, prec),
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(args, world),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "cpu": model, "kind": "oracle",
+                         "sample": desc},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def _config(args, prec):
-    return {"workload": f"configs[1]: N={args.n} exponential decay a_ij=0.99^|i-j| (A=B), tile 32, "
-                        f"tau={args.tau:g}, {prec.upper()} path", "N": args.n, "tile": TILE, "lambda": LAM,
-            "tau": args.tau, "precision": prec,
-            "parallelism": f"row-partition x{args.gpus}" if args.gpus > 1 else "single GPU",
-            "l2": "flushed before every timed step (512 MB write, then 512 MB read of another buffer)"}
+def _config(args, world):
+    N = args.n
+    big = N * N * (2 if args.precision in ("bf16", "fp16") else 4) > L2_BYTES
+    return {"workload": f"configs[4]: N={N} exponential decay a_ij={args.lam}^|i-j| (A=B), tile 32, "
+                        f"tau={args.tau:g}, {args.precision.upper()} path", "N": N, "tile": TILE,
+            "lambda": args.lam, "tau": args.tau, "precision": args.precision,
+            "parallelism": f"C row blocks balanced by skip-map work x{world}" if world > 1 else "single GPU",
+            "l2": ("inputs larger than L2 (no flush)" if big else
+                   "flushed before every timed step (512 MB write, then 512 MB read of another buffer)")}
 
 
 # --------------------------------------------------------------- GPU path ---
-def _device_inputs(N, prec, dev):
-    A32 = synth.decay_matrix(N, "exp", LAM)
-    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp32x3": torch.float32}[prec]
-    A = torch.from_numpy(A32).to(device=dev).to(dt)
-    return A32, A
+def _flusher(dev):
+    buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    rd = torch.zeros(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    out = torch.empty((), dtype=torch.float32, device=dev)
+
+    def flush():
+        buf.zero_()
+        torch.sum(rd, dim=0, out=out)
+    return flush
 
 
 def _timed(fn, steps, warmup, flush, stream):
@@ -177,7 +223,8 @@ def _timed(fn, steps, warmup, flush, stream):
     torch.cuda.synchronize()
     ms = []
     for _ in range(steps):
-        flush()
+        if flush is not None:
+            flush()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         fn()
@@ -187,6 +234,51 @@ def _timed(fn, steps, warmup, flush, stream):
     return ms
 
 
+def _roofline(st, prec, ms_mul, ms_norms, N, peaks, es, traffic):
+    """Roofline of the multiply: its floor is max(kept tensor FLOPs / tensor peak, compulsory
+    bytes / HBM peak) with the compulsory bytes = C written once + A read once (A = B)."""
+    kept_flops = 2.0 * TILE ** 3 * st["kept"]
+    mma_flops = kept_flops * (6 if prec == "fp32x3" else 1)   # fp32x3: six BF16 products per kept pair
+    c_bytes = 4.0 * N * N + es * N * N
+    if prec == "fp32":
+        fpeak, fname = peaks["fp32_tflops"], peaks["fp32_source"]
+    else:
+        fpeak, fname = peaks["bf16_tflops"], peaks["source"] + " bf16 dense, burst"
+    t_flop = mma_flops / (fpeak * 1e12)
+    t_byte = c_bytes / (peaks["hbm_gbs"] * 1e9)
+    tensor_bound = t_flop >= t_byte
+    s = ms_mul / 1e3
+    kname = {"fp32": "spamm_mul_simt_kernel", "fp32x3": "spamm_mul_x3_kernel"}.get(prec, "spamm_mul_dual_kernel")
+    roof = {"kernel": kname, "bound": ("tensor" if prec != "fp32" else "alu") if tensor_bound else "hbm",
+            "achieved": (mma_flops / s / 1e12) if tensor_bound else (c_bytes / s / 1e9),
+            "peak": fpeak if tensor_bound else peaks["hbm_gbs"],
+            "unit": "TFLOP/s" if tensor_bound else "GB/s",
+            "traffic": traffic,
+            "work_per_launch": (f"{'6*' if prec == 'fp32x3' else ''}2*32^3*kept = {mma_flops:.4g} FLOP "
+                                f"(kept={st['kept']}); compulsory bytes {c_bytes:.4g} (C write + A read)"),
+            "floor_ms": max(t_flop, t_byte) * 1e3, "peak_source": fname if tensor_bound else peaks["source"]}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    if prec != "fp32" and tensor_bound:
+        roof["frac_vs_sustained_peak"] = (mma_flops / s / 1e12) / peaks["bf16_tflops_sustained"]
+    norm_bytes = 1.0 * N * N * es + 2.0 * (N // TILE) ** 2 * 8      # A = B: read once, both maps written
+    norms = {"kernel": "tile_norms_kernel (A = B: one read, both maps)", "bound": "hbm",
+             "achieved": norm_bytes / (ms_norms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    norms["frac"] = norms["achieved"] / peaks["hbm_gbs"]
+    return roof, norms, kept_flops
+
+
+def _traffic(workload):
+    """dram read+write bytes per launch of the dominant kernel from an ncu --set full capture of
+    this exact workload (profiles/ncu_traffic.json, keyed by the config's workload string); null
+    when no capture of this workload exists."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(workload)
+    except (OSError, ValueError):
+        return None
+
+
 def run_ours(args, rank, world, local_rank):
     from paper_2103_13042_b200 import spamm as sp
     dev = torch.device("cuda", local_rank)
@@ -194,26 +286,16 @@ def run_ours(args, rank, world, local_rank):
     N, prec, tau = args.n, args.precision, args.tau
     peaks = _peaks()
     stream = torch.cuda.current_stream()
-    # L2 flush between timed steps: write a 512 MB buffer (evicts everything), then read a
-    # second 512 MB buffer so the flush's own dirty lines are written back before the timed
-    # region instead of inside the first kernel of the step (L2 ends clean, holding none of
-    # A, B, C or the plan's maps).
-    flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    flush_rd = torch.zeros(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    flush_out = torch.empty((), dtype=torch.float32, device=dev)
-
-    def flush():
-        flush_buf.zero_()
-        torch.sum(flush_rd, dim=0, out=flush_out)
+    es = 4 if prec in ("fp32", "fp32x3") else 2
+    big = N * N * es > L2_BYTES
+    flush = None if big else _flusher(dev)
 
     comm = None
     if world > 1:
-        import torch.distributed as dist
-        uid = [sp.spamm_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = sp.spamm_nccl_comm_init(world, rank, uid[0])
+        from paper_2103_13042_b200 import dist as spd
+        comm = spd.nccl_comm(rank, world)
 
-    A32, A = _device_inputs(N, prec, dev)
+    A = synth.toeplitz_device(_table(N, args.lam, prec), N, DT[prec], device=dev)
     C = torch.empty((N, N), dtype=torch.float32, device=dev)
     plan = sp.Plan(N, N, N, tau, prec, flags=sp.SPAMM_FLAG_TIMING)
 
@@ -223,18 +305,20 @@ def run_ours(args, rank, world, local_rank):
         else:
             sp.spamm_run(plan.handle, A, A, C)
 
-    # ---------------- headline: K timed steps (each step bracketed by CUDA events)
+    # ---------------- headline: W warm-up steps, then K timed steps (CUDA events per step,
+    # barrier + synchronize on both sides of the timed region, max over ranks)
     for _ in range(args.warmup):
         step()
-    _barrier(world)
     torch.cuda.synchronize()
+    _barrier(world)
     clocks = ClockSampler(local_rank)
     clocks.start()
     launches0 = sp.spamm_launch_count()
     step_ms, stage = [], {"norms": [], "skipmap": [], "multiply": []}
     t_wall = time.perf_counter()
     for _ in range(args.steps):
-        flush()
+        if flush is not None:
+            flush()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         step()
@@ -242,155 +326,102 @@ def run_ours(args, rank, world, local_rank):
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         st = plan.stats()
-        stage["norms"].append(st["ms_norms"])
-        stage["skipmap"].append(st["ms_skipmap"])
-        stage["multiply"].append(st["ms_multiply"])
+        for k in stage:
+            stage[k].append(st["ms_" + k])
     torch.cuda.synchronize()
     _barrier(world)
     wall_s = time.perf_counter() - t_wall
     launches = sp.spamm_launch_count() - launches0
     clk = clocks.stop()
     st = plan.stats()
-    ms_local = statistics.mean(step_ms)
-    ms = _max_over_ranks(ms_local, world)
-    dense_flops = 2.0 * N * N * N
-    value = dense_flops / (ms / 1e3) / 1e12
-
-    # ---------------- roofline of the dominant kernel (device time inside the timed region)
-    kept_flops = 2.0 * TILE ** 3 * st["kept"]
-    es = 4 if prec in ("fp32", "fp32x3") else 2
+    ms = _max_over_ranks(statistics.mean(step_ms), world)
+    value = 2.0 * N ** 3 / (ms / 1e3) / 1e12
     mean = {k: statistics.mean(v) for k, v in stage.items()}
-    dominant = max(mean, key=mean.get)
-    traffic = _ncu_traffic(prec)
-    if dominant == "multiply":
-        peak = peaks["bf16_tflops"] if prec != "fp32" else _fp32_peak(peaks)
-        # fp32x3 executes six BF16 products per kept pair on the tensor cores
-        mma_flops = kept_flops * (6 if prec == "fp32x3" else 1)
-        achieved = mma_flops / (mean["multiply"] / 1e3) / 1e12
-        # BF16/FP16: 256 x 256 macro-tiles (macro_i = 8) run multiply_dual.cu, 128 x 256 multiply_umma.cu
-        tc_kernel = "spamm_mul_dual_kernel" if st.get("macro_i") == 8 else "spamm_mul_umma_kernel"
-        kname = {"fp32": "spamm_mul_simt_kernel", "fp32x3": "spamm_mul_x3_kernel"}.get(prec, tc_kernel)
-        work = (f"6*2*32^3*kept = {mma_flops:.4g} BF16 MMA FLOP (kept={st['kept']})" if prec == "fp32x3"
-                else f"2*32^3*kept = {kept_flops:.4g} FLOP (kept={st['kept']})")
-        roof = {"kernel": kname,
-                "bound": "tensor" if prec != "fp32" else "alu", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic.get("multiply"),
-                "work_per_launch": work,
-                "peak_source": peaks["source"] + (" bf16 burst" if prec != "fp32" else
-                                                  " FP32 CUDA-core 148 SM x 128 FMA x 2 x sm_max clock")}
-    else:
-        bytes_alg = 1.0 * N * N * es + 2.0 * (N // TILE) ** 2 * 8     # A = B: read once (norms.cu)
-        achieved = bytes_alg / (mean["norms"] / 1e3) / 1e9
-        roof = {"kernel": "tile_norms_kernel", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic.get("norms"),
-                "work_per_launch": f"read A and B once ({bytes_alg:.4g} B)", "peak_source": peaks["source"]}
-    # secondary: the HBM-bound norm stage
-    # A = B (C = A*A): the norm kernel reads the matrix once and writes both maps
-    norm_bytes = 1.0 * N * N * es + 2.0 * (N // TILE) ** 2 * 8
-    norms_roof = {"kernel": "tile_norms_kernel (A = B: one read, both maps)", "bound": "hbm",
-                  "achieved": norm_bytes / (mean["norms"] / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
-    norms_roof["frac"] = norms_roof["achieved"] / peaks["hbm_gbs"]
+    cfg = _config(args, world)
+    roof, norms_roof, kept_flops = _roofline(st, prec, mean["multiply"], mean["norms"], N, peaks, es,
+                                             _traffic(cfg["workload"]))
+    shares = {k: v / max(sum(mean.values()), 1e-9) for k, v in mean.items()}
+    kept_all = _sum_over_ranks(st["kept"], world)
 
-    # ---------------- end to end through the public API with host buffers
-    e2e = None
-    if not args.no_e2e:
-        e2e = _e2e(sp, A32, prec, N, tau, args, stream, flush, world, rank, comm)
-
-    # ---------------- tau sweep, both paths, and cuBLAS on the same box
-    sweep, cublas = None, None
+    e2e = None if args.no_e2e else _e2e(sp, plan, A, C, prec, N, args, world, rank, comm)
+    sweep = None
     if not args.no_sweep and world == 1:
-        sweep, cublas = _sweep(sp, N, stream, flush)
-
+        sweep = _sweeps(sp, A, N, prec, args, flush, stream, dev)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dt, fl = oracle_sample(N, prec, tau)
-        cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": _cpu_threads(), "kind": "oracle",
-               "sample": f"{ORACLE_SAMPLE_TILE_ROWS} middle tile rows ({ORACLE_SAMPLE_TILE_ROWS * TILE} of {N} rows "
-                         f"of C) x full B, float64 numpy oracle incl. norm maps; {dt:.2f} s"}
-
+    if rank == 0 and not args.no_cpu_baseline:
+        dt, fl, desc = oracle_sample(N, args.lam, prec, tau)
+        threads, model = _cpu_info()
+        cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "cpu": model, "kind": "oracle",
+               "sample": f"{desc}; {dt:.2f} s"}
+    plan.close()
     if comm is not None:
         sp.spamm_nccl_comm_destroy(comm)
     if rank != 0:
         return
     line = {
-        "metric": "SpAMM effective TFLOP/s (dense-equivalent 2MNK/t)", "value": value, "unit": "TFLOP/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": prec, "data": "synthetic", "config": _config(args, prec),
-        "stages_ms": mean, "valid_ratio": st["valid_ratio"], "kept_pairs": st["kept"],
-        "macro_steps": st["macro_entries"],
-        "kept_tflops": kept_flops / (ms / 1e3) / 1e12,
-        "roofline": roof, "roofline_norms": norms_roof,
-        "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-        "wall_s_timed_region_incl_flush": wall_s,
-        "cpu_baseline": cpu, "sweep": sweep, "cublas": cublas,
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": prec, "data": "synthetic (device-generated Toeplitz input)",
+        "config": cfg, "stages_ms": mean, "stage_share": shares, "valid_ratio": st["valid_ratio"],
+        "kept_pairs": kept_all, "kept_tflops": 2.0 * TILE ** 3 * kept_all / (ms / 1e3) / 1e12,
+        "roofline": roof, "roofline_norms": norms_roof, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk, "wall_s_timed_region": wall_s, "cpu_baseline": cpu, "sweep": sweep,
     }
-    if cublas and prec in cublas:
-        line["speedup_vs_cublas"] = cublas[prec]["ms"] / ms
+    if sweep and sweep.get("cublas", {}).get(f"N={N}"):
+        line["speedup_vs_cublas"] = sweep["cublas"][f"N={N}"]["ms"] / ms
     print(json.dumps(line), flush=True)
 
 
-def _fp32_peak(peaks):
-    return 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
-
-
-def _ncu_traffic(prec):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        try:
-            return json.load(open(p)).get(prec, {})
-        except Exception:
-            return {}
-    return {}
-
-
-def _e2e(sp, A32, prec, N, tau, args, stream, flush, world, rank, comm):
-    """End to end through the public API: every step copies that step's A (the workload is
-    C = A*A, so A is the only input) from pinned host memory, runs spamm_run, and copies C back
-    to pinned host memory.  Steps are pipelined over three streams with double buffers (step
-    i+1's upload and step i-1's download overlap step i's compute, as a streaming user would
-    run it); the timed region spans the first upload to the last download.  Inputs are larger
-    than L2 and arrive fresh from the host every step."""
-    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp32x3": torch.float32}[prec]
-    host = torch.from_numpy(A32).to(dt)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    Ah = [host.pin_memory(), host.clone().pin_memory()]
-    Ch = [torch.empty((N, N), dtype=torch.float32).pin_memory() for _ in range(2)]
-    Ad = [torch.empty_like(host, device=dev) for _ in range(2)]
-    Cd = [torch.empty((N, N), dtype=torch.float32, device=dev) for _ in range(2)]
-    plan = sp.Plan(N, N, N, tau, prec)
-    s_up, s_cmp, s_dn = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+def _e2e(sp, plan, A, C, prec, N, args, world, rank, comm):
+    """End to end through the public API with host buffers: every step copies the step's input
+    A (C = A*A) from pinned host memory to the device, runs the SpAMM (spamm_run, or
+    spamm_multiply_mgpu on this rank's share) and copies this rank's rows of C back to pinned
+    host memory.  Two device buffer sets: step i+1's upload and step i-1's download overlap
+    step i's compute (upload / compute / download streams)."""
+    dev = A.device
+    host_a = torch.empty((N, N), dtype=A.dtype, pin_memory=True)
+    host_a.copy_(A)
+    Ad = [A, torch.empty_like(A)]
+    Cd = [C, torch.empty_like(C)]
+    row_part = None
+    if world > 1:
+        sp.spamm_multiply_mgpu(plan.handle, comm, rank, world, A, A, C, 0)
+        cut = sp.spamm_get_partition(plan.handle, world)
+        row_part = (min(cut[rank] * TILE, N), min(cut[rank + 1] * TILE, N))
+    r0, r1 = row_part or (0, N)
+    host_c = torch.empty((max(r1 - r0, 1), N), dtype=torch.float32, pin_memory=True)
+    s_up, s_cmp, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("up", "cmp", "dn")}
-    started = [[False, False]]
+    started = [False, False]
 
     def step(i):
         b = i % 2
         with torch.cuda.stream(s_up):
-            if started[0][b]:
-                s_up.wait_event(ev["cmp"][b])          # Ad[b] free: its previous product is done
-            Ad[b].copy_(Ah[b], non_blocking=True)
+            if started[b]:
+                s_up.wait_event(ev["cmp"][b])
+            Ad[b].copy_(host_a, non_blocking=True)
             ev["up"][b].record(s_up)
         with torch.cuda.stream(s_cmp):
             s_cmp.wait_event(ev["up"][b])
-            if started[0][b]:
-                s_cmp.wait_event(ev["dn"][b])          # Cd[b] free: its previous download is done
+            if started[b]:
+                s_cmp.wait_event(ev["dn"][b])
             if world > 1:
-                sp.spamm_multiply_mgpu(plan.handle, comm, rank, world, Ad[b], Ad[b], Cd[b], sp.SPAMM_MGPU_GATHER_C,
-                                       stream=s_cmp)
+                sp.spamm_multiply_mgpu(plan.handle, comm, rank, world, Ad[b], Ad[b], Cd[b], 0, stream=s_cmp)
             else:
                 sp.spamm_run(plan.handle, Ad[b], Ad[b], Cd[b], stream=s_cmp)
             ev["cmp"][b].record(s_cmp)
         with torch.cuda.stream(s_dn):
             s_dn.wait_event(ev["cmp"][b])
-            Ch[b].copy_(Cd[b], non_blocking=True)
+            if r1 > r0:
+                host_c.copy_(Cd[b][r0:r1], non_blocking=True)
             ev["dn"][b].record(s_dn)
-        started[0][b] = True
+        started[b] = True
 
     for i in range(2):
         step(i)
     torch.cuda.synchronize()
     _barrier(world)
-    n = max(4, args.steps)
+    n = max(3, min(args.steps, 6))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s_up)
     for i in range(n):
@@ -399,67 +430,80 @@ def _e2e(sp, A32, prec, N, tau, args, stream, flush, world, rank, comm):
     e1.record(s_up)
     e1.synchronize()
     ms = _max_over_ranks(e0.elapsed_time(e1) / n, world)
-    plan.close()
+    del Ad[1], Cd[1]
+    torch.cuda.empty_cache()
+    h2d = int(host_a.numel() * host_a.element_size()) * world
+    d2h = int(N * N * 4)
     return {"value": 2.0 * N ** 3 / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": int(host.numel() * host.element_size()),
-            "d2h_bytes_per_step": int(N * N * 4), "steps": n,
-            "note": "pinned host A -> device, spamm_run (C = A*A), C -> pinned host, every step; "
-                    "pipelined over upload/compute/download streams with double buffers"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n,
+            "note": "pinned host A -> device, SpAMM through the C ABI, this rank's C rows -> pinned host, every "
+                    "step; pipelined over upload / compute / download streams with two device buffer sets"}
 
 
-def _sweep(sp, N, stream, flush):
+def _sweep_one(sp, A, N, prec, taus, flush, stream, reps=3):
     out = []
-    A32 = synth.decay_matrix(N, "exp", LAM)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    cublas = {}
-    for prec in ("fp32", "fp32x3", "bf16"):
-        dt = {"bf16": torch.bfloat16, "fp32": torch.float32, "fp32x3": torch.float32}[prec]
-        A = torch.from_numpy(A32).to(device=dev).to(dt)
-        C = torch.empty((N, N), dtype=torch.float32, device=dev)
-        plan = sp.Plan(N, N, N, TAU_SWEEP[0], prec, flags=sp.SPAMM_FLAG_TIMING)
-        for tau in TAU_SWEEP:
+    C = torch.empty((N, N), dtype=torch.float32, device=A.device)
+    with sp.Plan(N, N, N, taus[0], prec, flags=sp.SPAMM_FLAG_TIMING) as plan:
+        for tau in taus:
             plan.set_tau(tau)
             stages = {"norms": [], "skipmap": [], "multiply": []}
-
-            def step():
-                sp.spamm_run(plan.handle, A, A, C)
-
             ms_list = []
-            for i in range(2 + 5):
-                flush()
+            for i in range(1 + reps):
+                if flush is not None:
+                    flush()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                step()
+                sp.spamm_run(plan.handle, A, A, C)
                 e1.record(stream)
                 e1.synchronize()
-                if i >= 2:
+                if i >= 1:
                     ms_list.append(e0.elapsed_time(e1))
                     s = plan.stats()
                     for k in stages:
                         stages[k].append(s["ms_" + k])
             s = plan.stats()
             ms = statistics.median(ms_list)
-            out.append({"precision": prec, "tau": tau, "ms": ms, "valid_ratio": s["valid_ratio"],
+            out.append({"N": N, "precision": prec, "tau": tau, "ms": ms, "valid_ratio": s["valid_ratio"],
                         "kept": s["kept"], "stages_ms": {k: statistics.median(v) for k, v in stages.items()},
                         "tflops_dense_equiv": 2.0 * N ** 3 / (ms / 1e3) / 1e12,
-                        "tflops_kept": 2.0 * TILE ** 3 * s["kept"] / (ms / 1e3) / 1e12})
-        plan.close()
-        # cuBLAS dense GEMM on the same matrices (torch.matmul -> cublas), same flush protocol
-        torch.backends.cuda.matmul.allow_tf32 = False
-        torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
-        gemm = lambda: torch.matmul(A, A)  # noqa: E731
-        if prec == "fp32x3":   # same FP32 inputs and accuracy class: compared with the SGEMM
-            ms_c = cublas["fp32"]["ms"]
-        else:
-            ms_c = statistics.median(_timed(gemm, 3 if prec == "fp32" else 5, 2, flush, stream))
-            cublas[prec] = {"ms": ms_c, "tflops": 2.0 * N ** 3 / (ms_c / 1e3) / 1e12,
-                            "call": "torch.matmul (cuBLAS), " + ("FP32 SGEMM, TF32 off" if prec == "fp32"
-                                                                else "BF16 in, FP32 accumulate")}
-        for r in out:
-            if r["precision"] == prec:
-                r["speedup_vs_cublas"] = ms_c / r["ms"]
-        del A, C
-    return out, cublas
+                        "tflops_kept": 2.0 * TILE ** 3 * s["kept"] / (ms / 1e3) / 1e12,
+                        "multiply_tflops_kept": 2.0 * TILE ** 3 * s["kept"] / (statistics.median(stages["multiply"]) / 1e3) / 1e12})
+    del C
+    return out
+
+
+def _cublas(A, flush, stream, reps):
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+    ms = statistics.median(_timed(lambda: torch.matmul(A, A), reps, 1, flush, stream))
+    N = A.shape[0]
+    return {"ms": ms, "tflops": 2.0 * N ** 3 / (ms / 1e3) / 1e12,
+            "call": "torch.matmul (cuBLAS), " + ("FP32 SGEMM, TF32 off" if A.dtype == torch.float32
+                                                else f"{str(A.dtype)[6:]} in, FP32 accumulate")}
+
+
+def _sweeps(sp, A, N, prec, args, flush, stream, dev):
+    """tau sweeps on configs[4] (the headline size), the north_star's N = 16384 exponential-decay
+    target and configs[1] N = 8192, with cuBLAS dense GEMM on the same box and inputs."""
+    res, cublas = [], {}
+    res += _sweep_one(sp, A, N, prec, TAU5, flush, stream)
+    cublas[f"N={N}"] = _cublas(A, flush, stream, 3)
+    small_flush = _flusher(dev)
+    for n2, lam2, precs, taus in ((16384, 0.99, ("bf16", "fp32x3", "fp32"), TAU5), (8192, 0.99, ("bf16", "fp32x3"), TAU9)):
+        for p2 in precs:
+            A2 = synth.toeplitz_device(_table(n2, lam2, p2), n2, DT[p2], device=dev)
+            res += _sweep_one(sp, A2, n2, p2, taus, small_flush, stream)
+            if p2 != "fp32x3":
+                cublas[f"N={n2} {p2}"] = _cublas(A2, small_flush, stream, 3)
+            del A2
+    for r in res:
+        key = f"N={r['N']}" if r["N"] == N else f"N={r['N']} {'fp32' if r['precision'] == 'fp32x3' else r['precision']}"
+        if key in cublas and (r["N"] != N or r["precision"] == prec):
+            r["speedup_vs_cublas"] = cublas[key]["ms"] / r["ms"]
+    torch.cuda.empty_cache()
+    return {"points": res, "cublas": cublas,
+            "workloads": {f"N={N}": f"configs[4] lambda={args.lam}", "N=16384": "north_star target, lambda=0.99",
+                          "N=8192": "configs[1], lambda=0.99"}}
 
 
 def _barrier(world):
@@ -477,6 +521,30 @@ def _max_over_ranks(x, world):
     return float(t.item())
 
 
+def _sum_over_ranks(x, world):
+    if world <= 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(args_list, n):
+    """--gpus N started without a launcher: run N ranks under torch.distributed.run ourselves."""
+    if torch.cuda.device_count() < n:
+        sys.exit(f"bench.py: --gpus {n} requested but only {torch.cuda.device_count()} CUDA device(s) visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *args_list]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -486,17 +554,21 @@ def main():
     ap.add_argument("--precision", choices=["bf16", "fp16", "fp32", "fp32x3"], default="bf16")
     ap.add_argument("--tau", type=float, default=TAU_HEADLINE)
     ap.add_argument("--n", type=int, default=N_DEFAULT)
-    ap.add_argument("--ref-rows", type=int, default=16, help="oracle sample (tile rows) per reference step")
+    ap.add_argument("--lam", type=float, default=LAM_DEFAULT)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-
+    if args.impl == "ours":
+        args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _spawn(sys.argv[1:], args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and "WORLD_SIZE" in os.environ:
+    if world != args.gpus:
+        if rank == 0:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
         args.gpus = world
     if args.impl == "reference":
         run_reference(args, rank, world)

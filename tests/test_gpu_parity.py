@@ -13,6 +13,7 @@ import torch
 
 import oracle
 import synth
+from gpu_helpers import tile_max_rel
 
 pytestmark = pytest.mark.gpu
 
@@ -152,6 +153,10 @@ def test_spamm_parity_ragged(sp, prec, shape, q):
     # tighter regression guards: FP32 accumulation of exactly-representable products (fp32,
     # bf16/fp16 with the same rounded inputs on both sides), FP32-level split products (fp32x3)
     assert err <= {"fp32": 2e-6, "fp32x3": 5e-6}.get(prec, 1e-5), err
+    # per C tile, relative to the same tile of SpAMM(|A|, |B|) (same keep set): a single wrong
+    # tile cannot hide inside the global norm
+    absref = oracle.spamm(np.abs(A), np.abs(B), tau, T, nA, nB)
+    assert tile_max_rel(C, ref, absref) <= {"fp32": 2e-6, "fp32x3": 5e-6}.get(prec, 1e-5)
 
 
 def test_macro_lists_match_oracle(sp):
