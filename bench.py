@@ -273,9 +273,8 @@ def _traffic(workload):
     when no capture of this workload exists."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(p))
-        return d.get(workload)
-    except (OSError, ValueError):
+        return json.load(open(p)).get(workload, {}).get("multiply")
+    except (OSError, ValueError, AttributeError):
         return None
 
 

@@ -64,20 +64,19 @@ typedef enum {
                       6 bytes per element), the multiply sums the six products a0b0 + a0b1 +
                       a1b0 + a0b2 + a1b1 + a2b0 per kept pair with two-level FP32 accumulation
                       (TMEM partials of 4 k-steps added in registers).  FP32-level accuracy;
-                      same norms, tau semantics and skip map as SPAMM_FP32.  Single GPU only
-                      (spamm_multiply_mgpu with nranks > 1 returns SPAMM_E_UNSUPPORTED). */
+                      same norms, tau semantics and skip map as SPAMM_FP32. */
 } spamm_precision;
 
 /* plan flags */
 #define SPAMM_FLAG_NONE           0u
 #define SPAMM_FLAG_TIMING         1u  /* record per-stage CUDA events (spamm_get_stats) */
-#define SPAMM_FLAG_SYNC_SKIPMAP   2u  /* size the skip map exactly with one stream sync
-                                         instead of reserving the worst case up front  */
 
 /* spamm_multiply flags */
 #define SPAMM_MUL_AUTO            1u  /* run spamm_norms + spamm_build_skipmap first (spamm_run) */
 
 #define SPAMM_MUL_OUTPUT_NORMS    2u  /* spamm_multiply_chain: also write the tile norms of the result */
+#define SPAMM_MUL_LOW_ONLY        4u  /* spamm_multiply_chain: C_low is the only output (no FP32 C is
+                                         written or read; C may be NULL; needs beta = 0) */
 
 /* spamm_multiply_mgpu flags (Sec. 3.4) */
 #define SPAMM_MGPU_INPUTS_REPLICATED 0u  /* every rank already holds full A and B           */
@@ -132,14 +131,17 @@ spamm_status spamm_norms(spamm_plan_t p, const void* A, int64_t lda, const void*
                          void* stream);
 
 /* Stage 2 (Alg. 2 lines 3-16; Sec. 3.5.1):
- * keep(i,k,j) <=> !(nA[i][k] * nB[k][j] < tau) in float64 (NaN kept).  Emits
- *   leaf lists: k_idx[kept] (uint16), the list of C tile t = i*BN+j is the ascending run
- *               k_idx[tile_start[t] .. tile_start[t] + V[t]) (lists stored macro-tile-major)
- *   V[i][j]   : list lengths;  row_work[i] = sum_j V[i][j]
- *   macro lists: per macro-tile of macro_i x macro_j C tiles, the union of kept k
- *               in ascending order with a keep bit per C tile, and an LPT schedule.
- * Requires spamm_norms on this plan (else SPAMM_E_STATE).  Stream-ordered; with
- * SPAMM_FLAG_SYNC_SKIPMAP it synchronises the stream once to size the lists. */
+ * keep(i,k,j) <=> !(nA[i][k] * nB[k][j] < tau) in float64 (NaN kept).  Builds
+ *   macro lists: per macro-tile of macro_i x macro_j C tiles, the union of kept k in
+ *               ascending order with a keep bit per C tile (the complete skip map), the
+ *               tensor path's pre-decoded MMA runs, and an LPT schedule;
+ *   row_work[i] = sum_j V[i][j];  kept / macro-entry totals.
+ * Output-sensitive: a norm pyramid (max and min of the norms over each macro row / column and
+ * 32 k-tiles; one quadtree level of Eq. 1) decides whole chunks of k exactly
+ * (all skipped / all kept) and only the remaining chunks test their products one by one.
+ * The per-C-tile view (V, ascending k lists) is expanded from the macro lists on request
+ * (spamm_get_skipmap / spamm_get_counts).  Requires spamm_norms on this plan (else
+ * SPAMM_E_STATE).  Stream-ordered, no host synchronisation. */
 spamm_status spamm_build_skipmap(spamm_plan_t p, void* stream);
 
 /* Stage 3 (Sec. 3.3, Alg. 2/3): C[i,j] = sum over kept k, ascending,
@@ -171,16 +173,32 @@ spamm_status spamm_partition_rows(const int64_t* row_work, int64_t BM, int nrank
 
 /* Row-partitioned SpAMM over nranks GPUs of one node (Sec. 3.4, Alg. 4):
  *   1. (INPUTS_ON_ROOT) ncclBroadcast of A and B from rank 0 into the caller's buffers;
- *   2. each rank norms its share of A's and B's tile rows; ncclAllGather of the maps;
- *   3. each rank counts kept pairs for its provisional rows; ncclAllGather of row work;
- *      spamm_partition_rows cuts C tile-rows by work (identical on every rank);
- *   4. each rank emits the lists of its rows and multiplies them into C rows;
- *   5. (GATHER_C) C rows are exchanged so every rank holds all of C.
+ *   2. each rank norms its share of A's tile rows and B's tile columns (FP32X3: all of them,
+ *      its split planes are operands); grouped ncclBroadcasts all-gather the maps;
+ *   3. each rank builds the skip map of its provisional (even) macro-row share, which yields
+ *      that share's row work; ncclAllReduce of the row work;
+ *   4. a one-CTA kernel cuts macro rows at equal shares of the total work with the rule of
+ *      spamm_partition_rows (identical on every rank, decided on the device: no host sync);
+ *      each rank completes the skip map of its final rows and multiplies them into C rows;
+ *   5. (GATHER_C) C rows are exchanged so every rank holds all of C (this step reads the cut
+ *      back to the host: one stream synchronisation).
  * A, B, C are full-size device buffers on every rank (only this rank's rows of C are
- * written unless GATHER_C).  comm: ncclComm_t from spamm_nccl_comm_init. */
+ * written unless GATHER_C).  comm: ncclComm_t from spamm_nccl_comm_init.  At most 64 ranks;
+ * chained outputs are single-GPU (SPAMM_E_UNSUPPORTED).  The partition is readable with
+ * spamm_get_partition (synchronises). */
 spamm_status spamm_multiply_mgpu(spamm_plan_t p, void* nccl_comm, int rank, int nranks,
                                  const void* A, int64_t lda, const void* B, int64_t ldb,
                                  float* C, int64_t ldc, uint32_t flags, void* stream);
+
+/* The same nranks-rank computation emulated on ONE GPU for verification (the survey's P4
+ * invariant: multi-rank C and skip maps equal single-GPU ones): plans[q] plays rank q (all
+ * plans of the same shape, precision, tau and device), C[q] is rank q's full-size C buffer.
+ * Phases and kernels are exactly those of spamm_multiply_mgpu; only the transport differs --
+ * the collectives are device copies between the plans' buffers on `stream`, in rank order.
+ * flags: SPAMM_MGPU_GATHER_C as above (INPUTS_ON_ROOT is a no-op: the ranks share A and B). */
+spamm_status spamm_multiply_mgpu_local(spamm_plan_t* plans, int nranks, const void* A, int64_t lda,
+                                       const void* B, int64_t ldb, float* const* C, int64_t ldc,
+                                       uint32_t flags, void* stream);
 
 /* General update C = alpha * SpAMM(A, B, tau) + beta * C (the problem statement's alpha and
  * beta) for every later spamm_multiply / spamm_run /
@@ -198,7 +216,9 @@ spamm_status spamm_set_scalars(spamm_plan_t p, double alpha, double beta);
  *     elements): writes C rounded (RNE) to the plan's input type -- the next product's operand;
  *   - with SPAMM_MUL_OUTPUT_NORMS: writes the float64 tile norms of the written result into a
  *     plan-owned map nC[BM][BN] (Eq. 2 of the values stored: C, or C_low's rounded values when
- *     given -- reading R4), readable with spamm_get_output_norms.
+ *     given -- reading R4), readable with spamm_get_output_norms;
+ *   - with SPAMM_MUL_LOW_ONLY (BF16/FP16 plans, C_low required, beta = 0): C_low is the only
+ *     output -- no FP32 C is stored (C may be NULL), halving the output traffic.
  * FP32X3 plans return SPAMM_E_UNSUPPORTED. */
 spamm_status spamm_multiply_chain(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
                                   float* C, int64_t ldc, void* C_low, int64_t ldcl, uint32_t flags,

@@ -31,9 +31,7 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
 
-spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void* base,
-                            uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_inner,
-                            uint32_t box_outer, CUtensorMapSwizzle swz) {
+static bool resolve_encode() {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -41,7 +39,13 @@ spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t e
         q == cudaDriverEntryPointSuccess)
       g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   });
-  if (!g_encode) return fail(SPAMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return g_encode != nullptr;
+}
+
+spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void* base,
+                            uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_inner,
+                            uint32_t box_outer, CUtensorMapSwizzle swz) {
+  if (!resolve_encode()) return fail(SPAMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {ld_elems * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
@@ -55,8 +59,7 @@ spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t e
 spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
                             uint64_t mid, uint64_t outer, uint64_t mid_stride_bytes, uint64_t outer_stride_bytes,
                             uint32_t box0, uint32_t box1, uint32_t box2, CUtensorMapSwizzle swz) {
-  CUtensorMap dummy;
-  SPAMM_TRY(encode_tmap_2d(&dummy, dt, 2, base, 16, 1, 16, 8, 1, CU_TENSOR_MAP_SWIZZLE_NONE));  // resolves g_encode
+  if (!resolve_encode()) return fail(SPAMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {inner, mid, outer};
   cuuint64_t strides[2] = {mid_stride_bytes, outer_stride_bytes};
   cuuint32_t box[3] = {box0, box1, box2};
@@ -70,8 +73,7 @@ spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void
 // --------------------------------------------------------------- validation
 static size_t esize_of(spamm_precision p) { return f32_inputs(p) ? 4 : 2; }
 
-static spamm_status check_matrix(const void* ptr, int64_t rows, int64_t cols, int64_t ld, size_t esize,
-                                 const char* name) {
+spamm_status check_matrix(const void* ptr, int64_t rows, int64_t cols, int64_t ld, size_t esize, const char* name) {
   if (ptr == nullptr) return fail(SPAMM_E_INVALID, std::string(name) + " is NULL");
   if (ld < cols) return fail(SPAMM_E_INVALID, std::string(name) + ": leading dimension < columns");
   if ((reinterpret_cast<uintptr_t>(ptr) & 15u) != 0)
@@ -128,29 +130,40 @@ spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, 
 
 static void free_plan(Plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->nA, p->nBt, p->V, p->U, p->leaf_start, p->L, p->leaf_base, p->macro_ptr, p->row_work, p->leaf_k, p->macro_ent, p->macro_run,
-                  p->order, p->bucket_pos, p->ticket, p->sched, p->cub_tmp, p->sk_scratch, p->sk_ticket, p->sk_wpre, p->split_cnt, p->split_scr,
-                  p->planes, p->nC};
+  void* ptrs[] = {p->nA, p->nBt, p->pyr, p->V, p->U, p->L, p->leaf_start, p->row_work, p->ticket, p->sched,
+                  p->leaf_k, p->macro_ent, p->macro_run, p->order, p->bucket_pos, p->mstart, p->d_range,
+                  p->ts_cnt, p->ts_part, p->planes, p->nC};
   for (void* q : ptrs)
     if (q) cudaFree(q);
-  if (p->mstart && p->mstart != p->macro_ptr) cudaFree(p->mstart);
-  if (p->Uw && p->Uw != p->U) cudaFree(p->Uw);
-  if (p->h_totals) cudaFreeHost(p->h_totals);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
   delete p;
 }
 
-// worst-case leaf list reservation budget (bytes); above it the skip map is sized exactly
-static constexpr size_t kWorstCaseBudget = size_t(8) << 30;
+// per-C-tile k lists (2 B per C tile and k: 17 GB at N = 65536) are reserved at plan creation
+// when under this budget, else on the first request for them
+static constexpr size_t kLeafEagerBudget = size_t(2) << 30;
 
-static spamm_status ensure_leaf_capacity(Plan& p, int64_t need) {
-  if (need <= p.leaf_cap) return SPAMM_OK;
-  if (p.leaf_k) cudaFree(p.leaf_k);
-  p.leaf_k = nullptr;
-  p.leaf_cap = 0;
-  SPAMM_TRY(alloc(reinterpret_cast<void**>(&p.leaf_k), sizeof(uint16_t) * static_cast<size_t>(need)));
-  p.leaf_cap = need;
+static spamm_status ensure_leaf_storage(Plan& p) {
+  if (p.leaf_alloc) return SPAMM_OK;
+  SPAMM_TRY(alloc(reinterpret_cast<void**>(&p.leaf_k),
+                  sizeof(uint16_t) * static_cast<size_t>(p.BM * p.BN) * static_cast<size_t>(p.BK)));
+  p.leaf_alloc = true;
+  return SPAMM_OK;
+}
+
+// host view of the range decided on the device (multi-GPU partition)
+spamm_status sync_range(Plan& p) {
+  if (!p.range_on_device) return SPAMM_OK;
+  int64_t h[kRangeWords];
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
+  SPAMM_CUDA_TRY(cudaMemcpy(h, p.d_range, sizeof(h), cudaMemcpyDeviceToHost));
+  p.row_begin_macro = h[0];
+  p.row_end_macro = h[1];
+  const int nr = static_cast<int>(h[4]);
+  p.last_partition.assign(nr + 1, 0);
+  for (int q = 0; q <= nr; ++q) p.last_partition[q] = std::min<int64_t>(h[6 + q] * p.MI, p.BM);
+  p.range_on_device = false;
   return SPAMM_OK;
 }
 
@@ -185,6 +198,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   if (!tau_ok(tau)) return fail(SPAMM_E_INVALID, "tau must be finite and >= 0");
   if (prec != SPAMM_FP32 && prec != SPAMM_BF16 && prec != SPAMM_FP16 && prec != SPAMM_FP32X3)
     return fail(SPAMM_E_INVALID, "unknown precision");
+  if (flags & ~SPAMM_FLAG_TIMING) return fail(SPAMM_E_INVALID, "unknown plan flag");
   if (tile != kTile) {
     if (tile == 64 || tile == 128) return fail(SPAMM_E_UNSUPPORTED, "only tile (LoNum) = 32 is implemented");
     return fail(SPAMM_E_INVALID, "tile must be 32, 64 or 128");
@@ -205,16 +219,11 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->BM = BM;
   p->BK = BK;
   p->BN = BN;
-  // the 256 x 256 two-issuer tensor path needs fixed list regions and whole 32-column B boxes
-  // (the macro lists are always reserved at their worst case; the per-C-tile lists only on request)
-  const bool fixed_ok = !(flags & SPAMM_FLAG_SYNC_SKIPMAP);
-  p->umma_variant = umma_variant_from_env();
-  p->dual = !f32_inputs(prec) && fixed_ok && p->umma_variant == 5;
-  if (!f32_inputs(prec) && !p->dual && p->umma_variant == 5) p->umma_variant = 0;
-  p->MI = p->dual ? kMacroI_dual : kMacroI;
-  p->MJ = f32_inputs(prec) ? kMacroJ_simt : kMacroJ_umma;
+  const bool tc = !f32_inputs(prec);   // BF16/FP16: 256 x 256 two-issuer tensor path
+  p->MI = p->MJ = tc ? kMacroTC : kMacroF32;
   p->GM = (BM + p->MI - 1) / p->MI;
   p->GN = (BN + p->MJ - 1) / p->MJ;
+  p->NC = (BK + kChunk - 1) / kChunk;
   p->device = dev;
   p->row_begin_macro = 0;
   p->row_end_macro = p->GM;
@@ -226,72 +235,41 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     st = alloc(reinterpret_cast<void**>(&p->field), sizeof(type) * static_cast<size_t>(count));
   ALLOC(nA, double, BM * BK);
   ALLOC(nBt, double, BN * BK);
-  ALLOC(V, int64_t, nleaf + 1);
-  ALLOC(U, int64_t, nmac + 1);
+  ALLOC(pyr, double, 2 * (p->GM + p->GN) * p->NC);
+  ALLOC(V, int64_t, nleaf);
   ALLOC(leaf_start, int64_t, nleaf);
+  ALLOC(U, int64_t, nmac + 1);
   ALLOC(L, int64_t, nmac + 1);
-  ALLOC(leaf_base, int64_t, nmac + 1);
-  ALLOC(macro_ptr, int64_t, nmac + 1);
   ALLOC(row_work, int64_t, BM + BK + 4);
   ALLOC(ticket, unsigned int, 1);
   ALLOC(sched, unsigned int, 4);   // [0] tile claims, [1] zero-fill unit claims
   ALLOC(order, int32_t, nmac);
   ALLOC(bucket_pos, int64_t, BK + 2);
+  ALLOC(mstart, int64_t, nmac);
+  ALLOC(d_range, int64_t, kRangeWords);
+  // macro lists at their worst case (macro-tile t owns entries [t*BK, t*BK + U[t])): the skip map
+  // is one stream-ordered pass with no host synchronisation
+  ALLOC(macro_ent, uint8_t, static_cast<size_t>(tc ? 16 : 8) * static_cast<size_t>(nmac * BK));
+  if (tc) ALLOC(macro_run, uint4, 2 * nmac * BK);   // one 4 x 8 run entry per 128-row half and k-step
 #undef ALLOC
-  if (st == SPAMM_OK && cudaMemset(p->V, 0, sizeof(int64_t) * (nleaf + 1)) != cudaSuccess)
-    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
-  if (st == SPAMM_OK && cudaMemset(p->U, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess)
-    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
-  if (st == SPAMM_OK && cudaMemset(p->L, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess)
-    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
-  if (st == SPAMM_OK && cudaMemset(p->ticket, 0, sizeof(unsigned int)) != cudaSuccess)
-    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
   if (st == SPAMM_OK) {
     p->hist = p->row_work + BM;
     p->totals = p->hist + BK + 2;
   }
+  if (st == SPAMM_OK && (cudaMemset(p->U, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||
+                         cudaMemset(p->L, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||
+                         cudaMemset(p->ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
+                         cudaMemset(p->sched, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
+                         cudaMemset(p->row_work, 0, sizeof(int64_t) * (BM + BK + 4)) != cudaSuccess))
+    st = fail(SPAMM_E_CUDA, "cudaMemset failed");
   if (st == SPAMM_OK) {
-    p->cub_tmp_bytes = skipmap_cub_bytes(nleaf, nmac);
-    st = alloc(&p->cub_tmp, p->cub_tmp_bytes);
+    std::vector<int64_t> h(static_cast<size_t>(nmac));
+    for (int64_t t = 0; t < nmac; ++t) h[static_cast<size_t>(t)] = t * BK;
+    if (cudaMemcpy(p->mstart, h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      st = fail(SPAMM_E_CUDA, "cudaMemcpy failed");
   }
-  // macro lists: worst case GM*GN*BK entries (8 B each) -- small relative to A and B
-  if (st == SPAMM_OK) {
-    p->macro_cap = nmac * BK;
-    // (k, mask) entries: 8 bytes, or 16 bytes (k, mask_lo, mask_hi, 0) for 8 x 8 macro-tiles
-    st = alloc(reinterpret_cast<void**>(&p->macro_ent), (p->dual ? 16 : 8) * static_cast<size_t>(p->macro_cap));
-    // tensor-path entries: one uint4 per k-step, two (one per 128-row half) for 8 x 8 macro-tiles
-    if (st == SPAMM_OK && !f32_inputs(prec))
-      st = alloc(reinterpret_cast<void**>(&p->macro_run),
-                 sizeof(uint4) * static_cast<size_t>(p->macro_cap) * (p->dual ? 2 : 1));
-  }
-  // fixed regions (single-pass skip map into worst-case macro-list regions) unless SYNC_SKIPMAP;
-  // the per-C-tile lists (2 B per C tile and k: 17 GB at N = 65536) are reserved when first asked
-  // for (spamm_get_skipmap / spamm_get_counts), and eagerly when that is under kWorstCaseBudget
-  if (st == SPAMM_OK && !(flags & SPAMM_FLAG_SYNC_SKIPMAP)) {
-    p->fixed_regions = true;
-    const size_t worst = sizeof(uint16_t) * static_cast<size_t>(nleaf) * static_cast<size_t>(BK);
-    if (worst <= kWorstCaseBudget) st = ensure_leaf_capacity(*p, nleaf * BK);
-  }
-  // macro-tile t's entries start at t*BK (fixed regions) or at the scanned offset macro_ptr[t]
-  if (st == SPAMM_OK) {
-    if (p->fixed_regions) {
-      st = alloc(reinterpret_cast<void**>(&p->mstart), sizeof(int64_t) * static_cast<size_t>(nmac));
-      if (st == SPAMM_OK) {
-        std::vector<int64_t> h(static_cast<size_t>(nmac));
-        for (int64_t t = 0; t < nmac; ++t) h[static_cast<size_t>(t)] = t * BK;
-        if (cudaMemcpy(p->mstart, h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-          st = fail(SPAMM_E_CUDA, "cudaMemcpy failed");
-      }
-    } else {
-      p->mstart = p->macro_ptr;
-    }
-  }
-  if (st == SPAMM_OK) {
-    if (p->fixed_regions && !f32_inputs(prec) && umma_variant_wide(p->umma_variant))
-      st = alloc(reinterpret_cast<void**>(&p->Uw), sizeof(int64_t) * static_cast<size_t>(nmac + 1));
-    else
-      p->Uw = p->U;
-  }
+  if (st == SPAMM_OK && sizeof(uint16_t) * static_cast<size_t>(nleaf) * static_cast<size_t>(BK) <= kLeafEagerBudget)
+    st = ensure_leaf_storage(*p);
   // FP32X3: the three bfloat16 planes of A and of B (leading dimensions rounded to 8 elements
   // so every row is 16-byte aligned for TMA)
   if (st == SPAMM_OK && prec == SPAMM_FP32X3) {
@@ -300,8 +278,6 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     st = alloc(reinterpret_cast<void**>(&p->planes),
                sizeof(uint16_t) * 3 * (static_cast<size_t>(M * p->ldpa) + static_cast<size_t>(K * p->ldpb)));
   }
-  if (st == SPAMM_OK && cudaMallocHost(reinterpret_cast<void**>(&p->h_totals), 2 * sizeof(int64_t)) != cudaSuccess)
-    st = fail(SPAMM_E_NOMEM, "cudaMallocHost failed");
   if (st == SPAMM_OK) {
     for (auto& e : p->ev)
       if (cudaEventCreate(&e) != cudaSuccess) st = fail(SPAMM_E_CUDA, "cudaEventCreate failed");
@@ -320,8 +296,10 @@ spamm_status spamm_plan(spamm_plan_t* p, int64_t N, int32_t tile, double tau, sp
 
 spamm_status spamm_plan_destroy(spamm_plan_t h) {
   if (!h) return SPAMM_OK;
-  cudaDeviceSynchronize();
-  free_plan(reinterpret_cast<Plan*>(h));
+  Plan* p = reinterpret_cast<Plan*>(h);
+  // the plan's work is ordered on the stream of its last call: wait for it, not for the device
+  if (p->last_stream != nullptr || p->norms_ready) cudaStreamSynchronize(p->last_stream);
+  free_plan(p);
   return SPAMM_OK;
 }
 
@@ -347,53 +325,51 @@ spamm_status spamm_set_scalars(spamm_plan_t h, double alpha, double beta) {
 
 namespace spamm {
 
-// stage 1 over tile rows [ar0, ar1) of A and tile columns [bj0, bj1) of B
-spamm_status do_norms_range(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t ar0,
-                            int64_t ar1, int64_t bj0, int64_t bj1, cudaStream_t s) {
+// stage 1 over tile rows [ar0, ar1) of A and tile columns [bj0, bj1) of B; with zero_ws the norm
+// kernel also zeroes the skip map's counters (saves a memset node in spamm_run)
+static spamm_status norms_impl(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t ar0,
+                               int64_t ar1, int64_t bj0, int64_t bj1, bool zero_ws, cudaStream_t s) {
   SPAMM_TRY(check_matrix(A, p.M, p.K, lda, esize_of(p.prec), "A"));
   SPAMM_TRY(check_matrix(B, p.K, p.N, ldb, esize_of(p.prec), "B"));
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[0], s));
   // A (M x K): tile row i, tile col k -> nA[i*BK + k];  B (K x N) column strip [bj0*T, bj1*T):
   // tile row k, tile col j -> nBt[j*BK + k]
-  SPAMM_TRY(launch_norms2(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s));
-  p.ws_zeroed = p.zero_ws_next;
+  p.zero_ws_next = zero_ws;
+  const spamm_status st = launch_norms2(p, A, lda, ar0, ar1, B, ldb, bj0, bj1, s);
   p.zero_ws_next = false;
+  SPAMM_TRY(st);
+  p.ws_zeroed = zero_ws;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[1], s));
   p.ev_norms = timing;
   p.norms_ready = true;
+  p.pyr_ready = false;
   p.skipmap_ready = false;
   p.last_stream = s;
   return SPAMM_OK;
 }
 
-spamm_status do_norms(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t s) {
-  return do_norms_range(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, s);
+spamm_status do_norms_range(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t ar0,
+                            int64_t ar1, int64_t bj0, int64_t bj1, cudaStream_t s) {
+  return norms_impl(p, A, lda, B, ldb, ar0, ar1, bj0, bj1, false, s);
 }
 
-spamm_status do_skipmap(Plan& p, int64_t gi0, int64_t gi1, cudaStream_t s) {
+static spamm_status do_skipmap(Plan& p, cudaStream_t s) {
   if (!p.norms_ready) return fail(SPAMM_E_STATE, "spamm_build_skipmap before spamm_norms");
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
-  p.leaf_ready = false;
-  if (p.fixed_regions) {
-    SPAMM_TRY(launch_skipmap_fused(p, gi0, gi1, s));
-  } else {
-    p.leaf_ready = true;   // the emit pass writes the per-C-tile lists itself
-    SPAMM_TRY(launch_skipmap_count(p, gi0, gi1, s));
-    if (p.leaf_cap < p.BM * p.BN * p.BK) {
-      // exact sizing: one stream synchronisation
-      SPAMM_CUDA_TRY(cudaMemcpyAsync(p.h_totals, p.leaf_base + p.GM * p.GN, sizeof(int64_t),
-                                     cudaMemcpyDeviceToHost, s));
-      SPAMM_CUDA_TRY(cudaStreamSynchronize(s));
-      SPAMM_TRY(ensure_leaf_capacity(p, std::max<int64_t>(p.h_totals[0], 1)));
-    }
-    SPAMM_TRY(launch_skipmap_emit(p, gi0, gi1, s));
-  }
+  if (!p.pyr_ready) SPAMM_TRY(launch_pyramid(p, s));
+  // row_work [BM], hist [BK+2] and totals [2] are contiguous in one allocation
+  if (!p.ws_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 4), s));
+  p.ws_zeroed = false;
+  SPAMM_TRY(launch_skipmap(p, 0, p.GM, false, true, true, s));
+  p.sched_zeroed = true;   // the last CTA zeroes the multiply's claim counters
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[3], s));
   p.ev_skip = timing;
-  p.row_begin_macro = gi0;
-  p.row_end_macro = gi1;
+  p.leaf_ready = false;
+  p.range_on_device = false;
+  p.row_begin_macro = 0;
+  p.row_end_macro = p.GM;
   p.skipmap_ready = true;
   p.last_stream = s;
   return SPAMM_OK;
@@ -404,7 +380,7 @@ spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int
   if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "spamm_multiply before spamm_build_skipmap");
   SPAMM_TRY(check_matrix(A, p.M, p.K, lda, esize_of(p.prec), "A"));
   SPAMM_TRY(check_matrix(B, p.K, p.N, ldb, esize_of(p.prec), "B"));
-  SPAMM_TRY(check_matrix(C, p.M, p.N, ldc, 4, "C"));
+  if (!p.out_low_only) SPAMM_TRY(check_matrix(C, p.M, p.N, ldc, 4, "C"));
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[4], s));
   if (p.prec == SPAMM_FP32X3) {
@@ -413,10 +389,7 @@ spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int
     SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
                                    s));
   } else {
-    if (p.dual)
-      SPAMM_TRY(launch_multiply_dual(p, A, lda, B, ldb, C, ldc, s));
-    else
-      SPAMM_TRY(launch_multiply_umma(p, A, lda, B, ldb, C, ldc, s));
+    SPAMM_TRY(launch_multiply_dual(p, A, lda, B, ldb, C, ldc, s));
   }
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[5], s));
   p.ev_mul = timing;
@@ -431,13 +404,13 @@ extern "C" {
 spamm_status spamm_norms(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, void* stream) {
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
-  return do_norms(p, A, lda, B, ldb, static_cast<cudaStream_t>(stream));
+  return norms_impl(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, false, static_cast<cudaStream_t>(stream));
 }
 
 spamm_status spamm_build_skipmap(spamm_plan_t h, void* stream) {
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
-  return do_skipmap(p, 0, p.GM, static_cast<cudaStream_t>(stream));
+  return do_skipmap(p, static_cast<cudaStream_t>(stream));
 }
 
 spamm_status spamm_multiply(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
@@ -445,10 +418,10 @@ spamm_status spamm_multiply(spamm_plan_t h, const void* A, int64_t lda, const vo
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags & ~SPAMM_MUL_AUTO) return fail(SPAMM_E_INVALID, "unknown spamm_multiply flag");
   if (flags & SPAMM_MUL_AUTO) {
-    p.zero_ws_next = p.fixed_regions;   // the norm kernel zeroes the skip map's counters
-    SPAMM_TRY(do_norms(p, A, lda, B, ldb, s));
-    SPAMM_TRY(do_skipmap(p, 0, p.GM, s));
+    SPAMM_TRY(norms_impl(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, true, s));
+    SPAMM_TRY(do_skipmap(p, s));
   }
   return do_multiply(p, A, lda, B, ldb, C, ldc, s);
 }
@@ -458,24 +431,33 @@ spamm_status spamm_multiply_chain(spamm_plan_t h, const void* A, int64_t lda, co
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags & ~(SPAMM_MUL_AUTO | SPAMM_MUL_OUTPUT_NORMS | SPAMM_MUL_LOW_ONLY))
+    return fail(SPAMM_E_INVALID, "unknown spamm_multiply_chain flag");
+  const bool low_only = (flags & SPAMM_MUL_LOW_ONLY) != 0;
   if (C_low != nullptr) {
     if (f32_inputs(p.prec)) return fail(SPAMM_E_INVALID, "C_low is for BF16/FP16 plans (FP32 C is the next input)");
     SPAMM_TRY(check_matrix(C_low, p.M, p.N, ldcl, 2, "C_low"));
+  }
+  if (low_only) {
+    if (C_low == nullptr) return fail(SPAMM_E_INVALID, "SPAMM_MUL_LOW_ONLY needs C_low");
+    if (p.beta != 0.0) return fail(SPAMM_E_INVALID, "SPAMM_MUL_LOW_ONLY needs beta = 0 (no FP32 C to read)");
   }
   if (p.prec == SPAMM_FP32X3) return fail(SPAMM_E_UNSUPPORTED, "chained outputs: FP32, BF16, FP16 only");
   if ((flags & SPAMM_MUL_OUTPUT_NORMS) && !p.nC)
     SPAMM_TRY(alloc(reinterpret_cast<void**>(&p.nC), sizeof(double) * static_cast<size_t>(p.BM * p.BN)));
   if (flags & SPAMM_MUL_AUTO) {
-    SPAMM_TRY(do_norms(p, A, lda, B, ldb, s));
-    SPAMM_TRY(do_skipmap(p, 0, p.GM, s));
+    SPAMM_TRY(norms_impl(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, true, s));
+    SPAMM_TRY(do_skipmap(p, s));
   }
   p.out_norms = (flags & SPAMM_MUL_OUTPUT_NORMS) != 0;
   p.out_low = C_low;
   p.out_ldl = ldcl;
-  const spamm_status st = do_multiply(p, A, lda, B, ldb, C, ldc, s);
+  p.out_low_only = low_only;
+  const spamm_status st = do_multiply(p, A, lda, B, ldb, low_only ? nullptr : C, ldc, s);
   p.nc_ready = st == SPAMM_OK && p.out_norms;
   p.out_norms = false;
   p.out_low = nullptr;
+  p.out_low_only = false;
   return st;
 }
 
@@ -501,6 +483,7 @@ spamm_status spamm_set_norms(spamm_plan_t h, const double* nA, const double* nB,
   SPAMM_CUDA_TRY(cudaMemcpyAsync(p.nA, nA, sizeof(double) * static_cast<size_t>(p.BM * p.BK), cudaMemcpyDeviceToDevice, s));
   SPAMM_TRY(launch_transpose_f64(nB, p.BK, p.BN, p.nBt, s));   // nB [BK][BN] -> nB^T [BN][BK]
   p.norms_ready = true;
+  p.pyr_ready = false;
   p.skipmap_ready = false;
   p.b_is_a = false;
   p.last_stream = s;
@@ -524,11 +507,12 @@ spamm_status spamm_get_norms(spamm_plan_t h, const double** dA, const double** d
   return p.norms_ready ? SPAMM_OK : fail(SPAMM_E_STATE, "norms not computed");
 }
 
-// The fused skip-map pass writes the macro-level lists only; the per-C-tile view is
-// expanded from them on first request (same stream, then synchronised).
+// The skip map writes the macro-level lists only; the per-C-tile view is expanded from them on
+// first request (same stream, then synchronised).
 static spamm_status ensure_leaf_lists(spamm::Plan& p) {
   if (p.leaf_ready) return SPAMM_OK;
-  if (p.fixed_regions) SPAMM_TRY(ensure_leaf_capacity(p, p.BM * p.BN * p.BK));
+  SPAMM_TRY(sync_range(p));
+  SPAMM_TRY(ensure_leaf_storage(p));
   SPAMM_TRY(launch_leaf_expand(p, p.last_stream));
   SPAMM_CUDA_TRY(cudaStreamSynchronize(p.last_stream));
   p.leaf_ready = true;
@@ -565,6 +549,7 @@ spamm_status spamm_get_macro(spamm_plan_t h, const int64_t** d_start, const int6
   if (!h) return fail(SPAMM_E_INVALID, "plan is NULL");
   Plan& p = *reinterpret_cast<Plan*>(h);
   if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "skip map not built");
+  SPAMM_TRY(sync_range(p));
   if (d_start) *d_start = p.mstart;
   if (d_count) *d_count = p.U;
   if (d_entries) *d_entries = reinterpret_cast<const uint32_t*>(p.macro_ent);
@@ -577,6 +562,7 @@ spamm_status spamm_get_macro(spamm_plan_t h, const int64_t** d_start, const int6
 spamm_status spamm_get_partition(spamm_plan_t h, int64_t* row_begin, int nranks) {
   if (!h || !row_begin) return fail(SPAMM_E_INVALID, "NULL argument");
   Plan& p = *reinterpret_cast<Plan*>(h);
+  SPAMM_TRY(sync_range(p));
   if (static_cast<int>(p.last_partition.size()) != nranks + 1)
     return fail(SPAMM_E_STATE, "no partition for this rank count");
   std::memcpy(row_begin, p.last_partition.data(), sizeof(int64_t) * (nranks + 1));
@@ -586,6 +572,7 @@ spamm_status spamm_get_partition(spamm_plan_t h, int64_t* row_begin, int nranks)
 spamm_status spamm_get_stats(spamm_plan_t h, spamm_stats* out) {
   if (!h || !out) return fail(SPAMM_E_INVALID, "NULL argument");
   Plan& p = *reinterpret_cast<Plan*>(h);
+  SPAMM_TRY(sync_range(p));
   std::memset(out, 0, sizeof(*out));
   out->M = p.M;
   out->N = p.N;
@@ -618,19 +605,20 @@ spamm_status spamm_get_stats(spamm_plan_t h, spamm_stats* out) {
 spamm_status spamm_partition_rows(const int64_t* row_work, int64_t BM, int nranks, int64_t* row_begin) {
   if (!row_work || !row_begin) return fail(SPAMM_E_INVALID, "NULL argument");
   if (BM <= 0 || nranks <= 0) return fail(SPAMM_E_INVALID, "BM and nranks must be positive");
-  // prefix sums; cut r is the first row whose exclusive prefix reaches r*total/nranks
-  long double total = 0;
+  // cut r = first row i whose exclusive prefix `pre` reaches the r-th share by half of its own
+  // work:  pre + w_i / 2 >= r * total / n  <=>  2 n pre + n w_i >= 2 r total  (integers: the
+  // device partition of spamm_multiply_mgpu applies the identical rule to macro rows)
+  int64_t total = 0;
   for (int64_t i = 0; i < BM; ++i) {
     if (row_work[i] < 0) return fail(SPAMM_E_INVALID, "negative row work");
-    total += static_cast<long double>(row_work[i]);
+    total += row_work[i];
   }
+  const int64_t n = nranks;
   row_begin[0] = 0;
-  long double pre = 0;
-  int64_t i = 0;
+  int64_t pre = 0, i = 0;
   for (int r = 1; r < nranks; ++r) {
-    const long double target = total * r / nranks;
-    while (i < BM && pre + static_cast<long double>(row_work[i]) / 2 < target) {
-      pre += static_cast<long double>(row_work[i]);
+    while (i < BM && 2 * n * pre + n * row_work[i] < 2 * static_cast<int64_t>(r) * total) {
+      pre += row_work[i];
       ++i;
     }
     row_begin[r] = std::max<int64_t>(i, row_begin[r - 1]);

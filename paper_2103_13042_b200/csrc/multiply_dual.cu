@@ -47,17 +47,14 @@ constexpr int kDBSlot = 32 * 256 * 2;                 // B[32 x 256] as eight [3
 constexpr int kDStepBytes = kDASlot + kDBSlot;        // one 32-deep k-step
 constexpr int kDThreads = 384;   // w0 A/claims, w1-2 MMA, w3 B, w4-11 epilogue
 constexpr int kDTQ = 4;                               // tile ring depth
-constexpr int64_t kMaxSplit = 148;
-constexpr int64_t kOrdS = 12;                         // blocked claim order: super-block side (tiles)                    // k-split tiles per launch (scratch: 256 KB each)
-// kPack k-steps of one macro-tile per ring stage (one wait / commit per stage for the issuers);
-// the ring holds 6 k-steps either way (192 KB)
-template <int kPack>
-struct DCfg {
-  static constexpr int kStages = 6 / kPack;
-  static constexpr int kStageBytes = kPack * kDStepBytes;
-  // align slack, stages, zero atom, barriers + entry batches + tile ring
-  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 1024 + 4096;
-};
+constexpr int64_t kOrdS = 12;                         // blocked claim order: super-block side (tiles)
+// kPack = 2 k-steps of one macro-tile per ring stage (one wait / commit per stage for the issuers;
+// measured 174 -> 165 us against one per stage, r01e); the ring holds 6 k-steps (192 KB)
+constexpr int kPack = 2;
+constexpr int kDStages = 6 / kPack;
+constexpr int kDStageBytes = kPack * kDStepBytes;
+// align slack, stages, zero atom, barriers + entry batches + tile ring
+constexpr size_t kDSmem = 1024 + static_cast<size_t>(kDStages) * kDStageBytes + 1024 + 4096;
 
 constexpr uint32_t kFullRun = 0u | (7u << 3) | (15u << 6);
 constexpr uint32_t kFirst = 1u << 29, kLast = 1u << 30, kNoStep = 1u << 28, kEnd = 1u << 27;
@@ -66,8 +63,6 @@ constexpr uint32_t kWideSt = 1u << 25;
 
 struct DTile {
   int64_t t, e0, e1;   // macro-tile, k-step range [e0, e1) (in k-steps, entry pairs)
-  int64_t part;        // 0 whole tile; 1 / 2 first / second half of a k-split tile (C = P1 + P2)
-  int64_t slot;        // k-split tiles: index into the handshake counters and the partial scratch
 };
 
 // warp-uniform copy of lane 0's value (lets the compiler keep MMA operands in uniform registers)
@@ -92,32 +87,26 @@ struct DChain {
   int64_t ldn;
   void* clow;
   int64_t ldl;
+  int low_only;   // SPAMM_MUL_LOW_ONLY: C_low is the only output (no FP32 C stores)
 };
 
-template <uint32_t kFmt, bool kGen, int kPack>
+template <uint32_t kFmt, bool kGen>
 __global__ void __launch_bounds__(kDThreads, 1)
     spamm_mul_dual_kernel(const __grid_constant__ DMaps mp, const int64_t* __restrict__ mstart,
                           const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
-                          const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ n_empty_p, int64_t GN,
+                          const int32_t* __restrict__ order, int64_t n_tiles, int64_t t0,
+                          const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
-                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int dbg, int zf_per_wait, int wide_ok,
-                          unsigned int* __restrict__ split_cnt, float* __restrict__ split_scr, int64_t split_req,
-                          int order_mode, int64_t t0, int use3d) {
+                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int use3d) {
+  if (rng != nullptr) {   // multi-GPU: the macro-row range was decided on the device
+    t0 = rng[0] * GN;
+    n_tiles = (rng[1] - rng[0]) * GN;
+  }
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
-  // claim order: LPT (descending k-steps), or blocked when every CTA gets many tiles (order_mode:
-  // 0 = blocked if n_work >= 16 x grid, 1 = LPT, 2 = blocked)
-  const bool row_order = order_mode == 2 || (order_mode == 0 && n_work >= 16 * static_cast<int64_t>(gridDim.x));
-  // k-split tail (plain epilogue only): split_req < 0 = the last (n_work mod grid) tiles
-  int64_t n_split = 0;
-  if (!kGen && split_cnt != nullptr) {
-    if (split_req >= 0)
-      n_split = split_req < n_work ? split_req : n_work;
-    else if (n_work > static_cast<int64_t>(gridDim.x))
-      n_split = n_work % static_cast<int64_t>(gridDim.x);
-    if (n_split > kMaxSplit) n_split = kMaxSplit;
-  }
-  constexpr int kDStages = DCfg<kPack>::kStages, kDStageBytes = DCfg<kPack>::kStageBytes;
+  // claim order: LPT (descending k-steps), or blocked when every CTA gets many tiles
+  const bool row_order = n_work >= 16 * static_cast<int64_t>(gridDim.x);
+  constexpr int wide_ok = 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sZero = smem + kDStages * kDStageBytes;    // 1 KB zeros: MMA zero atom, bulk zero-fill source
@@ -174,7 +163,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
   // compete with the operand loads' first DRAM touches (multiply 165 vs 152 us without them).
   const int64_t n_units = n_empty * 8;
   auto zero_unit = [&]() -> bool {
-    if (dbg & 1) return false;   // dbg 1: no zero-fill (timing experiments only)
     unsigned int u32 = 0;
     if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
     const int64_t u = __shfl_sync(0xffffffffu, u32, 0);
@@ -201,11 +189,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
     int tq_s = 0;
     uint32_t tq_ph = 0;
     auto claim = [&]() -> DTile {
-      DTile d{-1, 0, 0, 0, 0};
+      DTile d{-1, 0, 0};
       unsigned int idx = 0;
       if (lane == 0) idx = atomicAdd(sched, 1u);
       idx = __shfl_sync(0xffffffffu, idx, 0);
-      const int64_t n_whole = n_work - n_split;
       if (row_order) {
         // many tiles per CTA: balance comes for free, so claim in a blocked tile order (kOrdS x kOrdS
         // super-blocks row-major, tiles row-major inside; empty tiles skipped): the ~grid tiles in
@@ -230,19 +217,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
           idx = __shfl_sync(0xffffffffu, idx, 0);
         }
       }
-      if (static_cast<int64_t>(idx) < n_whole) {
+      if (static_cast<int64_t>(idx) < (n_empty_p ? n_work : n_tiles)) {
         d.t = order[idx];
         d.e0 = mstart[d.t];
         d.e1 = d.e0 + mcount[d.t];
-      } else if (static_cast<int64_t>(idx) < n_whole + 2 * n_split) {
-        // the LPT tail's last n_split tiles in k-halves, both halves claimed back to back
-        const int64_t j = static_cast<int64_t>(idx) - n_whole;
-        d.t = order[n_whole + j / 2];
-        d.part = 1 + (j & 1);
-        d.slot = j / 2;
-        const int64_t e0 = mstart[d.t], cnt = mcount[d.t], mid = e0 + (cnt + 1) / 2;
-        d.e0 = d.part == 1 ? e0 : mid;
-        d.e1 = d.part == 1 ? mid : e0 + cnt;
       }
       return d;
     };
@@ -600,38 +578,12 @@ __global__ void __launch_bounds__(kDThreads, 1)
       if (cur.t < 0) break;
       const int64_t I = cur.t / GN, J = cur.t % GN;
       const unsigned long long tw = prof ? clock64() : 0;
-      // while the accumulator fills: at most zf_per_wait zero-fill units (spread over the kernel
-      // instead of a burst at its start), the remainder after the last tile
-      for (int z = 0; z < zf_per_wait && !mbar_try_wait(&tfull[h], par); ++z)
-        if (!zero_unit()) break;
       mbar_wait(&tfull[h], par);
       par ^= 1;
       if (prof && warp == 4 && lane == 0) prof[blockIdx.x * 16 + 12] += clock64() - tw;
       tc_fence_after();
       const uint32_t tq_addr = tbase + 256u * static_cast<uint32_t>(h);
-      // k-split halves: per warp slice (32 rows x 256 columns), the first half to get here parks
-      // its partial in scratch; the second waits only for that write, adds (P1 + P2 = P2 + P1
-      // exactly, so the result does not depend on which half came first) and stores C
-      bool split_first = false;
-      unsigned int* scnt = nullptr;
-      float* sscr = nullptr;
-      if (cur.part != 0) {
-        const int slice = h * 4 + q;
-        scnt = split_cnt + (cur.slot * 8 + slice) * 2;
-        sscr = split_scr + (cur.slot * 8 + slice) * (32 * 256);
-        unsigned int old = 0;
-        if (lane == 0) old = atomicAdd(scnt, 1u);
-        split_first = __shfl_sync(0xffffffffu, old, 0) == 0u;
-        if (!split_first) {
-          if (lane == 0) {
-            const volatile unsigned int* d = scnt + 1;
-            while (*d == 0u) __nanosleep(64);
-          }
-          __syncwarp();
-          __threadfence();
-        }
-      }
-      if (kGen) {
+      if constexpr (kGen) {
         double tsum[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // C tiles (I*8 + 4h + q, J*8 + c)
 #pragma unroll 1
         for (int hh = 0; hh < 8; ++hh) {
@@ -651,7 +603,9 @@ __global__ void __launch_bounds__(kDThreads, 1)
               float* cp = C + row * ldc + col;
               float2 x = make_float2(__uint_as_float(v[4 * i + 2 * rr]), __uint_as_float(v[4 * i + 2 * rr + 1]));
               const bool two = col + 1 < N;
-              if (two) {
+              if (co.low_only) {   // alpha only (beta = 0 is required): no FP32 C exists
+                x = make_float2(ab.alpha * x.x, two ? ab.alpha * x.y : 0.f);
+              } else if (two) {
                 x = axpby2(ab, x, cp);
                 __stcs(reinterpret_cast<float2*>(cp), x);
               } else {
@@ -692,8 +646,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
             if (lane == 0 && ti * 32 < M && tj * 32 < N) co.nC[ti * co.ldn + tj] = sqrt(x);
           }
         }
-        continue;
-      }
+      } else {
 #pragma unroll 1
       for (int hh = 0; hh < 8; ++hh) {
         const int lh = hh & 1;                // lanes [16*lh, 16*lh + 16) of the quadrant
@@ -714,20 +667,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
           float* cb = C + rb * ldc + col;
           float2 pa = make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
           float2 pb = make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-          if (dbg & 2) continue;   // dbg 2: no C stores (timing experiments only)
-          if (cur.part != 0) {
-            const int r = 16 * lh + t1, cc = c0 + 8 * i + 2 * t0;   // within the warp's slice
-            float2* sa = reinterpret_cast<float2*>(sscr + r * 256 + cc);
-            float2* sb = reinterpret_cast<float2*>(sscr + (r + 8) * 256 + cc);
-            if (split_first) {
-              __stcg(sa, pa);
-              __stcg(sb, pb);
-              continue;
-            }
-            const float2 oa = __ldcg(sa), ob = __ldcg(sb);
-            pa = make_float2(oa.x + pa.x, oa.y + pa.y);
-            pb = make_float2(ob.x + pb.x, ob.y + pb.y);
-          }
           if (col + 1 < N) {
             if (ra < M) __stcs(reinterpret_cast<float2*>(ca), pa);
             if (rb < M) __stcs(reinterpret_cast<float2*>(cb), pb);
@@ -737,18 +676,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
           }
         }
       }
-      if (cur.part != 0) {
-        if (split_first) {   // the partial is visible: release the second half
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) atomicExch(scnt + 1, 1u);
-        } else {             // both halves are done with this slot: reset it for the next launch
-          __syncwarp();
-          if (lane == 0) {
-            scnt[0] = 0u;
-            scnt[1] = 0u;
-          }
-        }
       }
     }
     if (tl && warp == 4 && lane == 0) stamp(3);
@@ -763,7 +690,39 @@ __global__ void __launch_bounds__(kDThreads, 1)
   if (tl && threadIdx.x == 0) stamp(5);
 }
 
-template <uint32_t kFmt, bool kGen, int kPack>
+#ifdef SPAMM_PROFILE
+// per-CTA issuer counters and a globaltimer timeline (compile with -DSPAMM_PROFILE)
+static void print_profile(const unsigned long long* hp, int grid) {
+  double a[16] = {0};
+  double mx = 0, mn = 1e30;
+  for (int c = 0; c < grid; ++c) {
+    for (int k = 0; k < 16; ++k) a[k] += static_cast<double>(hp[c * 16 + k]) / grid;
+    mx = std::max(mx, static_cast<double>(hp[c * 16]));
+    mn = std::min(mn, static_cast<double>(hp[c * 16]));
+  }
+  for (int h = 0; h < 2; ++h)
+    fprintf(stderr, "[dual prof] issuer %d cycles/CTA %.0f (min %.0f max %.0f): full-wait %.0f tmem-empty %.0f "
+            "mma %.0f commit %.0f stages %.0f\n", h, a[6 * h], mn, mx, a[6 * h + 1], a[6 * h + 2], a[6 * h + 3],
+            a[6 * h + 4], a[6 * h + 5]);
+  fprintf(stderr, "[dual prof] epilogue warp 4 tmem-full wait %.0f; issuer 0 full-wait in a tile's first 3 stages %.0f\n",
+          a[12], a[13]);
+  const unsigned long long* t = hp + 1024 * 16;
+  unsigned long long g0 = ~0ull;
+  for (int c = 0; c < grid; ++c) g0 = std::min(g0, t[c * 8]);
+  double m[6] = {0}, mxs[6] = {0};
+  for (int c = 0; c < grid; ++c)
+    for (int k = 0; k < 6; ++k) {
+      const double v = (static_cast<double>(t[c * 8 + k]) - static_cast<double>(g0)) * 1e-3;
+      m[k] += v / grid;
+      mxs[k] = std::max(mxs[k], v);
+    }
+  fprintf(stderr, "[dual tl] us from first CTA start (mean / max): start %.1f/%.1f prologue %.1f/%.1f issuer-done %.1f/%.1f "
+          "last-drain %.1f/%.1f zero-fill-done %.1f/%.1f cta-end %.1f/%.1f\n", m[0], mxs[0], m[1], mxs[1], m[2], mxs[2],
+          m[3], mxs[3], m[4], mxs[4], m[5], mxs[5]);
+}
+#endif
+
+template <uint32_t kFmt, bool kGen>
 spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                            cudaStream_t s, CUtensorMapDataType dt) {
   DMaps mp;
@@ -782,96 +741,37 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
     SPAMM_TRY(encode_tmap_2d(&mp.b2d1, dt, 2, B, p.N, p.K, ldb, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
     SPAMM_TRY(encode_tmap_2d(&mp.b2d2, dt, 2, B, p.N, p.K, ldb, 32, 64, CU_TENSOR_MAP_SWIZZLE_64B));
   }
-  auto kern = spamm_mul_dual_kernel<kFmt, kGen, kPack>;
-  constexpr size_t kDSmem = DCfg<kPack>::kSmem;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDSmem)));
-    attr_set = true;
-  }
-  const int64_t n_tiles = (p.row_end_macro - p.row_begin_macro) * p.GN;
-  if (n_tiles <= 0) return SPAMM_OK;
+  auto kern = spamm_mul_dual_kernel<kFmt, kGen>;
+  SPAMM_SET_SMEM(kern, static_cast<int>(kDSmem), p.device);
+  // range: host-known for single-GPU calls, decided on the device for the multi-GPU partition
+  const int64_t n_tiles = p.range_on_device ? 0 : (p.row_end_macro - p.row_begin_macro) * p.GN;
+  if (!p.range_on_device && n_tiles <= 0) return SPAMM_OK;
   // the LPT order ends with the macro-tiles without kept pairs (hist[0] of them); with the
   // plain epilogue the epilogue warps zero-fill those, otherwise they go through the pipeline
   // (beta * C_old, chained norms)
-  const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
+  const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
   if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, 2 * sizeof(unsigned int), s));
   p.sched_zeroed = false;
-  // SPAMM_DEBUG_DUAL_MODE: timing experiments that break the result (bit 1: no zero-fill of empty tiles,
-  // bit 2: no C stores)
-  const int dbg = getenv("SPAMM_DEBUG_DUAL_MODE") ? atoi(getenv("SPAMM_DEBUG_DUAL_MODE")) : 0;
-  // tile claim order (SPAMM_DUAL_ORDER: 0 auto, 1 LPT, 2 blocked)
-  const int order_mode = getenv("SPAMM_DUAL_ORDER") ? atoi(getenv("SPAMM_DUAL_ORDER")) : 0;
-  // k-split of the LPT tail.s last tiles (SPAMM_DUAL_SPLIT=n tiles, -1 = n_work mod grid; default off)
-  const int64_t split_req = getenv("SPAMM_DUAL_SPLIT") ? atoll(getenv("SPAMM_DUAL_SPLIT")) : 0;   // measured slower (r01p)
-  if (split_req != 0 && !p.split_cnt) {   // [kMaxSplit][8 slices][arrived, done] counters + [kMaxSplit][8][32 x 256] partials
-    if (cudaMalloc(&p.split_cnt, sizeof(unsigned int) * kMaxSplit * 16) != cudaSuccess ||
-        cudaMalloc(&p.split_scr, sizeof(float) * kMaxSplit * 8 * 32 * 256) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(SPAMM_E_NOMEM, "k-split workspace");
-    }
-    SPAMM_CUDA_TRY(cudaMemsetAsync(p.split_cnt, 0, sizeof(unsigned int) * kMaxSplit * 16, s));
-  }
-  // stages of two consecutive k-steps load 64-deep boxes (SPAMM_DUAL_WIDE=0 disables)
-  const bool wide_ok = !getenv("SPAMM_DUAL_WIDE") || atoi(getenv("SPAMM_DUAL_WIDE")) != 0;
-  // zero-fill units an epilogue warp may take while waiting for one accumulator (SPAMM_DUAL_ZF)
-  const int zf_per_wait = getenv("SPAMM_DUAL_ZF") ? atoi(getenv("SPAMM_DUAL_ZF")) : 0;   // measured best: all at the end (r01k)
-  static unsigned long long* prof = nullptr;
-  if (getenv("SPAMM_DEBUG_UMMA_PROF") && !prof) cudaMalloc(&prof, 1024 * 24 * 8);
-  if (prof) cudaMemsetAsync(prof, 0, 1024 * 24 * 8, s);
-  kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, kGen ? nullptr : p.hist, p.GN, C, ldc, p.M,
-                                       p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                       DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl}, prof, dbg,
-                                       zf_per_wait, wide_ok && kPack == 2 ? 1 : 0, p.split_cnt, p.split_scr, split_req,
-                                       order_mode, p.row_begin_macro * p.GN, p.N % 32 == 0 ? 1 : 0);
+  unsigned long long* prof = nullptr;
+#ifdef SPAMM_PROFILE
+  static unsigned long long* prof_buf = nullptr;
+  if (!prof_buf) cudaMalloc(&prof_buf, 1024 * 24 * 8);
+  prof = prof_buf;
+  cudaMemsetAsync(prof, 0, 1024 * 24 * 8, s);
+#endif
+  kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, p.row_begin_macro * p.GN,
+                                       p.range_on_device ? p.d_range : nullptr, kGen ? nullptr : p.hist, p.GN, C, ldc,
+                                       p.M, p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
+                                       DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
+                                       prof, p.N % 32 == 0 ? 1 : 0);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
-  if (prof) {
-    static unsigned long long hp[1024 * 24];
-    cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    double a[16] = {0};
-    double mx = 0, mn = 1e30;
-    for (int c = 0; c < grid; ++c) {
-      for (int k = 0; k < 16; ++k) a[k] += static_cast<double>(hp[c * 16 + k]) / grid;
-      mx = std::max(mx, static_cast<double>(hp[c * 16]));
-      mn = std::min(mn, static_cast<double>(hp[c * 16]));
-    }
-    for (int h = 0; h < 2; ++h)
-      fprintf(stderr, "[dual prof] issuer %d cycles/CTA %.0f (min %.0f max %.0f): full-wait %.0f tmem-empty %.0f "
-              "mma %.0f commit %.0f stages %.0f\n", h, a[6 * h], mn, mx, a[6 * h + 1], a[6 * h + 2], a[6 * h + 3],
-              a[6 * h + 4], a[6 * h + 5]);
-    fprintf(stderr, "[dual prof] epilogue warp 4 tmem-full wait %.0f; issuer 0 full-wait in a tile's first 3 stages %.0f\n",
-            a[12], a[13]);
-    {
-      const unsigned long long* t = hp + 1024 * 16;
-      unsigned long long g0 = ~0ull;
-      for (int c = 0; c < grid; ++c) g0 = std::min(g0, t[c * 8]);
-      double m[6] = {0}, mx[6] = {0};
-      for (int c = 0; c < grid; ++c)
-        for (int k = 0; k < 6; ++k) {
-          const double v = (static_cast<double>(t[c * 8 + k]) - static_cast<double>(g0)) * 1e-3;
-          m[k] += v / grid;
-          mx[k] = std::max(mx[k], v);
-        }
-      fprintf(stderr, "[dual tl] us from first CTA start (mean / max): start %.1f/%.1f prologue %.1f/%.1f issuer-done %.1f/%.1f "
-              "last-drain %.1f/%.1f zero-fill-done %.1f/%.1f cta-end %.1f/%.1f\n", m[0], mx[0], m[1], mx[1], m[2], mx[2],
-              m[3], mx[3], m[4], mx[4], m[5], mx[5]);
-    }
-    if (getenv("SPAMM_DEBUG_UMMA_PROF_CTA")) {
-      double by_n[8] = {0}, cnt_n[8] = {0};
-      for (int c = 0; c < grid; ++c) {
-        const int nt = static_cast<int>(std::min<unsigned long long>(hp[c * 16 + 14], 7));
-        by_n[nt] += static_cast<double>(hp[c * 16]);
-        cnt_n[nt] += 1;
-      }
-      for (int n = 0; n < 8; ++n)
-        if (cnt_n[n] > 0) fprintf(stderr, "[dual cta] %d tiles: %.0f CTAs, mean issuer cycles %.0f\n", n, cnt_n[n], by_n[n] / cnt_n[n]);
-      for (int c = 0; c < grid; ++c)
-        fprintf(stderr, "[dual cta] cta %d sm %llu tiles %llu cycles %llu full %llu\n", c, hp[c * 16 + 15], hp[c * 16 + 14],
-                hp[c * 16], hp[c * 16 + 1]);
-    }
-  }
+#ifdef SPAMM_PROFILE
+  static unsigned long long hp[1024 * 24];
+  cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  print_profile(hp, grid);
+#endif
   return SPAMM_OK;
 }
 
@@ -880,19 +780,10 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
 spamm_status launch_multiply_dual(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s) {
   const bool gen = p.alpha != 1.0 || p.beta != 0.0 || p.out_norms || p.out_low != nullptr;
-  // k-steps per ring stage (SPAMM_DUAL_PACK=1|2, default 2)
-  const int pack = getenv("SPAMM_DUAL_PACK") && atoi(getenv("SPAMM_DUAL_PACK")) == 1 ? 1 : 2;
   const CUtensorMapDataType dt = p.prec == SPAMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  if (p.prec == SPAMM_BF16) {
-    if (gen) return pack == 1 ? launch_dual_t<1, true, 1>(p, A, lda, B, ldb, C, ldc, s, dt)
-                              : launch_dual_t<1, true, 2>(p, A, lda, B, ldb, C, ldc, s, dt);
-    return pack == 1 ? launch_dual_t<1, false, 1>(p, A, lda, B, ldb, C, ldc, s, dt)
-                     : launch_dual_t<1, false, 2>(p, A, lda, B, ldb, C, ldc, s, dt);
-  }
-  if (gen) return pack == 1 ? launch_dual_t<0, true, 1>(p, A, lda, B, ldb, C, ldc, s, dt)
-                            : launch_dual_t<0, true, 2>(p, A, lda, B, ldb, C, ldc, s, dt);
-  return pack == 1 ? launch_dual_t<0, false, 1>(p, A, lda, B, ldb, C, ldc, s, dt)
-                   : launch_dual_t<0, false, 2>(p, A, lda, B, ldb, C, ldc, s, dt);
+  if (p.prec == SPAMM_BF16)
+    return gen ? launch_dual_t<1, true>(p, A, lda, B, ldb, C, ldc, s, dt) : launch_dual_t<1, false>(p, A, lda, B, ldb, C, ldc, s, dt);
+  return gen ? launch_dual_t<0, true>(p, A, lda, B, ldb, C, ldc, s, dt) : launch_dual_t<0, false>(p, A, lda, B, ldb, C, ldc, s, dt);
 }
 
 }  // namespace spamm

@@ -40,8 +40,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_simt_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
                           const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
-                          const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, const Axpby ab,
-                          double* __restrict__ nC, int64_t ldn, int64_t BM, int64_t BN) {
+                          const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ rng,
+                          int64_t GN, const Axpby ab, double* __restrict__ nC, int64_t ldn, int64_t BM, int64_t BN) {
+  if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU range decided on the device
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* sA = reinterpret_cast<float*>(smem);
@@ -212,17 +213,13 @@ spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const fl
                            CU_TENSOR_MAP_SWIZZLE_128B));
   SPAMM_TRY(encode_tmap_2d(&tB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, p.N, p.K, ldb, 128, 32,
                            CU_TENSOR_MAP_SWIZZLE_NONE));
-  static bool attr_set = false;
-  if (!attr_set) {
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(spamm_mul_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kSmemBytes)));
-    attr_set = true;
-  }
-  const int64_t n_tiles = static_cast<int64_t>(p.row_end_macro - p.row_begin_macro) * p.GN;
-  if (n_tiles <= 0) return SPAMM_OK;
-  const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
-  spamm_mul_simt_kernel<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.mstart, p.U, p.macro_ent,
-                                                           p.order, n_tiles, p.GN,
+  SPAMM_SET_SMEM(spamm_mul_simt_kernel, static_cast<int>(kSmemBytes), p.device);
+  const int64_t n_tiles = p.range_on_device ? 0 : static_cast<int64_t>(p.row_end_macro - p.row_begin_macro) * p.GN;
+  if (!p.range_on_device && n_tiles <= 0) return SPAMM_OK;
+  const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
+  spamm_mul_simt_kernel<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.mstart, p.U,
+                                                           static_cast<const uint2*>(p.macro_ent), p.order, n_tiles,
+                                                           p.range_on_device ? p.d_range : nullptr, p.GN,
                                                            Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                                            p.out_norms ? p.nC : nullptr, p.BN, p.BM, p.BN);
   count_launch();

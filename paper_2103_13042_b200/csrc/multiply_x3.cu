@@ -58,11 +58,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
                         const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
                         int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab,
-                        int order_mode, int64_t t0, const int64_t* __restrict__ n_empty_p) {
-  // claim order: LPT, or blocked when every CTA gets >= 16 tiles with k-steps (order_mode: 0 auto,
-  // 1 LPT, 2 blocked); the LPT order ends with the n_empty tiles without kept pairs
+                        int64_t t0, const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p) {
+  if (rng != nullptr) {   // multi-GPU: the macro-row range was decided on the device
+    t0 = rng[0] * GN;
+    n_tiles = (rng[1] - rng[0]) * GN;
+  }
+  // claim order: LPT, or blocked when every CTA gets >= 16 tiles with k-steps; the LPT order
+  // ends with the n_empty tiles without kept pairs
   const int64_t n_work = n_tiles - (n_empty_p ? *n_empty_p : 0);
-  const bool blocked = order_mode == 2 || (order_mode == 0 && n_work >= 16 * static_cast<int64_t>(gridDim.x));
+  const bool blocked = n_work >= 16 * static_cast<int64_t>(gridDim.x);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sZero = smem + kStages * kStageBytes;                  // 512-B zero atom (D = 0 MMA)
@@ -364,22 +368,17 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
                            CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_tmap_3d(&mp.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pB, p.N, p.K, 3, static_cast<uint64_t>(ldb) * 2,
                            static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 3, CU_TENSOR_MAP_SWIZZLE_64B));
-  static bool attr_set = false;
-  if (!attr_set) {
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(spamm_mul_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kSmemBytes)));
-    attr_set = true;
-  }
-  const int64_t n_tiles = (p.row_end_macro - p.row_begin_macro) * p.GN;
-  if (n_tiles <= 0) return SPAMM_OK;
-  const int grid = static_cast<int>(n_tiles < p.num_sms ? n_tiles : p.num_sms);
-  SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
-  // claim order (SPAMM_X3_ORDER: 0 auto, 1 LPT, 2 blocked)
-  const int om = getenv("SPAMM_X3_ORDER") ? atoi(getenv("SPAMM_X3_ORDER")) : 0;
-  spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, p.macro_ent, p.order, n_tiles, p.GN, C,
-                                                         ldc, p.M, p.N, p.sched,
+  SPAMM_SET_SMEM(spamm_mul_x3_kernel, static_cast<int>(kSmemBytes), p.device);
+  const int64_t n_tiles = p.range_on_device ? 0 : (p.row_end_macro - p.row_begin_macro) * p.GN;
+  if (!p.range_on_device && n_tiles <= 0) return SPAMM_OK;
+  const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
+  if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
+  p.sched_zeroed = false;
+  spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, static_cast<const uint2*>(p.macro_ent),
+                                                         p.order, n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
                                                          Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                                         om, p.row_begin_macro * p.GN, p.hist);
+                                                         p.row_begin_macro * p.GN, p.range_on_device ? p.d_range : nullptr,
+                                                         p.hist);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;

@@ -29,6 +29,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kBoxBytesRow = 512;      // bytes per box row (256 BF16 / 128 FP32 columns)
 constexpr int kBoxBytes = 32 * kBoxBytesRow;   // 16 KB
 constexpr int kBoxesPerCta = 16;       // max column boxes walked by one CTA
+constexpr int kStages = 2;             // TMA ring depth (33 KB per CTA: 6 CTAs per SM)
 template <int S>
 constexpr size_t smem_bytes() { return 128 + static_cast<size_t>(S) * kBoxBytes + 1024; }
 
@@ -109,7 +110,7 @@ __device__ __forceinline__ void write_planes<float>(const NormJob& j, const uint
 }
 
 // grid = (max ncb, nrowA + nrowB); blockIdx.y < nrowA -> job A else job B.
-template <typename T, int kStages>
+template <typename T>
 __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_constant__ CUtensorMap tmA,
                                                               const __grid_constant__ CUtensorMap tmB, NormJob ja,
                                                               NormJob jb, int64_t* __restrict__ zws, int zn) {
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
 }
 
 template <typename T>
-spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B, int64_t ldb,
+spamm_status launch_t(Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B, int64_t ldb,
                       int64_t bj0, int64_t bj1, cudaStream_t s, CUtensorMapDataType dt) {
   constexpr int kCols = kBoxBytesRow / sizeof(T);
   CUtensorMap tA{}, tB{};
@@ -206,21 +207,19 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
   }
   // B is A (same square matrix, same layout, full ranges): read it once.  Tile (r, c) of A is
   // tile (k = r, j = c) of B, so its norm is also nB^T[c*BK + r] (C = A*A, e.g. matrix powers).
-  const_cast<Plan&>(p).b_is_a = false;
+  p.b_is_a = false;
   if (A == B && lda == ldb && p.M == p.K && p.K == p.N && ar0 == 0 && ar1 == p.BM && bj0 == 0 && bj1 == p.BN) {
-    const_cast<Plan&>(p).b_is_a = true;   // FP32X3: A's planes serve as B's
+    p.b_is_a = true;   // FP32X3: A's planes serve as B's
     ja.out2 = p.nBt;
     ja.out2_rs = 1;
     ja.out2_cs = p.BK;
     jb.nrow = 0;
   }
   // boxes per CTA: 8 (128 KB streamed per CTA) unless that leaves fewer than ~4 CTAs per SM,
-  // then fewer so that small problems are not latency-bound on a handful of CTAs
-  // ring depth and boxes per CTA (experiments: SPAMM_NORM_STAGES 2..4, SPAMM_NORM_BPC 1..16)
-  // default 2 stages (33 KB): 6 CTAs per SM, so the N = 8192 grid runs in ~one wave (measured
-  // 29.3 vs 31.1 us with 4 stages, r01f)
-  const int stages = getenv("SPAMM_NORM_STAGES") ? std::min(4, std::max(2, atoi(getenv("SPAMM_NORM_STAGES")))) : 2;
-  int bpc = getenv("SPAMM_NORM_BPC") ? std::min(kBoxesPerCta, std::max(1, atoi(getenv("SPAMM_NORM_BPC")))) : 8;
+  // then fewer so that small problems are not latency-bound on a handful of CTAs.  Ring depth 2
+  // (33 KB per CTA, 6 CTAs per SM: the N = 8192 grid runs in about one wave; 29.3 vs 31.1 us with
+  // 4 stages, r01f)
+  int bpc = 8;
   auto ncb_of = [&](const NormJob& jj, int b) -> int64_t {
     const int64_t per_cta = static_cast<int64_t>(b) * kCols;
     return jj.nrow > 0 ? (jj.cols + per_cta - 1) / per_cta : 0;
@@ -236,16 +235,7 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
     const void* Bs = static_cast<const char*>(B) + static_cast<size_t>(bj0) * kTile * sizeof(T);
     SPAMM_TRY(encode_tmap_2d(&tB, dt, sizeof(T), Bs, bcols, p.K, ldb, kCols, 32, CU_TENSOR_MAP_SWIZZLE_NONE));
   }
-  static bool attr = false;
-  if (!attr) {
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem_bytes<2>())));
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem_bytes<3>())));
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(tile_norms_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem_bytes<4>())));
-    attr = true;
-  }
+  SPAMM_SET_SMEM(tile_norms_kernel<T>, static_cast<int>(smem_bytes<kStages>()), p.device);
   int64_t* zws = p.zero_ws_next ? p.row_work : nullptr;
   const int zn = static_cast<int>(p.BM + p.BK + 4);
   const int64_t gx = std::max(ja.ncb, jb.ncb);
@@ -253,12 +243,7 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
   if (gx <= 0 || gy <= 0) return SPAMM_OK;
   if (gy > 65535) return fail(SPAMM_E_UNSUPPORTED, "more than 65535 tile rows in one norm launch");
   dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
-  if (stages == 2)
-    tile_norms_kernel<T, 2><<<grid, kThreads, smem_bytes<2>(), s>>>(tA, tB, ja, jb, zws, zn);
-  else if (stages == 3)
-    tile_norms_kernel<T, 3><<<grid, kThreads, smem_bytes<3>(), s>>>(tA, tB, ja, jb, zws, zn);
-  else
-    tile_norms_kernel<T, 4><<<grid, kThreads, smem_bytes<4>(), s>>>(tA, tB, ja, jb, zws, zn);
+  tile_norms_kernel<T><<<grid, kThreads, smem_bytes<kStages>(), s>>>(tA, tB, ja, jb, zws, zn);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
@@ -266,7 +251,7 @@ spamm_status launch_t(const Plan& p, const void* A, int64_t lda, int64_t ar0, in
 
 }  // namespace
 
-spamm_status launch_norms2(const Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B,
+spamm_status launch_norms2(Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B,
                            int64_t ldb, int64_t bj0, int64_t bj1, cudaStream_t s) {
   switch (p.prec) {
     case SPAMM_FP32:

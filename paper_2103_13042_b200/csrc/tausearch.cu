@@ -97,14 +97,13 @@ __global__ void __launch_bounds__(1024) ave_kernel(const double* __restrict__ pa
   if (threadIdx.x == 0) out[0] = red[0] / denom;
 }
 
-struct Scratch {
-  unsigned long long* cnt = nullptr;
-  double* part = nullptr;
-  ~Scratch() {
-    if (cnt) cudaFree(cnt);
-    if (part) cudaFree(part);
-  }
-};
+// plan-owned scratch of the search (allocated on the first search, reused afterwards)
+spamm_status ensure_scratch(Plan& p, int64_t nch) {
+  if (!p.ts_cnt) SPAMM_CUDA_TRY(cudaMalloc(&p.ts_cnt, sizeof(unsigned long long)));
+  if (nch > 0 && !p.ts_part)
+    SPAMM_CUDA_TRY(cudaMalloc(&p.ts_part, sizeof(double) * static_cast<size_t>(nch * 2 * p.BK + 1)));
+  return SPAMM_OK;
+}
 
 spamm_status count_on(const Plan& p, double tau, unsigned long long* d_cnt, cudaStream_t s, int64_t* kept) {
   SPAMM_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
@@ -131,9 +130,9 @@ spamm_status spamm_count_kept(spamm_plan_t h, double tau, int64_t* kept, void* s
   if (!(std::isfinite(tau) && tau >= 0.0)) return fail(SPAMM_E_INVALID, "tau must be finite and >= 0");
   Plan& p = *reinterpret_cast<Plan*>(h);
   if (!p.norms_ready) return fail(SPAMM_E_STATE, "spamm_count_kept before spamm_norms");
-  Scratch w;
-  SPAMM_CUDA_TRY(cudaMalloc(&w.cnt, sizeof(unsigned long long)));
-  return count_on(p, tau, w.cnt, static_cast<cudaStream_t>(stream), kept);
+  SPAMM_TRY(ensure_scratch(p, 0));
+  p.last_stream = static_cast<cudaStream_t>(stream);
+  return count_on(p, tau, p.ts_cnt, static_cast<cudaStream_t>(stream), kept);
 }
 
 spamm_status spamm_tau_search(spamm_plan_t h, double target, double tol, int32_t max_iter, double* tau_out,
@@ -145,9 +144,11 @@ spamm_status spamm_tau_search(spamm_plan_t h, double target, double tol, int32_t
   if (!p.norms_ready) return fail(SPAMM_E_STATE, "spamm_tau_search before spamm_norms");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t nchA = (p.BM + 63) / 64, nchB = (p.BN + 63) / 64, nch = std::max(nchA, nchB);
-  Scratch w;
-  SPAMM_CUDA_TRY(cudaMalloc(&w.cnt, sizeof(unsigned long long)));
-  SPAMM_CUDA_TRY(cudaMalloc(&w.part, sizeof(double) * static_cast<size_t>(nch * 2 * p.BK + 1)));
+  SPAMM_TRY(ensure_scratch(p, nch));
+  struct {
+    unsigned long long* cnt;
+    double* part;
+  } w{p.ts_cnt, p.ts_part};
   SPAMM_CUDA_TRY(cudaMemsetAsync(w.part, 0, sizeof(double) * static_cast<size_t>(nch * 2 * p.BK + 1), s));
   // ave: mean norm product over all BM*BK*BN triples (reading R17) = sum_k sA[k] sB[k] / triples
   colsum_kernel<<<dim3(static_cast<unsigned>((p.BK + 127) / 128), static_cast<unsigned>(nch), 2), 128, 0, s>>>(
@@ -160,6 +161,12 @@ spamm_status spamm_tau_search(spamm_plan_t h, double target, double tol, int32_t
   double ave = 0.0;
   SPAMM_CUDA_TRY(cudaMemcpyAsync(&ave, d_ave, sizeof(double), cudaMemcpyDeviceToHost, s));
   SPAMM_CUDA_TRY(cudaStreamSynchronize(s));
+  p.last_stream = s;
+  // all-zero maps (e.g. a chain converged to 0) or non-finite norms: the search's bracket
+  // [0, k*ave] is undefined
+  if (!(std::isfinite(ave) && ave > 0.0))
+    return fail(SPAMM_E_INVALID, "tau search needs finite norms with a positive mean product (ave = " +
+                                     std::to_string(ave) + ")");
 
   auto vr_at = [&](double t, double* vr) -> spamm_status {
     int64_t kept = 0;
@@ -176,8 +183,13 @@ spamm_status spamm_tau_search(spamm_plan_t h, double target, double tol, int32_t
       lo = tau;
       double vh = 0.0;
       SPAMM_TRY(vr_at(hi, &vh));
+      // Sec. 3.5.2 grows k by one; after 64 steps k doubles so that the bracket reaches the largest
+      // product (where vr = 0 <= target) in a bounded number of evaluations on heavy-tailed maps
+      int widen = 0;
       while (vh > target) {
-        ++k;
+        k = widen < 64 ? k + 1 : 2 * k;
+        ++widen;
+        if (k > (1 << 30)) return fail(SPAMM_E_INVALID, "tau search bracket did not converge");
         hi = k * ave;
         SPAMM_TRY(vr_at(hi, &vh));
       }

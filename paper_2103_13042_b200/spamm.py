@@ -19,9 +19,8 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "spamm.h")
 
 SPAMM_OK, SPAMM_E_INVALID, SPAMM_E_UNSUPPORTED, SPAMM_E_CUDA, SPAMM_E_NOMEM, SPAMM_E_NCCL, SPAMM_E_STATE = range(7)
 SPAMM_FP32, SPAMM_BF16, SPAMM_FP16, SPAMM_FP32X3 = 0, 1, 2, 3
-SPAMM_FLAG_NONE, SPAMM_FLAG_TIMING, SPAMM_FLAG_SYNC_SKIPMAP = 0, 1, 2
-SPAMM_MUL_AUTO, SPAMM_MUL_OUTPUT_NORMS = 1, 2
-SPAMM_MUL_AUTO = 1
+SPAMM_FLAG_NONE, SPAMM_FLAG_TIMING = 0, 1
+SPAMM_MUL_AUTO, SPAMM_MUL_OUTPUT_NORMS, SPAMM_MUL_LOW_ONLY = 1, 2, 4
 SPAMM_MGPU_INPUTS_REPLICATED, SPAMM_MGPU_INPUTS_ON_ROOT, SPAMM_MGPU_GATHER_C = 0, 1, 2
 
 DTYPE_OF = {SPAMM_FP32: torch.float32, SPAMM_BF16: torch.bfloat16, SPAMM_FP16: torch.float16,
@@ -69,6 +68,7 @@ def _load():
         "spamm_nccl_comm_destroy": [P],
         "spamm_partition_rows": [PI64, I64, ctypes.c_int, PI64],
         "spamm_multiply_mgpu": [P, P, ctypes.c_int, ctypes.c_int, P, I64, P, I64, P, I64, U32, P],
+        "spamm_multiply_mgpu_local": [PP, ctypes.c_int, P, I64, P, I64, PP, I64, U32, P],
         "spamm_get_norms": [P, PP, PP, PI64, PI64, PI64],
         "spamm_get_skipmap": [P, PP, PP, PI64],
         "spamm_get_counts": [P, PP, PP],
@@ -257,6 +257,19 @@ def spamm_multiply_mgpu(plan, comm, rank: int, nranks: int, A, B, C, flags: int 
                                     _stream(stream)))
 
 
+def spamm_multiply_mgpu_local(plans, A, B, Cs, flags: int = 0, stream=None) -> None:
+    """nranks = len(plans) ranks of spamm_multiply_mgpu emulated on one GPU (verification)."""
+    n = len(plans)
+    a, lda = _mat(A)
+    b, ldb = _mat(B)
+    ptrs = [_mat(c) for c in Cs]
+    if len({ld for _, ld in ptrs}) != 1:
+        raise ValueError("all C buffers must share one leading dimension")
+    hp = (ctypes.c_void_p * n)(*[p.value if isinstance(p, ctypes.c_void_p) else p for p in plans])
+    cp = (ctypes.c_void_p * n)(*[c.value for c, _ in ptrs])
+    _check(_lib.spamm_multiply_mgpu_local(hp, n, a, lda, b, ldb, cp, ptrs[0][1], int(flags), _stream(stream)))
+
+
 # ---------------------------------------------------------- introspection ---
 class _DevArray:
     """__cuda_array_interface__ view of plan-owned device memory (for torch.as_tensor)."""
@@ -313,7 +326,7 @@ def spamm_get_counts(plan):
 def spamm_get_macro(plan):
     """(start int64 [GM*GN], count int64 [GM*GN], entries [n, 2] int64 (k, mask) over all
     entry storage in use, order int32 [GM*GN], GM, GN); macro-tile t's list is
-    entries[start[t] : start[t] + count[t]].  Masks of 8 x 8 groups (CTA-pair path) use
+    entries[start[t] : start[t] + count[t]].  Masks of 8 x 8 groups (the BF16/FP16 path) use
     all 64 bits: view them as uint64."""
     st = spamm_get_stats(plan)
     ps, pc, e, o = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
@@ -324,7 +337,7 @@ def spamm_get_macro(plan):
     start = _view(ps.value, (nmac,), "<i8", torch.int64)
     count = _view(pc.value, (nmac,), "<i8", torch.int64)
     n = int((start + count).max().item()) if nmac else 0
-    wide = st["macro_i"] * st["macro_j"] > 32   # 8 x 8 pair tiles: (k, mask_lo, mask_hi, 0) words
+    wide = st["macro_i"] * st["macro_j"] > 32   # 8 x 8 tiles: (k, mask_lo, mask_hi, 0) words
     if not n:
         ent = torch.zeros((0, 2), dtype=torch.int64, device="cuda")
     elif wide:
@@ -388,18 +401,36 @@ class Plan:
     def set_scalars(self, alpha, beta):
         spamm_set_scalars(self.handle, alpha, beta)
 
+    def _check_ops(self, A, B, C=None):
+        """Operands against the plan (the C ABI sees only pointers and leading dimensions): a
+        float32 tensor given to a bf16 plan would be read as bf16, a short one past its end."""
+        M, N, K = self.shape
+        for name, t, shape, dt in (("A", A, (M, K), self.dtype), ("B", B, (K, N), self.dtype),
+                                   ("C", C, (M, N), torch.float32)):
+            if t is None:
+                continue
+            if not t.is_cuda:
+                raise ValueError(f"{name} must be a CUDA tensor")
+            if tuple(t.shape) != shape:
+                raise ValueError(f"{name} has shape {tuple(t.shape)}, the plan expects {shape}")
+            if t.dtype != dt:
+                raise ValueError(f"{name} has dtype {t.dtype}, the plan expects {dt}")
+
     def norms(self, A, B, stream=None):
+        self._check_ops(A, B)
         spamm_norms(self.handle, A, B, stream)
 
     def build_skipmap(self, stream=None):
         spamm_build_skipmap(self.handle, stream)
 
     def multiply(self, A, B, C, flags=0, stream=None):
+        self._check_ops(A, B, C)
         spamm_multiply(self.handle, A, B, C, flags, stream)
 
     def run(self, A, B, C=None, stream=None):
         if C is None:
             C = torch.empty((self.shape[0], self.shape[1]), dtype=torch.float32, device=A.device)
+        self._check_ops(A, B, C)
         spamm_run(self.handle, A, B, C, stream)
         return C
 
@@ -407,6 +438,7 @@ class Plan:
         return spamm_get_stats(self.handle)
 
     def multiply_chain(self, A, B, C, C_low=None, flags=SPAMM_MUL_OUTPUT_NORMS, stream=None):
+        self._check_ops(A, B, C)
         spamm_multiply_chain(self.handle, A, B, C, C_low, flags, stream)
 
     def output_norms(self):

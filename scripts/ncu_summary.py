@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise ncu reports / launch lists into profiles/ (text + ncu_traffic.json).
 
-  python scripts/ncu_summary.py --rep gpurun_out/prof_umma.ncu-rep --tag r01 [--prec bf16]
+  python scripts/ncu_summary.py --rep gpurun_out/prof.ncu-rep --tag r02a [--workload "<bench config.workload>"]
   python scripts/ncu_summary.py --launches gpurun_out/launches.csv --tag r01
 """
 import argparse
@@ -33,7 +33,7 @@ def to_bytes(val, unit):
     return v * scale
 
 
-def summarise_rep(rep, tag, prec):
+def summarise_rep(rep, tag, workload):
     rows, units = raw_rows(rep)
     lines = [f"# ncu --set full summary of {os.path.basename(rep)} ({tag})"]
     traffic = {}
@@ -56,7 +56,8 @@ def summarise_rep(rep, tag, prec):
         f.write("\n".join(lines) + "\n")
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     d = json.load(open(tp)) if os.path.exists(tp) else {}
-    d.setdefault(prec, {}).update(traffic)
+    if workload:   # keyed by bench.py's config.workload string: the bench uses it only for that workload
+        d.setdefault(workload, {}).update(traffic)
     json.dump(d, open(tp, "w"), indent=1)
     print("\n".join(lines[:40]))
 
@@ -91,9 +92,9 @@ if __name__ == "__main__":
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--tag", default="r01")
-    ap.add_argument("--prec", default="bf16")
+    ap.add_argument("--workload", default=None, help="bench.py config.workload of the captured run")
     a = ap.parse_args()
     if a.rep:
-        summarise_rep(a.rep, a.tag, a.prec)
+        summarise_rep(a.rep, a.tag, a.workload)
     if a.launches:
         summarise_launches(a.launches, a.tag)

@@ -301,25 +301,6 @@ def test_full_size_bench_config_sampled(sp, prec):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
-@pytest.mark.parametrize("shape", [(300, 257, 129), (1000, 1000, 1000)])
-def test_sync_skipmap_path(sp, prec, shape):
-    """SPAMM_FLAG_SYNC_SKIPMAP (count -> scan -> emit, exact list storage; the path plans
-    take when worst-case storage exceeds the budget, e.g. N = 65536) vs the oracle."""
-    M, N, K = shape
-    A = _rounded(synth.perturbed_decay_matrix(K, 0.95, seed=41, m=M), prec)
-    B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=42, m=K), prec)
-    nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
-    prods = np.unique(nA[:, :, None] * nB[None, :, :])
-    mid = len(prods) // 3
-    tau = float(0.5 * (prods[mid] + prods[mid + 1]))
-    plan, C = _run(sp, A, B, tau, prec, flags=sp.SPAMM_FLAG_SYNC_SKIPMAP)
-    diff, _ = _check_skipmap(sp, plan, nA, nB, tau)
-    assert diff == 0
-    err = _rel_fro(C, oracle.spamm(A, B, tau, T, nA, nB))
-    assert err <= (2e-6 if prec == "fp32" else 1e-5), err
-
-
-@pytest.mark.parametrize("prec", ["fp32", "bf16"])
 @pytest.mark.parametrize("N", [256, 1000])
 def test_aliased_a_equals_b_norms(sp, prec, N):
     """A and B the same buffer (C = A*A): the norm kernel reads it once and writes both maps;

@@ -99,3 +99,36 @@ def test_count_kept_nan_and_state(sp):
     with pytest.raises(sp.SpammError) as e:
         plan.tau_search(1.5)
     assert e.value.status == sp.SPAMM_E_INVALID
+
+
+@pytest.mark.parametrize("bad", ["zero", "nan", "inf"])
+def test_tau_search_degenerate_maps_fail_cleanly(sp, bad):
+    """All-zero maps (a chain converged to 0) or non-finite norms: the Sec. 3.5.2 bracket
+    [0, k*ave] is undefined; the search must return SPAMM_E_INVALID instead of looping."""
+    N = 128
+    A = np.zeros((N, N), np.float32) if bad == "zero" else synth.random_matrix(N, N, seed=65)
+    if bad == "nan":
+        A[3, 3] = np.nan
+    if bad == "inf":
+        A[3, 3] = np.inf
+    plan = sp.Plan(N, N, N, 0.0, "fp32")
+    plan.norms(_dev(A), _dev(A))
+    with pytest.raises(sp.SpammError) as e:
+        plan.tau_search(0.3)
+    assert e.value.status == sp.SPAMM_E_INVALID
+    assert plan.count_kept(0.0) == (N // T) ** 3        # the plan stays usable
+
+
+def test_tau_search_heavy_tail_terminates(sp):
+    """One huge tile among tiny ones: ave is far below the largest products, so the paper's
+    k += 1 bracket widening would need ~1e6 count evaluations; the widening turns geometric
+    after 64 steps and the search ends within max_iter bisection steps."""
+    N = 256
+    A = synth.random_matrix(N, N, seed=66, scale=1e-6)
+    A[:32, :32] = 1e6
+    plan = sp.Plan(N, N, N, 0.0, "fp32")
+    Ad = _dev(A)
+    plan.norms(Ad, Ad)
+    # target 0: vr(k*ave) > 0 until k*ave passes the largest product (~512 ave)
+    tau, vr, it = plan.tau_search(0.0, tol=1e-4, max_iter=40)
+    assert np.isfinite(tau) and vr <= 1.0 / 512 and it <= 40
