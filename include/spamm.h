@@ -234,6 +234,19 @@ spamm_status spamm_get_output_norms(spamm_plan_t p, const double** d_nC);
  * norm stage also splits the inputs). */
 spamm_status spamm_set_norms(spamm_plan_t p, const double* nA, const double* nB, void* stream);
 
+/* ------------------------------------------------------- convolution drop-in --- */
+/* a convolution layer as the SpAMM of its im2col
+ * GEMM, Y = SpAMM(W, im2col(X), tau).  X: [batch][C_in][H][Wd] (NCHW, contiguous, the plan's input
+ * type: float for FP32/FP32X3 plans, bf16/fp16 otherwise); W: [C_out][C_in*kh*kw] row-major
+ * (leading dimension ldw), the plan's A; Y: [C_out][batch*Ho*Wo] float row-major (ldy), column
+ * (n*Ho + y)*Wo + x, Ho = (H + 2 pad - kh)/stride + 1 (Wo likewise).  im2col row index
+ * (ci*kh + ky)*kw + kx; out-of-image taps are 0.  The plan must have M = C_out, K = C_in*kh*kw,
+ * N = batch*Ho*Wo (else SPAMM_E_INVALID).  A device kernel writes im2col(X) into plan-owned storage
+ * (allocated on the first call), then the three stages run as spamm_run.  Stream-ordered. */
+spamm_status spamm_conv2d_im2col(spamm_plan_t p, const void* W, int64_t ldw, const void* X, int64_t batch,
+                                 int64_t C_in, int64_t H, int64_t Wd, int32_t kh, int32_t kw, int32_t stride,
+                                 int32_t pad, float* Y, int64_t ldy, void* stream);
+
 /* ------------------------------------------------------------ tau search --- */
 
 /* Number of kept triples at tau, i.e. #{(i,k,j) : !(nA[i][k] * nB[k][j] < tau)} in float64

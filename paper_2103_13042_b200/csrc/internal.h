@@ -64,9 +64,9 @@ struct Plan {
   int64_t* U = nullptr;      // [GM*GN + 1] macro union counts (k-steps with a kept pair)
   int64_t* L = nullptr;      // [GM*GN + 1] kept pairs per macro-tile
   int64_t* leaf_start = nullptr;  // [BM*BN] start of each C tile's k list (leaf view, on request)
-  int64_t* row_work = nullptr;    // [BM + BK + 4]: row work, then the U histogram and totals (one memset)
-  int64_t* hist = nullptr;        // = row_work + BM: [BK+2] histogram of macro union counts
-  int64_t* totals = nullptr;      // = hist + BK + 2: [0] kept pairs, [1] macro entries
+  int64_t* row_work = nullptr;    // [BM + BK + 8]: row work, then the order pass's bucket counts and totals (one memset)
+  int64_t* hist = nullptr;        // = row_work + BM: [BK+2] bucket counts of the order pass
+  int64_t* totals = nullptr;      // = hist + BK + 2: [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
   unsigned int* ticket = nullptr; // CTA-completion ticket of the skip map (self-resetting)
   unsigned int* sched = nullptr;  // dynamic tile counters of the multiply kernels (reset per launch)
   uint16_t* leaf_k = nullptr;     // [BM*BN*BK] per-C-tile k lists (leaf view, on request)
@@ -82,6 +82,7 @@ struct Plan {
   // A planes [3][M][ldpa], then B planes [3][K][ldpb] (unused when B is A)
   uint16_t* planes = nullptr;
   int64_t ldpa = 0, ldpb = 0;
+  void* im2col = nullptr;         // spamm_conv2d_im2col: the K x N im2col matrix (allocated on first use)
   bool b_is_a = false;            // the last spamm_norms saw B == A (planes of A serve both)
   bool leaf_alloc = false;
 

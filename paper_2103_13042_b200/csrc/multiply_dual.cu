@@ -47,7 +47,6 @@ constexpr int kDBSlot = 32 * 256 * 2;                 // B[32 x 256] as eight [3
 constexpr int kDStepBytes = kDASlot + kDBSlot;        // one 32-deep k-step
 constexpr int kDThreads = 384;   // w0 A/claims, w1-2 MMA, w3 B, w4-11 epilogue
 constexpr int kDTQ = 4;                               // tile ring depth
-constexpr int64_t kOrdS = 12;                         // blocked claim order: super-block side (tiles)
 // kPack = 2 k-steps of one macro-tile per ring stage (one wait / commit per stage for the issuers;
 // measured 174 -> 165 us against one per stage, r01e); the ring holds 6 k-steps (192 KB)
 constexpr int kPack = 2;
@@ -102,10 +101,11 @@ __global__ void __launch_bounds__(kDThreads, 1)
     t0 = rng[0] * GN;
     n_tiles = (rng[1] - rng[0]) * GN;
   }
+  // claims follow the skip map's order (skipmap.cu order_pass: LPT for few tiles per CTA, ascending
+  // first kept k for many); the tiles without kept pairs come last and are zero-filled by the
+  // epilogue warps (plain epilogue), or go through the pipeline (n_empty_p == nullptr)
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
-  // claim order: LPT (descending k-steps), or blocked when every CTA gets many tiles
-  const bool row_order = n_work >= 16 * static_cast<int64_t>(gridDim.x);
   constexpr int wide_ok = 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -193,31 +193,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
       unsigned int idx = 0;
       if (lane == 0) idx = atomicAdd(sched, 1u);
       idx = __shfl_sync(0xffffffffu, idx, 0);
-      if (row_order) {
-        // many tiles per CTA: balance comes for free, so claim in a blocked tile order (kOrdS x kOrdS
-        // super-blocks row-major, tiles row-major inside; empty tiles skipped): the ~grid tiles in
-        // flight then share A row blocks and B column blocks in L2
-        const int64_t GMr = n_tiles / GN, nsbc = (GN + kOrdS - 1) / kOrdS;
-        for (;;) {
-          if (static_cast<int64_t>(idx) >= ((GMr + kOrdS - 1) / kOrdS) * nsbc * kOrdS * kOrdS) return d;
-          const int64_t sb = idx / (kOrdS * kOrdS), w = idx % (kOrdS * kOrdS);
-          const int64_t li = (sb / nsbc) * kOrdS + w / kOrdS, lj = (sb % nsbc) * kOrdS + w % kOrdS;
-          const int64_t t = t0 + li * GN + lj;
-          const bool in = li < GMr && lj < GN;
-          const int64_t c = in ? mcount[t] : 0;
-          // tiles without k-steps are zero-filled at the end, or (no zero-fill: alpha/beta, chained
-          // outputs) go through the pipeline like any tile
-          if (c > 0 || (in && n_empty_p == nullptr)) {
-            d.t = t;
-            d.e0 = mstart[t];
-            d.e1 = d.e0 + c;
-            return d;
-          }
-          if (lane == 0) idx = atomicAdd(sched, 1u);
-          idx = __shfl_sync(0xffffffffu, idx, 0);
-        }
-      }
-      if (static_cast<int64_t>(idx) < (n_empty_p ? n_work : n_tiles)) {
+      if (static_cast<int64_t>(idx) < n_work) {
         d.t = order[idx];
         d.e0 = mstart[d.t];
         d.e1 = d.e0 + mcount[d.t];
@@ -760,7 +736,7 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   cudaMemsetAsync(prof, 0, 1024 * 24 * 8, s);
 #endif
   kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, p.row_begin_macro * p.GN,
-                                       p.range_on_device ? p.d_range : nullptr, kGen ? nullptr : p.hist, p.GN, C, ldc,
+                                       p.range_on_device ? p.d_range : nullptr, kGen ? nullptr : p.totals + 2, p.GN, C, ldc,
                                        p.M, p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                        DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
                                        prof, p.N % 32 == 0 ? 1 : 0);

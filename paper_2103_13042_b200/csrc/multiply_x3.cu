@@ -63,10 +63,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     t0 = rng[0] * GN;
     n_tiles = (rng[1] - rng[0]) * GN;
   }
-  // claim order: LPT, or blocked when every CTA gets >= 16 tiles with k-steps; the LPT order
-  // ends with the n_empty tiles without kept pairs
-  const int64_t n_work = n_tiles - (n_empty_p ? *n_empty_p : 0);
-  const bool blocked = n_work >= 16 * static_cast<int64_t>(gridDim.x);
+  // claims follow the skip map's order (skipmap.cu order_pass); every tile, with or without
+  // k-steps, goes through the pipeline (the tiles without kept pairs are last)
+  (void)n_empty_p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sZero = smem + kStages * kStageBytes;                  // 512-B zero atom (D = 0 MMA)
@@ -117,24 +116,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) idx = atomicAdd(sched, 1u);
       idx = __shfl_sync(0xffffffffu, idx, 0);
       TileQ ti{-1, 0, 0};
-      if (blocked) {
-        // many tiles per CTA: a blocked order (12 x 12 super-blocks row-major, tiles row-major
-        // inside) so the tiles in flight share operand strips in L2 (as multiply_dual.cu)
-        const int64_t GMr = n_tiles / GN, nsbc = (GN + 11) / 12;
-        for (;;) {
-          if (static_cast<int64_t>(idx) >= ((GMr + 11) / 12) * nsbc * 144) return ti;
-          const int64_t sb = idx / 144, w = idx % 144;
-          const int64_t li = (sb / nsbc) * 12 + w / 12, lj = (sb % nsbc) * 12 + w % 12;
-          if (li < GMr && lj < GN) {
-            ti.t = t0 + li * GN + lj;
-            ti.e0 = mstart[ti.t];
-            ti.e1 = ti.e0 + mcount[ti.t];
-            return ti;
-          }
-          if (lane == 0) idx = atomicAdd(sched, 1u);
-          idx = __shfl_sync(0xffffffffu, idx, 0);
-        }
-      }
       if (static_cast<int64_t>(idx) < n_tiles) {
         ti.t = order[idx];
         ti.e0 = mstart[ti.t];
@@ -378,7 +359,7 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
                                                          p.order, n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
                                                          Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                                                          p.row_begin_macro * p.GN, p.range_on_device ? p.d_range : nullptr,
-                                                         p.hist);
+                                                         p.totals + 2);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;

@@ -225,18 +225,23 @@ __device__ void block_scan_array(const int64_t* in, int64_t* out, int64_t n, boo
 }
 
 struct OrderArgs {
-  int64_t* hist;         // [BK + 2] global histogram (written: the multiply reads hist[0])
+  int64_t* hist;         // [BK + 2] bucket counts (global fallback when they do not fit in shared memory)
   int64_t* bucket_pos;   // [BK + 2]
-  int64_t nbucket;       // BK + 1 (union counts 0..BK)
+  int64_t nbucket;       // BK + 1 (keys 0..BK)
   const int64_t* U;
   const int64_t* L;
+  const void* macro_ent; // first entry of macro-tile t at t*BK: its first kept k
+  int ent16;             // entries are 16 B (8 x 8 masks) else 8 B
+  int64_t BK, GN;
+  int num_sms;
   int32_t* order;
-  int64_t* totals;       // [0] kept pairs, [1] macro entries
+  int64_t* totals;       // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
   unsigned int* ticket;
   unsigned int* sched;   // the multiply's claim counters [4], zeroed by the last CTA
   int enabled;           // 0: no order pass (multi-GPU provisional range)
 };
 constexpr int kSmemBuckets = 4096;
+constexpr int64_t kOrdS = 12;   // tie order: 12 x 12 super-blocks of macro-tiles, row-major inside
 
 // warp-aggregated atomicAdd of 1 per lane on cnt[key]: lanes with equal keys share one atomic;
 // returns each lane's old value + its rank among the equal lanes
@@ -253,60 +258,91 @@ __device__ __forceinline__ T agg_inc(T* cnt, int64_t key, bool active) {
   return base + static_cast<T>(__popc(peers & ((1u << lane) - 1u)));
 }
 
-// LPT order of the macro-tiles [t0, t1) by descending union count U (bucket sort), histogram,
-// totals; one CTA (the last to finish), `sbuf` = dynamic shared memory of kSmemBuckets words.
+// The multiply's claim order of the macro-tiles [t0, t1) (a bucket sort, one CTA: the last to
+// finish the skip map; `sbuf` = dynamic shared memory of kSmemBuckets words):
+//   * few tiles per CTA (n_work < 16 per SM): longest processing time first -- key BK - U, so the
+//     long tiles start first and the short ones fill the tail (Sec. 3.5.1's balance goal);
+//   * many tiles per CTA (balance is free): ascending first kept k -- on banded products the tiles
+//     of one "shell" (same max(I, J)) start at the same k and share A or B strips, and consecutive
+//     shells reuse each other's strips a few k-steps later, so the operands are read from DRAM
+//     about once instead of once per tile (the L2 holds the moving k-window);
+//   * macro-tiles without kept pairs last (key BK; zero-filled by the multiply's epilogue warps).
+// Ties keep the 12 x 12 super-block enumeration (tiles in flight share strips in L2).
 __device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t* s_warp, unsigned long long* sbuf) {
-  const bool in_smem = oa.nbucket <= kSmemBuckets;
-  unsigned long long* h = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.hist);
-  for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) h[b] = 0ull;
-  __syncthreads();
-  int64_t kept = 0, ents = 0;
-  for (int64_t base = t0; base < t1; base += blockDim.x) {
-    const int64_t t = base + threadIdx.x;
-    const bool in = t < t1;
-    const int64_t u = in ? oa.U[t] : 0;
-    if (in) {
-      kept += oa.L[t];
-      ents += u;
-    }
-    agg_inc<unsigned long long>(h, u, in);
-  }
-  __syncthreads();
-  if (in_smem)   // the multiply reads hist[0] (macro-tiles without kept pairs)
-    for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) oa.hist[b] = static_cast<int64_t>(h[b]);
-  __syncthreads();
-  // bucket_pos[u] = number of macro-tiles with union count > u (descending buckets)
-  block_scan_array(oa.hist, oa.bucket_pos, oa.nbucket, true, s_warp);
-  unsigned long long* pos = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.bucket_pos);
-  if (in_smem)
-    for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) pos[b] = static_cast<unsigned long long>(oa.bucket_pos[b]);
-  __syncthreads();
-  for (int64_t base = t0; base < t1; base += blockDim.x) {
-    const int64_t t = base + threadIdx.x;
-    const bool in = t < t1;
-    const int64_t u = in ? oa.U[t] : 0;
-    const unsigned long long slot = agg_inc<unsigned long long>(pos, u, in);
-    if (in) oa.order[slot] = static_cast<int32_t>(t);
+  const int64_t GN = oa.GN, GMr = (t1 - t0) / GN, nsbc = (GN + kOrdS - 1) / kOrdS;
+  const int64_t n_enum = ((GMr + kOrdS - 1) / kOrdS) * nsbc * kOrdS * kOrdS;
+  auto tile_of = [&](int64_t idx) -> int64_t {   // super-block enumeration -> tile (or -1)
+    const int64_t sb = idx / (kOrdS * kOrdS), w = idx % (kOrdS * kOrdS);
+    const int64_t li = (sb / nsbc) * kOrdS + w / kOrdS, lj = (sb % nsbc) * kOrdS + w % kOrdS;
+    return (li < GMr && lj < GN) ? t0 + li * GN + lj : -1;
+  };
+  // pass 1: totals and the number of tiles with work
+  int64_t kept = 0, ents = 0, work = 0;
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    const int64_t u = oa.U[t];
+    kept += oa.L[t];
+    ents += u;
+    work += u > 0;
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
     kept += __shfl_xor_sync(0xffffffffu, kept, o);
     ents += __shfl_xor_sync(0xffffffffu, ents, o);
+    work += __shfl_xor_sync(0xffffffffu, work, o);
   }
-  __syncthreads();
   if ((threadIdx.x & 31) == 0) {
     s_warp[threadIdx.x >> 5] = kept;
-    s_warp[16 + (threadIdx.x >> 5)] = ents;
+    s_warp[8 + (threadIdx.x >> 5)] = ents;
+    s_warp[16 + (threadIdx.x >> 5)] = work;
+  }
+  __syncthreads();
+  int64_t tk = 0, te = 0, tw = 0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+    tk += s_warp[w];
+    te += s_warp[8 + w];
+    tw += s_warp[16 + w];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int64_t a = 0, b = 0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-      a += s_warp[w];
-      b += s_warp[16 + w];
-    }
-    oa.totals[0] = a;
-    oa.totals[1] = b;
+    oa.totals[0] = tk;
+    oa.totals[1] = te;
+    oa.totals[2] = (t1 - t0) - tw;
+  }
+  const bool by_k = tw >= 16 * static_cast<int64_t>(oa.num_sms);
+  auto key_of = [&](int64_t t) -> int64_t {
+    const int64_t u = oa.U[t];
+    if (u == 0) return oa.BK;
+    if (!by_k) return oa.BK - u;
+    const int64_t e = t * oa.BK;
+    return oa.ent16 ? static_cast<int64_t>(reinterpret_cast<const uint4*>(oa.macro_ent)[e].x)
+                    : static_cast<int64_t>(reinterpret_cast<const uint2*>(oa.macro_ent)[e].x);
+  };
+  // pass 2: bucket counts
+  const bool in_smem = oa.nbucket <= kSmemBuckets;
+  unsigned long long* h = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.hist);
+  for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) h[b] = 0ull;
+  __syncthreads();
+  for (int64_t base = t0; base < t1; base += blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    const bool in = t < t1;
+    agg_inc<unsigned long long>(h, in ? key_of(t) : 0, in);
+  }
+  __syncthreads();
+  if (in_smem)
+    for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) oa.hist[b] = static_cast<int64_t>(h[b]);
+  __syncthreads();
+  // pass 3: ascending bucket starts, then one slot per tile in super-block enumeration order
+  block_scan_array(oa.hist, oa.bucket_pos, oa.nbucket, false, s_warp);
+  unsigned long long* pos = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.bucket_pos);
+  if (in_smem)
+    for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) pos[b] = static_cast<unsigned long long>(oa.bucket_pos[b]);
+  __syncthreads();
+  for (int64_t base = 0; base < n_enum; base += blockDim.x) {
+    const int64_t t = base + threadIdx.x < n_enum ? tile_of(base + threadIdx.x) : -1;
+    const bool in = t >= 0;
+    const unsigned long long slot = agg_inc<unsigned long long>(pos, in ? key_of(t) : 0, in);
+    if (in) oa.order[slot] = static_cast<int32_t>(t);
+    __syncwarp();
   }
 }
 
@@ -597,7 +633,8 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
   SkipArgs a{p.nA, p.nBt, p.pyr, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.tau, gi0, gi1, 0, 0,
              on_device ? p.d_range : nullptr, p.U, p.L,
              row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run};
-  OrderArgs oa{p.hist, p.bucket_pos, nbucket, p.U, p.L, p.order, p.totals, p.ticket, p.sched, order ? 1 : 0};
+  OrderArgs oa{p.hist,  p.bucket_pos, nbucket, p.U, p.L, p.macro_ent, MI * MJ > 32 ? 1 : 0, p.BK, p.GN, p.num_sms,
+              p.order, p.totals, p.ticket, p.sched, order ? 1 : 0};
   auto kern = skip_pyr_kernel<MI, MJ>;
   SPAMM_SET_SMEM(kern, kSmemBuckets * static_cast<int>(sizeof(unsigned long long)), p.device);
   kern<<<static_cast<unsigned>(blocks), kWarps * 32, dyn, s>>>(a, oa);

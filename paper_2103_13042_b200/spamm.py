@@ -69,6 +69,7 @@ def _load():
         "spamm_partition_rows": [PI64, I64, ctypes.c_int, PI64],
         "spamm_multiply_mgpu": [P, P, ctypes.c_int, ctypes.c_int, P, I64, P, I64, P, I64, U32, P],
         "spamm_multiply_mgpu_local": [PP, ctypes.c_int, P, I64, P, I64, PP, I64, U32, P],
+        "spamm_conv2d_im2col": [P, P, I64, P, I64, I64, I64, I64, I32, I32, I32, I32, P, I64, P],
         "spamm_get_norms": [P, PP, PP, PI64, PI64, PI64],
         "spamm_get_skipmap": [P, PP, PP, PI64],
         "spamm_get_counts": [P, PP, PP],
@@ -207,6 +208,19 @@ def spamm_set_norms(plan, nA, nB, stream=None) -> None:
     nA, nB = nA.contiguous(), nB.contiguous()
     _check(_lib.spamm_set_norms(plan, ctypes.c_void_p(nA.data_ptr()), ctypes.c_void_p(nB.data_ptr()),
                                 _stream(stream)))
+
+
+# ------------------------------------------------------- convolution drop-in ---
+def spamm_conv2d_im2col(plan, W, X, Y, kh: int = 3, kw: int = 3, stride: int = 1, pad: int = 1,
+                        stream=None) -> None:
+    """Y = SpAMM(W, im2col(X)) (Sec. 4.3.2).  X: contiguous (batch, C_in, H, W) CUDA tensor."""
+    if X.dim() != 4 or not X.is_contiguous():
+        raise ValueError("X must be a contiguous NCHW tensor")
+    w, ldw = _mat(W)
+    y, ldy = _mat(Y)
+    nb, ci, h, wd = X.shape
+    _check(_lib.spamm_conv2d_im2col(plan, w, ldw, ctypes.c_void_p(X.data_ptr()), nb, ci, h, wd, kh, kw, stride, pad,
+                                    y, ldy, _stream(stream)))
 
 
 # -------------------------------------------------------------- tau search ---

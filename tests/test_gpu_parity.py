@@ -247,8 +247,12 @@ def test_errors_and_state(sp):
         plan.multiply(A, A, C)
     assert e.value.status == sp.SPAMM_E_STATE
     with pytest.raises(sp.SpammError) as e:
-        plan.norms(torch.zeros((64, 64)), A)     # host pointer
+        sp.spamm_norms(plan.handle, torch.zeros((64, 64)), A)     # host pointer through the raw ABI
     assert e.value.status == sp.SPAMM_E_INVALID
+    with pytest.raises(ValueError):                               # the Plan wrapper checks dtype / shape
+        plan.norms(torch.zeros((64, 64), device="cuda", dtype=torch.bfloat16), A)
+    with pytest.raises(ValueError):
+        plan.norms(torch.zeros((64, 32), device="cuda"), A)
     with pytest.raises(sp.SpammError) as e:
         sp.Plan(64, 64, 64, 1.0, "fp32", tile=64)
     assert e.value.status == sp.SPAMM_E_UNSUPPORTED
