@@ -138,6 +138,26 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 
 void count_launch(int n = 1);
 
+// Launch with programmatic dependent launch (PDL, griddepcontrol): the kernel's CTAs may be
+// scheduled while its stream predecessor drains.  Every kernel launched this way calls
+// pdl_wait() (sm100.cuh) before it touches global memory its predecessors write, and
+// pdl_trigger() once its own CTAs run, so a stage's launch latency and prologue (barrier init,
+// TMEM allocation, descriptor prefetch) overlap the previous stage's tail.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // stage launchers (implemented in the .cu files) -----------------------------
 // norms of A's tile rows [ar0, ar1) and B's tile columns [bj0, bj1) in one launch
 spamm_status launch_norms2(Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t ar1, const void* B,

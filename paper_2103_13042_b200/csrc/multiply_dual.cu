@@ -93,19 +93,13 @@ template <uint32_t kFmt, bool kGen>
 __global__ void __launch_bounds__(kDThreads, 1)
     spamm_mul_dual_kernel(const __grid_constant__ DMaps mp, const int64_t* __restrict__ mstart,
                           const int64_t* __restrict__ mcount, const uint4* __restrict__ ment,
-                          const int32_t* __restrict__ order, int64_t n_tiles, int64_t t0,
+                          const int32_t* __restrict__ order, int64_t n_tiles,
                           const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
                           const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int use3d) {
-  if (rng != nullptr) {   // multi-GPU: the macro-row range was decided on the device
-    t0 = rng[0] * GN;
-    n_tiles = (rng[1] - rng[0]) * GN;
-  }
   // claims follow the skip map's order (skipmap.cu order_pass: LPT for few tiles per CTA, ascending
   // first kept k for many); the tiles without kept pairs come last and are zero-filled by the
   // epilogue warps (plain epilogue), or go through the pipeline (n_empty_p == nullptr)
-  const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
-  const int64_t n_work = n_tiles - n_empty;
   constexpr int wide_ok = 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -155,6 +149,11 @@ __global__ void __launch_bounds__(kDThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   if (tl && threadIdx.x == 0) stamp(1);
+  pdl_wait();      // the skip map (order, lists, counts) and the claim counters are ready
+  pdl_trigger();
+  if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU: range decided on the device
+  const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
+  const int64_t n_work = n_tiles - n_empty;
 
   // Zero-fill of the macro-tiles without kept pairs (the LPT tail of `order`), done LAST: an
   // epilogue warp whose CTA has no more tiles claims 32-row units (32 KB of C) from a global
@@ -735,11 +734,14 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   prof = prof_buf;
   cudaMemsetAsync(prof, 0, 1024 * 24 * 8, s);
 #endif
-  kern<<<grid, kDThreads, kDSmem, s>>>(mp, p.mstart, p.U, p.macro_run, p.order, n_tiles, p.row_begin_macro * p.GN,
-                                       p.range_on_device ? p.d_range : nullptr, kGen ? nullptr : p.totals + 2, p.GN, C, ldc,
-                                       p.M, p.N, p.sched, Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                       DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
-                                       prof, p.N % 32 == 0 ? 1 : 0);
+  SPAMM_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kDThreads), kDSmem, s, mp, static_cast<const int64_t*>(p.mstart),
+                            static_cast<const int64_t*>(p.U), static_cast<const uint4*>(p.macro_run),
+                            static_cast<const int32_t*>(p.order), n_tiles,
+                            static_cast<const int64_t*>(p.range_on_device ? p.d_range : nullptr),
+                            static_cast<const int64_t*>(kGen ? nullptr : p.totals + 2), p.GN, C, ldc, p.M, p.N, p.sched,
+                            Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
+                            DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
+                            prof, p.N % 32 == 0 ? 1 : 0));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
 #ifdef SPAMM_PROFILE

@@ -58,11 +58,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
                         const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
                         int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab,
-                        int64_t t0, const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p) {
-  if (rng != nullptr) {   // multi-GPU: the macro-row range was decided on the device
-    t0 = rng[0] * GN;
-    n_tiles = (rng[1] - rng[0]) * GN;
-  }
+                        const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p) {
+  if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU: range decided on the device
   // claims follow the skip map's order (skipmap.cu order_pass); every tile, with or without
   // k-steps, goes through the pipeline (the tiles without kept pairs are last)
   (void)n_empty_p;
@@ -358,7 +355,7 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
   spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, static_cast<const uint2*>(p.macro_ent),
                                                          p.order, n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
                                                          Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                                         p.row_begin_macro * p.GN, p.range_on_device ? p.d_range : nullptr,
+                                                         p.range_on_device ? p.d_range : nullptr,
                                                          p.totals + 2);
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());

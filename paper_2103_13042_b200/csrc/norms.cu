@@ -124,6 +124,8 @@ __global__ void __launch_bounds__(kThreads) tile_norms_kernel(const __grid_const
   __shared__ uint64_t full[kStages];
   __shared__ double part[kWarps][kBoxesPerCta * TPB];
 
+  pdl_wait();      // predecessors may write A (chained products) or read the counters zeroed below
+  pdl_trigger();
   if (zws != nullptr && blockIdx.x == 0 && blockIdx.y == 0)   // the skip map's counters (spamm_run)
     for (int i = threadIdx.x; i < zn; i += blockDim.x) zws[i] = 0;
   const bool isA = blockIdx.y < ja.nrow;
@@ -243,7 +245,7 @@ spamm_status launch_t(Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t 
   if (gx <= 0 || gy <= 0) return SPAMM_OK;
   if (gy > 65535) return fail(SPAMM_E_UNSUPPORTED, "more than 65535 tile rows in one norm launch");
   dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
-  tile_norms_kernel<T><<<grid, kThreads, smem_bytes<kStages>(), s>>>(tA, tB, ja, jb, zws, zn);
+  SPAMM_CUDA_TRY(launch_pdl(tile_norms_kernel<T>, grid, dim3(kThreads), smem_bytes<kStages>(), s, tA, tB, ja, jb, zws, zn));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;

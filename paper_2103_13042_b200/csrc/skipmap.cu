@@ -30,6 +30,7 @@
 #include <type_traits>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace spamm {
 namespace {
@@ -146,6 +147,8 @@ __global__ void __launch_bounds__(256)
                    int64_t GM, int64_t GN, int64_t NC, double* __restrict__ pyr) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  sm100::pdl_wait();
+  sm100::pdl_trigger();
   if (w >= (GM + GN) * NC) return;
   const int64_t g = w / NC, c = w % NC;
   const bool isA = g < GM;
@@ -230,8 +233,6 @@ struct OrderArgs {
   int64_t nbucket;       // BK + 1 (keys 0..BK)
   const int64_t* U;
   const int64_t* L;
-  const void* macro_ent; // first entry of macro-tile t at t*BK: its first kept k
-  int ent16;             // entries are 16 B (8 x 8 masks) else 8 B
   int64_t BK, GN;
   int num_sms;
   int32_t* order;
@@ -262,12 +263,13 @@ __device__ __forceinline__ T agg_inc(T* cnt, int64_t key, bool active) {
 // finish the skip map; `sbuf` = dynamic shared memory of kSmemBuckets words):
 //   * few tiles per CTA (n_work < 16 per SM): longest processing time first -- key BK - U, so the
 //     long tiles start first and the short ones fill the tail (Sec. 3.5.1's balance goal);
-//   * many tiles per CTA (balance is free): ascending first kept k -- on banded products the tiles
-//     of one "shell" (same max(I, J)) start at the same k and share A or B strips, and consecutive
-//     shells reuse each other's strips a few k-steps later, so the operands are read from DRAM
-//     about once instead of once per tile (the L2 holds the moving k-window);
+//   * many tiles per CTA (balance is free): the 12 x 12 super-block enumeration (row-major blocks,
+//     row-major tiles inside), so the ~148 tiles in flight share A row strips and B column strips
+//     in L2 (measured at N = 65536: 244 GB of DRAM reads for 728 GB of operand loads; ordering by
+//     the first kept k instead put tiles of one anti-diagonal -- no shared strips -- in flight
+//     together: 645 GB, multiply 68 -> 103 ms, profiles/r02c_kstart_*);
 //   * macro-tiles without kept pairs last (key BK; zero-filled by the multiply's epilogue warps).
-// Ties keep the 12 x 12 super-block enumeration (tiles in flight share strips in L2).
+// Ties keep the super-block enumeration.
 __device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t* s_warp, unsigned long long* sbuf) {
   const int64_t GN = oa.GN, GMr = (t1 - t0) / GN, nsbc = (GN + kOrdS - 1) / kOrdS;
   const int64_t n_enum = ((GMr + kOrdS - 1) / kOrdS) * nsbc * kOrdS * kOrdS;
@@ -308,14 +310,11 @@ __device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t*
     oa.totals[1] = te;
     oa.totals[2] = (t1 - t0) - tw;
   }
-  const bool by_k = tw >= 16 * static_cast<int64_t>(oa.num_sms);
+  const bool blocked = tw >= 16 * static_cast<int64_t>(oa.num_sms);
   auto key_of = [&](int64_t t) -> int64_t {
     const int64_t u = oa.U[t];
     if (u == 0) return oa.BK;
-    if (!by_k) return oa.BK - u;
-    const int64_t e = t * oa.BK;
-    return oa.ent16 ? static_cast<int64_t>(reinterpret_cast<const uint4*>(oa.macro_ent)[e].x)
-                    : static_cast<int64_t>(reinterpret_cast<const uint2*>(oa.macro_ent)[e].x);
+    return blocked ? 0 : oa.BK - u;
   };
   // pass 2: bucket counts
   const bool in_smem = oa.nbucket <= kSmemBuckets;
@@ -373,6 +372,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
   extern __shared__ unsigned long long s_dyn[];   // last CTA: histogram / bucket positions
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
+  sm100::pdl_wait();
+  sm100::pdl_trigger();
   int64_t gi0 = a.gi0, gi1 = a.gi1, ex0 = a.ex0, ex1 = a.ex1;
   if (a.d_range) {
     gi0 = a.d_range[0];
@@ -633,11 +634,11 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
   SkipArgs a{p.nA, p.nBt, p.pyr, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.tau, gi0, gi1, 0, 0,
              on_device ? p.d_range : nullptr, p.U, p.L,
              row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run};
-  OrderArgs oa{p.hist,  p.bucket_pos, nbucket, p.U, p.L, p.macro_ent, MI * MJ > 32 ? 1 : 0, p.BK, p.GN, p.num_sms,
+  OrderArgs oa{p.hist, p.bucket_pos, nbucket, p.U, p.L, p.BK, p.GN, p.num_sms,
               p.order, p.totals, p.ticket, p.sched, order ? 1 : 0};
   auto kern = skip_pyr_kernel<MI, MJ>;
   SPAMM_SET_SMEM(kern, kSmemBuckets * static_cast<int>(sizeof(unsigned long long)), p.device);
-  kern<<<static_cast<unsigned>(blocks), kWarps * 32, dyn, s>>>(a, oa);
+  SPAMM_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(kWarps * 32), dyn, s, a, oa));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
@@ -648,10 +649,9 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
 spamm_status launch_pyramid(Plan& p, cudaStream_t s) {
   const int64_t warps = (p.GM + p.GN) * p.NC;
   const unsigned blocks = static_cast<unsigned>((warps + 7) / 8);
-  if (p.MI == kMacroTC)
-    pyramid_kernel<kMacroTC, kMacroTC><<<blocks, 256, 0, s>>>(p.nA, p.nBt, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.pyr);
-  else
-    pyramid_kernel<kMacroF32, kMacroF32><<<blocks, 256, 0, s>>>(p.nA, p.nBt, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.pyr);
+  auto kern = p.MI == kMacroTC ? pyramid_kernel<kMacroTC, kMacroTC> : pyramid_kernel<kMacroF32, kMacroF32>;
+  SPAMM_CUDA_TRY(launch_pdl(kern, dim3(blocks), dim3(256), 0, s, static_cast<const double*>(p.nA),
+                            static_cast<const double*>(p.nBt), p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.pyr));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
   p.pyr_ready = true;

@@ -151,3 +151,32 @@ def test_dense_many_tiles_blocked_claims(sp):
     torch.cuda.synchronize()
     ref = Ab.astype(np.float64) @ Bb.astype(np.float64)
     assert _rel_fro(C.cpu().numpy(), ref) <= 1e-6
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32", "fp32x3"])
+def test_spamm_run_graph_capture(sp, prec):
+    """spamm_run is stream-ordered with no host synchronisation, so a whole SpAMM (norms -> pyramid
+    -> skip map -> multiply, PDL-chained) can be captured in a CUDA graph and replayed; replays
+    pick up new operand values in the same buffers."""
+    M, N, K = 1000, 768, 600
+    A1 = _rounded(synth.perturbed_decay_matrix(K, 0.97, seed=171, m=M), prec)
+    A2 = _rounded(synth.perturbed_decay_matrix(K, 0.97, seed=172, m=M), prec)
+    B = _rounded(synth.perturbed_decay_matrix(N, 0.97, seed=173, m=K), prec)
+    nA1, nA2, nB = oracle.tile_norms(A1, T), oracle.tile_norms(A2, T), oracle.tile_norms(B, T)
+    tau = _tau_at(nA1, nB, 0.5)
+    plan = sp.Plan(M, N, K, tau, prec)
+    Ad, Bd = _dev(A1, prec), _dev(B, prec)
+    C = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    plan.run(Ad, Bd, C)                       # warm-up outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sp.spamm_run(plan.handle, Ad, Bd, C)
+    bar = 1e-5
+    for A, nA in ((A2, nA2), (A1, nA1), (A2, nA2)):
+        Ad.copy_(torch.from_numpy(A).to(Ad.dtype))
+        C.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert _rel_fro(C.cpu().numpy(), oracle.spamm(A, B, tau, T, nA, nB)) <= bar
+        assert plan.stats()["kept"] == oracle.count_kept(nA, nB, tau)
