@@ -49,6 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    # experiments only (e.g. -DSPAMM_PROFILE for the multiply's per-CTA counters); never set by tests
+    cmd += os.environ.get("SPAMM_NVCC_FLAGS", "").split()
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

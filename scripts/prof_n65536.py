@@ -1,5 +1,6 @@
 """One N = 65536 (configs[4], exp. decay 0.999, BF16) multiply with the dual kernel's profiling
-counters on (SPAMM_DEBUG_UMMA_PROF=1): python scripts/prof_n65536.py [tau]"""
+counters on (library built with SPAMM_NVCC_FLAGS=-DSPAMM_PROFILE python -m paper_2103_13042_b200.build --force):
+   python scripts/prof_n65536.py [tau]"""
 import os
 import sys
 
