@@ -297,6 +297,25 @@ __global__ void __launch_bounds__(kDThreads, 1)
                 }
               }
             }
+#ifdef SPAMM_PF_DIST
+            // experiment: L2 prefetch of the A boxes SPAMM_PF_DIST k-steps beyond this stage
+            for (int j = 0; j < np; ++j) {
+              const int64_t ep = eb + q + j + SPAMM_PF_DIST;
+              if (ep >= cur.e1) break;
+              uint32_t p0 = 0, p1 = 0;
+              if (lane == 0) {
+                p0 = ment[2 * ep].x;
+                p1 = ment[2 * ep + 1].x;
+              }
+              p0 = __shfl_sync(0xffffffffu, p0, 0);
+              p1 = __shfl_sync(0xffffffffu, p1, 0);
+              const int32_t kp = static_cast<int32_t>(p0 & 0xFFFFu) * 32;
+              if (elect_one()) {
+                if ((p0 >> 16) & 15u) tma_prefetch_2d(&mp.a1, kp, I * 256);
+                if ((p1 >> 16) & 15u) tma_prefetch_2d(&mp.a1, kp, I * 256 + 128);
+              }
+            }
+#endif
             if (++s == kDStages) {
               s = 0;
               ph ^= 1;
@@ -392,6 +411,32 @@ __global__ void __launch_bounds__(kDThreads, 1)
                 }
               }
             }
+#ifdef SPAMM_PF_DIST
+            // experiment: L2 prefetch of the B column boxes SPAMM_PF_DIST k-steps beyond this stage
+            for (int j = 0; j < np && use3d; ++j) {
+              const int64_t ep = eb + q + j + SPAMM_PF_DIST;
+              if (ep >= cur.e1) break;
+              uint32_t p0 = 0, p1 = 0;
+              if (lane == 0) {
+                p0 = ment[2 * ep].x;
+                p1 = ment[2 * ep + 1].x;
+              }
+              p0 = __shfl_sync(0xffffffffu, p0, 0);
+              p1 = __shfl_sync(0xffffffffu, p1, 0);
+              const uint32_t cols = (p0 >> 24) | (p1 >> 24);
+              const int32_t kp = static_cast<int32_t>(p0 & 0xFFFFu) * 32;
+              const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
+              if (elect_one()) {
+                int off = c0;
+                if (len == 8) tma_prefetch_3d(&mp.b1[0], 0, kp, jb);
+                else {
+                  if (len & 4) { tma_prefetch_3d(&mp.b1[1], 0, kp, jb + off); off += 4; }
+                  if (len & 2) { tma_prefetch_3d(&mp.b1[2], 0, kp, jb + off); off += 2; }
+                  if (len & 1) { tma_prefetch_3d(&mp.b1[3], 0, kp, jb + off); }
+                }
+              }
+            }
+#endif
             if (++s == kDStages) {
               s = 0;
               ph ^= 1;
