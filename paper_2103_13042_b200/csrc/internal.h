@@ -101,6 +101,11 @@ struct Plan {
   std::vector<int64_t> last_partition;
   cudaStream_t last_stream = nullptr;
 
+  // zero-fill of the macro-tiles without kept pairs on a side stream, concurrent with the tensor
+  // multiply (created on first use): fork / join events
+  cudaStream_t zf_stream = nullptr;
+  cudaEvent_t zf_fork = nullptr, zf_join = nullptr;
+
   // timing
   cudaEvent_t ev[6] = {};
   bool ev_norms = false, ev_skip = false, ev_mul = false;

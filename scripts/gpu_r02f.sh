@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round-2 GPU session F: multiply experiments at N = 65536 / 16384 / 8192 -- L2 prefetch distance of
-# the operand boxes (build-time -DSPAMM_PF_DIST), and the per-CTA issuer counters (-DSPAMM_PROFILE).
+# the operand boxes (build-time -DSPAMM_PF_DIST), zero-fill on a side stream (-DSPAMM_ZF_SIDE), and the
+# per-CTA issuer counters (-DSPAMM_PROFILE).
 OUT=gpurun_out/r02f
 mkdir -p $OUT
 run() {  # $1 = tag, $2 = nvcc flags
@@ -11,9 +12,11 @@ run() {  # $1 = tag, $2 = nvcc flags
   done
 }
 run base ""
+run zfside "-DSPAMM_ZF_SIDE"
 run pf4 "-DSPAMM_PF_DIST=4"
 run pf8 "-DSPAMM_PF_DIST=8"
 run pf16 "-DSPAMM_PF_DIST=16"
+run zfside_pf8 "-DSPAMM_ZF_SIDE -DSPAMM_PF_DIST=8"
 run base2 ""
 SPAMM_NVCC_FLAGS="-DSPAMM_PROFILE" python -m paper_2103_13042_b200.build --force > /dev/null
 timeout 300 python scripts/prof_n65536.py 1e-6 > $OUT/prof_counters_65536.log 2>&1; tail -6 $OUT/prof_counters_65536.log
