@@ -27,6 +27,7 @@
 // The per-C-tile k lists are expanded from the macro lists only on request (leaf_expand).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <type_traits>
 
 #include "internal.h"
@@ -240,6 +241,7 @@ struct OrderArgs {
   unsigned int* ticket;
   unsigned int* sched;   // the multiply's claim counters [4], zeroed by the last CTA
   int enabled;           // 0: no order pass (multi-GPU provisional range)
+  unsigned long long* prof;   // SPAMM_PROFILE: [0] first CTA start, [1] last CTA enters the order pass, [2] end
 };
 constexpr int kSmemBuckets = 4096;
 constexpr int64_t kOrdS = 12;   // tie order: 12 x 12 super-blocks of macro-tiles, row-major inside
@@ -373,6 +375,13 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   sm100::pdl_wait();
+#ifdef SPAMM_PROFILE
+  if (oa.prof && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    atomicMin(oa.prof, g);
+  }
+#endif
   sm100::pdl_trigger();
   int64_t gi0 = a.gi0, gi1 = a.gi1, ex0 = a.ex0, ex1 = a.ex1;
   if (a.d_range) {
@@ -519,9 +528,16 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+#ifdef SPAMM_PROFILE
+  if (oa.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(oa.prof[1]));
+#endif
   order_pass(oa, gi0 * a.GN, gi1 * a.GN, s_warp, s_dyn);
   if (threadIdx.x == 0) *oa.ticket = 0u;
   if (threadIdx.x < 4 && oa.sched) oa.sched[threadIdx.x] = 0u;
+#ifdef SPAMM_PROFILE
+  __syncthreads();
+  if (oa.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(oa.prof[2]));
+#endif
 }
 
 // Per-C-tile k lists (C tile (i,j) owns slots [(i*BN+j)*BK, +V)) expanded from the macro lists:
@@ -635,11 +651,27 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
              on_device ? p.d_range : nullptr, p.U, p.L,
              row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run};
   OrderArgs oa{p.hist, p.bucket_pos, nbucket, p.U, p.L, p.BK, p.GN, p.num_sms,
-              p.order, p.totals, p.ticket, p.sched, order ? 1 : 0};
+              p.order, p.totals, p.ticket, p.sched, order ? 1 : 0, nullptr};
+#ifdef SPAMM_PROFILE
+  static unsigned long long* prof = nullptr;
+  if (!prof) cudaMalloc(&prof, 64);
+  const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+  cudaMemcpyAsync(prof, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  oa.prof = prof;
+#endif
   auto kern = skip_pyr_kernel<MI, MJ>;
   SPAMM_SET_SMEM(kern, kSmemBuckets * static_cast<int>(sizeof(unsigned long long)), p.device);
   SPAMM_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(kWarps * 32), dyn, s, a, oa));
   count_launch();
+#ifdef SPAMM_PROFILE
+  if (order) {
+    unsigned long long h[3];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[skip prof] main part %.2f us, order pass %.2f us (%lld macro-tiles)\n", (h[1] - h[0]) * 1e-3,
+            (h[2] - h[1]) * 1e-3, static_cast<long long>((gi1 - gi0) * p.GN));
+  }
+#endif
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
 }

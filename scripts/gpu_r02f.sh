@@ -20,4 +20,7 @@ run zfside_pf8 "-DSPAMM_ZF_SIDE -DSPAMM_PF_DIST=8"
 run base2 ""
 SPAMM_NVCC_FLAGS="-DSPAMM_PROFILE" python -m paper_2103_13042_b200.build --force > /dev/null
 timeout 300 python scripts/prof_n65536.py 1e-6 > $OUT/prof_counters_65536.log 2>&1; tail -6 $OUT/prof_counters_65536.log
+for n in 8192 16384; do
+  timeout 300 python bench.py --n $n --lam 0.99 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > /dev/null 2> $OUT/prof_counters_$n.log; tail -5 $OUT/prof_counters_$n.log
+done
 python -m paper_2103_13042_b200.build --force > /dev/null
