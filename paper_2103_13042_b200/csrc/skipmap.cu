@@ -323,10 +323,17 @@ __device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t*
   unsigned long long* h = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.hist);
   for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) h[b] = 0ull;
   __syncthreads();
-  for (int64_t base = t0; base < t1; base += blockDim.x) {
-    const int64_t t = base + threadIdx.x;
-    const bool in = t < t1;
-    agg_inc<unsigned long long>(h, in ? key_of(t) : 0, in);
+  // (keys of kBatch iterations are loaded before their atomics: independent loads in flight)
+  constexpr int kBatch = 8;
+  for (int64_t base = t0; base < t1; base += static_cast<int64_t>(blockDim.x) * kBatch) {
+    int64_t key[kBatch];
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+      key[r] = t < t1 ? key_of(t) : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) agg_inc<unsigned long long>(h, key[r] < 0 ? 0 : key[r], key[r] >= 0);
   }
   __syncthreads();
   if (in_smem)
@@ -338,12 +345,20 @@ __device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t*
   if (in_smem)
     for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) pos[b] = static_cast<unsigned long long>(oa.bucket_pos[b]);
   __syncthreads();
-  for (int64_t base = 0; base < n_enum; base += blockDim.x) {
-    const int64_t t = base + threadIdx.x < n_enum ? tile_of(base + threadIdx.x) : -1;
-    const bool in = t >= 0;
-    const unsigned long long slot = agg_inc<unsigned long long>(pos, in ? key_of(t) : 0, in);
-    if (in) oa.order[slot] = static_cast<int32_t>(t);
-    __syncwarp();
+  for (int64_t base = 0; base < n_enum; base += static_cast<int64_t>(blockDim.x) * kBatch) {
+    int64_t tt[kBatch], key[kBatch];
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const int64_t idx = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+      tt[r] = idx < n_enum ? tile_of(idx) : -1;
+      key[r] = tt[r] >= 0 ? key_of(tt[r]) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {   // one 256-wide window at a time keeps the enumeration order
+      const unsigned long long slot = agg_inc<unsigned long long>(pos, key[r], tt[r] >= 0);
+      if (tt[r] >= 0) oa.order[slot] = static_cast<int32_t>(tt[r]);
+      __syncthreads();
+    }
   }
 }
 
