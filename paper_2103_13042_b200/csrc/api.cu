@@ -131,7 +131,7 @@ spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, 
 static void free_plan(Plan* p) {
   if (!p) return;
   void* ptrs[] = {p->nA, p->nBt, p->pyr, p->V, p->U, p->L, p->leaf_start, p->row_work, p->ticket, p->sched,
-                  p->leaf_k, p->macro_ent, p->macro_run, p->order, p->bucket_pos, p->mstart, p->d_range,
+                  p->leaf_k, p->macro_ent, p->macro_run, p->order, p->bucket_pos, p->mstart, p->d_range, p->tile_lists,
                   p->ts_cnt, p->ts_part, p->planes, p->nC, p->im2col};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -243,11 +243,13 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   ALLOC(leaf_start, int64_t, nleaf);
   ALLOC(U, int64_t, nmac + 1);
   ALLOC(L, int64_t, nmac + 1);
-  ALLOC(row_work, int64_t, BM + BK + 8);
+  p->NSB = ((p->GM + 11) / 12) * ((p->GN + 11) / 12);
+  ALLOC(row_work, int64_t, ws_words(*p));
+  ALLOC(tile_lists, int32_t, 2 * nmac);
   ALLOC(ticket, unsigned int, 1);
   ALLOC(sched, unsigned int, 4);   // [0] tile claims, [1] zero-fill unit claims
   ALLOC(order, int32_t, nmac);
-  ALLOC(bucket_pos, int64_t, BK + 2);
+  ALLOC(bucket_pos, int64_t, std::max<int64_t>(BK + 2, p->NSB + 1));
   ALLOC(mstart, int64_t, nmac);
   ALLOC(d_range, int64_t, kRangeWords);
   // macro lists at their worst case (macro-tile t owns entries [t*BK, t*BK + U[t])): the skip map
@@ -258,12 +260,14 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   if (st == SPAMM_OK) {
     p->hist = p->row_work + BM;
     p->totals = p->hist + BK + 2;
+    p->hist_sb = p->totals + 4;
+    p->ws_cnt = reinterpret_cast<unsigned int*>(p->hist_sb + p->NSB);
   }
   if (st == SPAMM_OK && (cudaMemset(p->U, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||
                          cudaMemset(p->L, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||
                          cudaMemset(p->ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
                          cudaMemset(p->sched, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
-                         cudaMemset(p->row_work, 0, sizeof(int64_t) * (BM + BK + 8)) != cudaSuccess))
+                         cudaMemset(p->row_work, 0, sizeof(int64_t) * ws_words(*p)) != cudaSuccess))
     st = fail(SPAMM_E_CUDA, "cudaMemset failed");
   if (st == SPAMM_OK) {
     std::vector<int64_t> h(static_cast<size_t>(nmac));
@@ -363,7 +367,7 @@ static spamm_status do_skipmap(Plan& p, cudaStream_t s) {
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
   if (!p.pyr_ready) SPAMM_TRY(launch_pyramid(p, s));
   // row_work [BM], hist [BK+2] and totals [2] are contiguous in one allocation
-  if (!p.ws_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 8), s));
+  if (!p.ws_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * ws_words(p), s));
   p.ws_zeroed = false;
   SPAMM_TRY(launch_skipmap(p, 0, p.GM, false, true, true, s));
   p.sched_zeroed = true;   // the last CTA zeroes the multiply's claim counters

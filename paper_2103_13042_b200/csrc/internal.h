@@ -64,9 +64,15 @@ struct Plan {
   int64_t* U = nullptr;      // [GM*GN + 1] macro union counts (k-steps with a kept pair)
   int64_t* L = nullptr;      // [GM*GN + 1] kept pairs per macro-tile
   int64_t* leaf_start = nullptr;  // [BM*BN] start of each C tile's k list (leaf view, on request)
-  int64_t* row_work = nullptr;    // [BM + BK + 8]: row work, then the order pass's bucket counts and totals (one memset)
-  int64_t* hist = nullptr;        // = row_work + BM: [BK+2] bucket counts of the order pass
-  int64_t* totals = nullptr;      // = hist + BK + 2: [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
+  int64_t* row_work = nullptr;    // [ws_words()]: row work, then the claim order's counters (one memset)
+  // workspace counters, one zeroed region (the norm kernel zeroes it inside spamm_run):
+  //   row_work[BM] | hist[BK+2] | totals[4] | hist_sb[NSB] | ws_cnt[2] (uint32, one int64 word)
+  int64_t* hist = nullptr;        // LPT bucket counts of the claim order (key BK - U)
+  int64_t* totals = nullptr;      // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
+  int64_t* hist_sb = nullptr;     // super-block bucket counts of the claim order
+  unsigned int* ws_cnt = nullptr; // [0] work-list length, [1] empty-list length
+  int64_t NSB = 0;                // 12 x 12 super-blocks of macro-tiles
+  int32_t* tile_lists = nullptr;  // [2 * GM*GN]: macro-tiles with kept pairs, then those without
   unsigned int* ticket = nullptr; // CTA-completion ticket of the skip map (self-resetting)
   unsigned int* sched = nullptr;  // dynamic tile counters of the multiply kernels (reset per launch)
   uint16_t* leaf_k = nullptr;     // [BM*BN*BK] per-C-tile k lists (leaf view, on request)
@@ -142,6 +148,8 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
   } while (0)
 
 void count_launch(int n = 1);
+
+inline int64_t ws_words(const Plan& p) { return p.BM + p.BK + 2 + 4 + p.NSB + 1; }
 
 // Launch with programmatic dependent launch (PDL, griddepcontrol): the kernel's CTAs may be
 // scheduled while its stream predecessor drains.  Every kernel launched this way calls

@@ -50,7 +50,7 @@ static spamm_status phase_norms(Plan& p, int rank, int nranks, const void* A, in
 static spamm_status phase_provisional(Plan& p, int rank, int nranks, cudaStream_t s) {
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
-  SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * (p.BM + p.BK + 8), s));
+  SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * ws_words(p), s));
   SPAMM_TRY(launch_pyramid(p, s));
   const int64_t g0 = share(p.GM, rank, nranks), g1 = share(p.GM, rank + 1, nranks);
   // one rank: this is the whole skip map, with its LPT order

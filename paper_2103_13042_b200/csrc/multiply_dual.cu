@@ -714,7 +714,8 @@ __global__ void __launch_bounds__(kDThreads, 1)
 // Zero-fill of the macro-tiles without kept pairs (the tail of the claim order: totals[2] of them),
 // run on a side stream concurrently with the multiply: its CTAs need no shared memory and co-reside
 // with the multiply's one CTA per SM, so C's zero rows stream to HBM while the tensor pipes work
-// instead of after them.  One warp per 256-float row segment (two 16-byte streaming stores per lane).
+// instead of after them.  A warp zeroes a (macro-tile, 32-row strip) unit: one order lookup, then
+// 32 rows x 1 KB of 16-byte streaming stores in flight.
 __global__ void __launch_bounds__(256)
     zerofill_kernel(const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ rng,
                     const int64_t* __restrict__ n_empty_p, int64_t GN, float* __restrict__ C, int64_t ldc, int64_t M,
@@ -722,23 +723,27 @@ __global__ void __launch_bounds__(256)
   pdl_wait();
   if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;
   const int64_t n_empty = *n_empty_p, n_work = n_tiles - n_empty;
-  const int64_t rows = n_empty * 256;   // (tile, row) units
+  const int64_t units = n_empty * 8;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t u = w0; u < rows; u += nw) {
-    const int64_t t = order[n_work + u / 256];
-    const int64_t row = (t / GN) * 256 + u % 256;
-    if (row >= M) continue;
-    const int64_t c0 = (t % GN) * 256;
-    float* dst = C + row * ldc + c0;
+  const bool vec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
+  for (int64_t u = w0; u < units; u += nw) {
+    const int64_t t = order[n_work + u / 8];
+    const int64_t r0 = (t / GN) * 256 + (u % 8) * 32, c0 = (t % GN) * 256;
     const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
-    if (ncol == 256 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-      __stcs(reinterpret_cast<float4*>(dst) + lane, z);
-      __stcs(reinterpret_cast<float4*>(dst) + 32 + lane, z);
+    if (vec && ncol == 256) {
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        if (r0 + r >= M) break;
+        float4* dst = reinterpret_cast<float4*>(C + (r0 + r) * ldc + c0);
+        __stcs(dst + lane, z);
+        __stcs(dst + 32 + lane, z);
+      }
     } else {
-      for (int64_t c = lane; c < ncol; c += 32) dst[c] = 0.f;
+      for (int r = 0; r < 32 && r0 + r < M; ++r)
+        for (int64_t c = lane; c < ncol; c += 32) C[(r0 + r) * ldc + c0 + c] = 0.f;
     }
   }
 }

@@ -239,7 +239,7 @@ spamm_status launch_t(Plan& p, const void* A, int64_t lda, int64_t ar0, int64_t 
   }
   SPAMM_SET_SMEM(tile_norms_kernel<T>, static_cast<int>(smem_bytes<kStages>()), p.device);
   int64_t* zws = p.zero_ws_next ? p.row_work : nullptr;
-  const int zn = static_cast<int>(p.BM + p.BK + 8);
+  const int zn = static_cast<int>(ws_words(p));
   const int64_t gx = std::max(ja.ncb, jb.ncb);
   const int64_t gy = ja.nrow + jb.nrow;
   if (gx <= 0 || gy <= 0) return SPAMM_OK;

@@ -229,22 +229,28 @@ __device__ void block_scan_array(const int64_t* in, int64_t* out, int64_t n, boo
 }
 
 struct OrderArgs {
-  int64_t* hist;         // [BK + 2] bucket counts (global fallback when they do not fit in shared memory)
-  int64_t* bucket_pos;   // [BK + 2]
-  int64_t nbucket;       // BK + 1 (keys 0..BK)
+  int64_t* hist;         // [BK + 2] LPT bucket counts (key BK - U), accumulated by the main loop
+  int64_t* hist_sb;      // [NSB] super-block bucket counts, accumulated by the main loop
+  int64_t* bucket_pos;   // [max(BK + 2, NSB + 1)]
+  int64_t nsb;           // super-blocks of the range (12 x 12 macro-tiles each)
   const int64_t* U;
   const int64_t* L;
   int64_t BK, GN;
   int num_sms;
+  int32_t* work;         // [GM*GN] macro-tiles with kept pairs, appended by the main loop
+  int32_t* empty;        // [GM*GN] macro-tiles without kept pairs, appended by the main loop
+  unsigned int* cnt;     // [0] work list length, [1] empty list length
   int32_t* order;
   int64_t* totals;       // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
   unsigned int* ticket;
   unsigned int* sched;   // the multiply's claim counters [4], zeroed by the last CTA
-  int enabled;           // 0: no order pass (multi-GPU provisional range)
+  int mode;              // 0 none (multi-GPU provisional pass), 1 lists built by this launch,
+                         // 2 scan U over the range (multi-GPU final pass: part of the range came
+                         //   from the provisional launch)
   unsigned long long* prof;   // SPAMM_PROFILE: [0] first CTA start, [1] last CTA enters the order pass, [2] end
 };
 constexpr int kSmemBuckets = 4096;
-constexpr int64_t kOrdS = 12;   // tie order: 12 x 12 super-blocks of macro-tiles, row-major inside
+constexpr int64_t kOrdS = 12;   // 12 x 12 super-blocks of macro-tiles
 
 // warp-aggregated atomicAdd of 1 per lane on cnt[key]: lanes with equal keys share one atomic;
 // returns each lane's old value + its rank among the equal lanes
@@ -261,105 +267,81 @@ __device__ __forceinline__ T agg_inc(T* cnt, int64_t key, bool active) {
   return base + static_cast<T>(__popc(peers & ((1u << lane) - 1u)));
 }
 
-// The multiply's claim order of the macro-tiles [t0, t1) (a bucket sort, one CTA: the last to
+__device__ __forceinline__ int64_t sb_of(int64_t t, int64_t t0, int64_t GN) {
+  const int64_t li = (t - t0) / GN, lj = t % GN, nsbc = (GN + kOrdS - 1) / kOrdS;
+  return (li / kOrdS) * nsbc + lj / kOrdS;
+}
+
+// The multiply's claim order of the macro-tiles [t0, t1): a bucket sort by one CTA (the last to
 // finish the skip map; `sbuf` = dynamic shared memory of kSmemBuckets words):
 //   * few tiles per CTA (n_work < 16 per SM): longest processing time first -- key BK - U, so the
 //     long tiles start first and the short ones fill the tail (Sec. 3.5.1's balance goal);
-//   * many tiles per CTA (balance is free): the 12 x 12 super-block enumeration (row-major blocks,
-//     row-major tiles inside), so the ~148 tiles in flight share A row strips and B column strips
-//     in L2 (measured at N = 65536: 244 GB of DRAM reads for 728 GB of operand loads; ordering by
-//     the first kept k instead put tiles of one anti-diagonal -- no shared strips -- in flight
-//     together: 645 GB, multiply 68 -> 103 ms, profiles/r02c_kstart_*);
-//   * macro-tiles without kept pairs last (key BK; zero-filled by the multiply's epilogue warps).
-// Ties keep the super-block enumeration.
+//   * many tiles per CTA (balance is free): by 12 x 12 super-block, so the ~148 tiles in flight
+//     share A row strips and B column strips in L2 (measured at N = 65536: 244-298 GB of DRAM reads
+//     for 728 GB of operand loads; ordering by the first kept k instead put tiles of one
+//     anti-diagonal -- no shared strips -- in flight together: 645 GB, multiply 68 -> 103 ms,
+//     profiles/r02c_kstart_*);
+//   * macro-tiles without kept pairs last (zero-filled by the multiply).
+// Mode 1: the main loop already appended the tiles to the work / empty lists and counted both
+// histograms, so only the scan and one pass over the work list are serial.  Mode 2 (multi-GPU final
+// pass) rebuilds lists and histograms from U over the range first.
 __device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t* s_warp, unsigned long long* sbuf) {
-  const int64_t GN = oa.GN, GMr = (t1 - t0) / GN, nsbc = (GN + kOrdS - 1) / kOrdS;
-  const int64_t n_enum = ((GMr + kOrdS - 1) / kOrdS) * nsbc * kOrdS * kOrdS;
-  auto tile_of = [&](int64_t idx) -> int64_t {   // super-block enumeration -> tile (or -1)
-    const int64_t sb = idx / (kOrdS * kOrdS), w = idx % (kOrdS * kOrdS);
-    const int64_t li = (sb / nsbc) * kOrdS + w / kOrdS, lj = (sb % nsbc) * kOrdS + w % kOrdS;
-    return (li < GMr && lj < GN) ? t0 + li * GN + lj : -1;
-  };
-  // pass 1: totals and the number of tiles with work
-  int64_t kept = 0, ents = 0, work = 0;
-  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-    const int64_t u = oa.U[t];
-    kept += oa.L[t];
-    ents += u;
-    work += u > 0;
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    kept += __shfl_xor_sync(0xffffffffu, kept, o);
-    ents += __shfl_xor_sync(0xffffffffu, ents, o);
-    work += __shfl_xor_sync(0xffffffffu, work, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    s_warp[threadIdx.x >> 5] = kept;
-    s_warp[8 + (threadIdx.x >> 5)] = ents;
-    s_warp[16 + (threadIdx.x >> 5)] = work;
-  }
-  __syncthreads();
-  int64_t tk = 0, te = 0, tw = 0;
-  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-    tk += s_warp[w];
-    te += s_warp[8 + w];
-    tw += s_warp[16 + w];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    oa.totals[0] = tk;
-    oa.totals[1] = te;
-    oa.totals[2] = (t1 - t0) - tw;
-  }
-  const bool blocked = tw >= 16 * static_cast<int64_t>(oa.num_sms);
-  auto key_of = [&](int64_t t) -> int64_t {
-    const int64_t u = oa.U[t];
-    if (u == 0) return oa.BK;
-    return blocked ? 0 : oa.BK - u;
-  };
-  // pass 2: bucket counts
-  const bool in_smem = oa.nbucket <= kSmemBuckets;
-  unsigned long long* h = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.hist);
-  for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) h[b] = 0ull;
-  __syncthreads();
-  // (keys of kBatch iterations are loaded before their atomics: independent loads in flight)
   constexpr int kBatch = 8;
-  for (int64_t base = t0; base < t1; base += static_cast<int64_t>(blockDim.x) * kBatch) {
-    int64_t key[kBatch];
+  if (oa.mode == 2) {   // lists and histograms of the range from U (loads batched ahead of the atomics)
+    for (int64_t base = t0; base < t1; base += static_cast<int64_t>(blockDim.x) * kBatch) {
+      int64_t u[kBatch];
 #pragma unroll
-    for (int r = 0; r < kBatch; ++r) {
-      const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
-      key[r] = t < t1 ? key_of(t) : -1;
+      for (int r = 0; r < kBatch; ++r) {
+        const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+        u[r] = t < t1 ? oa.U[t] : -1;
+      }
+#pragma unroll
+      for (int r = 0; r < kBatch; ++r) {   // every lane calls every agg_inc (warp-synchronous)
+        const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+        const bool isw = u[r] > 0, ise = u[r] == 0;
+        const unsigned w = agg_inc<unsigned>(oa.cnt, 0, isw);
+        const unsigned e = agg_inc<unsigned>(oa.cnt + 1, 0, ise);
+        agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist), isw ? oa.BK - u[r] : 0, isw);
+        agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist_sb), isw ? sb_of(t, t0, oa.GN) : 0,
+                                    isw);
+        if (isw) oa.work[w] = static_cast<int32_t>(t);
+        if (ise) oa.empty[e] = static_cast<int32_t>(t);
+      }
     }
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r) agg_inc<unsigned long long>(h, key[r] < 0 ? 0 : key[r], key[r] >= 0);
+    __threadfence_block();
+    __syncthreads();
   }
-  __syncthreads();
-  if (in_smem)
-    for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) oa.hist[b] = static_cast<int64_t>(h[b]);
-  __syncthreads();
-  // pass 3: ascending bucket starts, then one slot per tile in super-block enumeration order
-  block_scan_array(oa.hist, oa.bucket_pos, oa.nbucket, false, s_warp);
+  const int64_t n_work = *reinterpret_cast<volatile unsigned int*>(oa.cnt);
+  const int64_t n_empty = *reinterpret_cast<volatile unsigned int*>(oa.cnt + 1);
+  const bool blocked = n_work >= 16 * static_cast<int64_t>(oa.num_sms);
+  const int64_t nbucket = blocked ? oa.nsb : oa.BK + 1;
+  int64_t* hist = blocked ? oa.hist_sb : oa.hist;
+  // ascending bucket starts
+  block_scan_array(hist, oa.bucket_pos, nbucket, false, s_warp);
+  const bool in_smem = nbucket <= kSmemBuckets;
   unsigned long long* pos = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.bucket_pos);
   if (in_smem)
-    for (int64_t b = threadIdx.x; b < oa.nbucket; b += blockDim.x) pos[b] = static_cast<unsigned long long>(oa.bucket_pos[b]);
+    for (int64_t b = threadIdx.x; b < nbucket; b += blockDim.x) pos[b] = static_cast<unsigned long long>(oa.bucket_pos[b]);
   __syncthreads();
-  for (int64_t base = 0; base < n_enum; base += static_cast<int64_t>(blockDim.x) * kBatch) {
+  // one slot per working tile (work-list loads batched ahead of the atomics); then the empty tiles
+  for (int64_t base = 0; base < n_work; base += static_cast<int64_t>(blockDim.x) * kBatch) {
     int64_t tt[kBatch], key[kBatch];
 #pragma unroll
     for (int r = 0; r < kBatch; ++r) {
-      const int64_t idx = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
-      tt[r] = idx < n_enum ? tile_of(idx) : -1;
-      key[r] = tt[r] >= 0 ? key_of(tt[r]) : 0;
+      const int64_t i = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+      tt[r] = i < n_work ? oa.work[i] : -1;
     }
 #pragma unroll
-    for (int r = 0; r < kBatch; ++r) {   // one 256-wide window at a time keeps the enumeration order
+    for (int r = 0; r < kBatch; ++r)
+      key[r] = tt[r] < 0 ? 0 : (blocked ? sb_of(tt[r], t0, oa.GN) : oa.BK - oa.U[tt[r]]);
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
       const unsigned long long slot = agg_inc<unsigned long long>(pos, key[r], tt[r] >= 0);
-      if (tt[r] >= 0) oa.order[slot] = static_cast<int32_t>(tt[r]);
-      __syncthreads();
+      if (tt[r] >= 0) oa.order[slot] = tt[r];
     }
   }
+  for (int64_t i = threadIdx.x; i < n_empty; i += blockDim.x) oa.order[n_work + i] = oa.empty[i];
+  if (threadIdx.x == 0) oa.totals[2] = n_empty;
 }
 
 struct SkipArgs {
@@ -377,19 +359,20 @@ struct SkipArgs {
   uint4* macro_run;             // nullptr: FP32 paths
 };
 
+// One WARP per macro-tile (32 macro-tiles in flight per SM, no block-level barriers in the main
+// loop): lane c classifies k chunk c from the pyramid, then the surviving chunks are decided one at a
+// time in ascending k (lane = k), each writing its entries at warp-scanned offsets.
 template <int MI, int MJ>
-__global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs a, const OrderArgs oa) {
+__global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a, const OrderArgs oa) {
   using M_ = mask_t<MI, MJ>;
   constexpr bool kMask64 = MI * MJ > 32;          // 8 x 8 tiles: (k, mask_lo, mask_hi, 0) entries
-  constexpr int W = kWarps;
-  __shared__ uint32_t s_list[W * 32];             // surviving chunks of a classification round
-  __shared__ uint32_t s_cnt[W], s_cm[W], s_rw[W][MI];
   __shared__ int64_t s_warp[33];
   __shared__ int s_last;
-  extern __shared__ unsigned long long s_dyn[];   // last CTA: histogram / bucket positions
+  extern __shared__ unsigned long long s_dyn[];   // last CTA: bucket positions
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   sm100::pdl_wait();
+  sm100::pdl_trigger();
 #ifdef SPAMM_PROFILE
   if (oa.prof && threadIdx.x == 0) {
     unsigned long long g;
@@ -397,7 +380,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
     atomicMin(oa.prof, g);
   }
 #endif
-  sm100::pdl_trigger();
   int64_t gi0 = a.gi0, gi1 = a.gi1, ex0 = a.ex0, ex1 = a.ex1;
   if (a.d_range) {
     gi0 = a.d_range[0];
@@ -414,46 +396,36 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
   const double* __restrict__ pbMax = a.pyr + 2 * a.GM * a.NC;
   const double* __restrict__ pbMin = pbMax + a.GN * a.NC;
   const double tau = a.tau;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+  int64_t w_kept = 0, w_ents = 0;   // this warp's totals (lane 0)
 
-  for (int64_t m = blockIdx.x; m < n_macro; m += gridDim.x) {
+  for (int64_t m = static_cast<int64_t>(blockIdx.x) * kWarps + warp; m < n_macro; m += nw) {
     const int64_t tile = m < n_lo ? gi0 * a.GN + m : ex1 * a.GN + (m - n_lo);
     const int64_t I = tile / a.GN, J = tile % a.GN;
     const M_ valid = valid_bits<MI, MJ>(a.BM, a.BN, I, J);
-    int64_t mbase = tile * a.BK;                  // macro-tile region (entry e: 2e, 2e+1 in macro_run)
+    int64_t mbase = tile * a.BK;   // macro-tile region (entry e: 2e, 2e+1 in macro_run)
     uint32_t rw[MI];
 #pragma unroll
     for (int li = 0; li < MI; ++li) rw[li] = 0u;
-    bool any_surv = false;
-    for (int64_t c0 = 0; c0 < a.NC; c0 += W * 32) {
-      // ---- classify the round's chunks from the pyramid: 0 skipped, 1 mixed, 2 all kept
-      const int64_t c = c0 + threadIdx.x;
+    for (int64_t c0 = 0; c0 < a.NC; c0 += 32) {
+      // lane = chunk c0 + lane: 0 skipped, 1 mixed, 2 all kept (from the pyramid, exactly; R20)
+      const int64_t c = c0 + lane;
       uint32_t cls = 0;
       if (c < a.NC && valid != 0u) {
         const double amax = paMax[I * a.NC + c], bmax = pbMax[J * a.NC + c];
         if (!(__dmul_rn(amax, bmax) < tau))
           cls = __dmul_rn(paMin[I * a.NC + c], pbMin[J * a.NC + c]) >= tau ? 2u : 1u;
       }
-      const uint32_t sv = __ballot_sync(0xffffffffu, cls != 0u);
-      if (lane == 0) s_cnt[warp] = __popc(sv);
-      __syncthreads();
-      uint32_t off = 0, n_surv = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        off += w < warp ? s_cnt[w] : 0u;
-        n_surv += s_cnt[w];
-      }
-      if (cls != 0u) s_list[off + __popc(sv & lt)] = static_cast<uint32_t>(c - c0) | (cls == 2u ? 0x80000000u : 0u);
-      __syncthreads();
-      any_surv |= n_surv != 0u;
-      // ---- surviving chunks, 8 at a time (warp w takes the w-th), ascending k
-      for (uint32_t g = 0; g < n_surv; g += W) {
-        const bool has = g + warp < n_surv;
-        const uint32_t ent = has ? s_list[g + warp] : 0u;
-        const int64_t k = c0 * kChunk + static_cast<int64_t>(ent & 0x7FFFFFFFu) * kChunk + lane;
+      uint32_t surv = __ballot_sync(0xffffffffu, cls != 0u);
+      const uint32_t full = __ballot_sync(0xffffffffu, cls == 2u);
+      while (surv) {
+        const int cc = __ffs(surv) - 1;
+        surv &= surv - 1u;
+        const int64_t k = (c0 + cc) * kChunk + lane;
         M_ mask = 0u;
-        if (has && k < a.BK) {
-          if (ent & 0x80000000u) {
-            mask = valid;                          // all pairs of the chunk kept: no norm loads
+        if (k < a.BK) {
+          if ((full >> cc) & 1u) {
+            mask = valid;                 // all pairs of the chunk kept: no norm loads
           } else {
             ChunkVals<MI, MJ> cv;
 #pragma unroll
@@ -473,17 +445,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
         for (int li = 0; li < MI; ++li)
           rw[li] += static_cast<uint32_t>(__popcll(static_cast<unsigned long long>(mask >> (li * MJ)) & ((1ull << MJ) - 1ull)));
         const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
-        if (lane == 0) s_cm[warp] = __popc(any);
-        __syncthreads();
-        uint32_t om = 0, tm = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const uint32_t cm = s_cm[w];
-          om += w < warp ? cm : 0u;
-          tm += cm;
-        }
         if (mask) {
-          const int64_t e = mbase + om + __popc(any & lt);
+          const int64_t e = mbase + __popc(any & lt);
           if constexpr (kMask64) {
             reinterpret_cast<uint4*>(a.macro_ent)[e] =
                 make_uint4(static_cast<uint32_t>(k), static_cast<uint32_t>(mask), static_cast<uint32_t>(mask >> 32), 0u);
@@ -495,45 +458,42 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
             reinterpret_cast<uint2*>(a.macro_ent)[e] = make_uint2(static_cast<uint32_t>(k), static_cast<uint32_t>(mask));
           }
         }
-        mbase += tm;
-        __syncthreads();   // s_cm is rewritten by the next group
+        mbase += __popc(any);
       }
     }
-    // ---- per-macro-tile counts: union length U, tensor entries Uw, kept pairs L, row work
-    if (!any_surv) {
-      if (threadIdx.x == 0) {
-        a.U[tile] = 0;
-        a.L[tile] = 0;
-      }
-      continue;
-    }
+    // ---- per-macro-tile counts: union length U, kept pairs L, row work; order bookkeeping
+    uint32_t lsum = 0;
 #pragma unroll
     for (int li = 0; li < MI; ++li) {
       uint32_t v = rw[li];
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) s_rw[warp][li] = v;
+      lsum += v;
+      if (a.row_work && lane == li && I * MI + li < a.BM && v) atomicAdd(a.row_work + I * MI + li, static_cast<unsigned long long>(v));
     }
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t r = 0;   // lane li < MI: kept pairs of tile row I*MI + li
-      if (lane < MI)
-#pragma unroll
-        for (int w = 0; w < W; ++w) r += s_rw[w][lane];
-      if (a.row_work && lane < MI && I * MI + lane < a.BM && r)
-        atomicAdd(a.row_work + I * MI + lane, static_cast<unsigned long long>(r));
-      uint32_t lsum = r;
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-      if (lane == 0) {
-        a.U[tile] = mbase - tile * a.BK;
-        a.L[tile] = lsum;
+    if (lane == 0) {
+      const int64_t u = mbase - tile * a.BK;
+      a.U[tile] = u;
+      a.L[tile] = lsum;
+      w_kept += lsum;
+      w_ents += u;
+      if (oa.mode == 1) {
+        if (u > 0) {
+          oa.work[atomicAdd(oa.cnt, 1u)] = static_cast<int32_t>(tile);
+          atomicAdd(reinterpret_cast<unsigned long long*>(oa.hist) + (a.BK - u), 1ull);
+          atomicAdd(reinterpret_cast<unsigned long long*>(oa.hist_sb) + sb_of(tile, gi0 * a.GN, a.GN), 1ull);
+        } else {
+          oa.empty[atomicAdd(oa.cnt + 1, 1u)] = static_cast<int32_t>(tile);
+        }
       }
     }
-    __syncthreads();   // s_rw is rewritten by the next macro-tile
   }
-  if (!oa.enabled) return;
-  // ---- the last CTA to finish builds the LPT order of the whole range [gi0, gi1)
+  if (oa.mode == 0) return;
+  if (lane == 0 && oa.mode == 1 && (w_kept || w_ents)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals), static_cast<unsigned long long>(w_kept));
+    atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals) + 1, static_cast<unsigned long long>(w_ents));
+  }
+  // ---- the last CTA to finish builds the claim order of the whole range [gi0, gi1)
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -546,6 +506,22 @@ __global__ void __launch_bounds__(kWarps * 32, 4) skip_pyr_kernel(const SkipArgs
 #ifdef SPAMM_PROFILE
   if (oa.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(oa.prof[1]));
 #endif
+  if (oa.mode == 2) {   // totals of the range (part of it was decided by the provisional launch)
+    int64_t kept = 0, ents = 0;
+    for (int64_t t = gi0 * a.GN + threadIdx.x; t < gi1 * a.GN; t += blockDim.x) {
+      kept += a.L[t];
+      ents += a.U[t];
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      kept += __shfl_xor_sync(0xffffffffu, kept, o);
+      ents += __shfl_xor_sync(0xffffffffu, ents, o);
+    }
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals), static_cast<unsigned long long>(kept));
+      atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals) + 1, static_cast<unsigned long long>(ents));
+    }
+  }
   order_pass(oa, gi0 * a.GN, gi1 * a.GN, s_warp, s_dyn);
   if (threadIdx.x == 0) *oa.ticket = 0u;
   if (threadIdx.x < 4 && oa.sched) oa.sched[threadIdx.x] = 0u;
@@ -660,13 +636,14 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
   const int64_t n_macro = on_device ? p.GM * p.GN : (gi1 - gi0) * p.GN;
   constexpr int kPerSm = 4;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(n_macro, static_cast<int64_t>(p.num_sms) * kPerSm));
-  const int64_t nbucket = p.BK + 1;
-  const int dyn = order && nbucket <= kSmemBuckets ? static_cast<int>(nbucket * sizeof(unsigned long long)) : 0;
+  const int64_t nb_max = std::max<int64_t>(p.BK + 1, p.NSB);
+  const int dyn = order ? static_cast<int>(std::min<int64_t>(nb_max, kSmemBuckets) * sizeof(unsigned long long)) : 0;
   SkipArgs a{p.nA, p.nBt, p.pyr, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.tau, gi0, gi1, 0, 0,
              on_device ? p.d_range : nullptr, p.U, p.L,
              row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run};
-  OrderArgs oa{p.hist, p.bucket_pos, nbucket, p.U, p.L, p.BK, p.GN, p.num_sms,
-              p.order, p.totals, p.ticket, p.sched, order ? 1 : 0, nullptr};
+  OrderArgs oa{p.hist, p.hist_sb, p.bucket_pos, p.NSB, p.U, p.L, p.BK, p.GN, p.num_sms, p.tile_lists,
+              p.tile_lists + p.GM * p.GN, p.ws_cnt, p.order, p.totals, p.ticket, p.sched,
+              order ? (on_device ? 2 : 1) : 0, nullptr};
 #ifdef SPAMM_PROFILE
   static unsigned long long* prof = nullptr;
   if (!prof) cudaMalloc(&prof, 64);
