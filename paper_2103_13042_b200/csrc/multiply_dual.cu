@@ -829,12 +829,6 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
     }
     SPAMM_CUDA_TRY(cudaEventRecord(p.zf_fork, s));
     SPAMM_CUDA_TRY(cudaStreamWaitEvent(p.zf_stream, p.zf_fork, 0));
-    zerofill_kernel<<<2 * p.num_sms, 256, 0, p.zf_stream>>>(p.order, n_tiles,
-                                                           p.range_on_device ? p.d_range : nullptr, p.totals + 2,
-                                                           p.GN, C, ldc, p.M, p.N);
-    count_launch();
-    SPAMM_CUDA_TRY(cudaGetLastError());
-    SPAMM_CUDA_TRY(cudaEventRecord(p.zf_join, p.zf_stream));
   }
   unsigned long long* prof = nullptr;
 #ifdef SPAMM_PROFILE
@@ -851,7 +845,22 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
                             Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                             DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
                             prof, p.N % 32 == 0 ? 1 : 0, side_zf ? 0 : 1));
-  if (side_zf) SPAMM_CUDA_TRY(cudaStreamWaitEvent(s, p.zf_join, 0));
+  if (side_zf) {
+    // launched after the multiply so its CTAs take the SMs first; the zero-fill CTAs (no shared
+    // memory) keep the SMs' maximum shared-memory carveout so both kernels co-reside
+    static std::atomic<unsigned long long> carve{0};
+    if (!(carve.load() & (1ull << (p.device & 63)))) {
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(zerofill_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      carve.fetch_or(1ull << (p.device & 63));
+    }
+    zerofill_kernel<<<2 * p.num_sms, 256, 0, p.zf_stream>>>(p.order, n_tiles,
+                                                           p.range_on_device ? p.d_range : nullptr, p.totals + 2,
+                                                           p.GN, C, ldc, p.M, p.N);
+    count_launch();
+    SPAMM_CUDA_TRY(cudaGetLastError());
+    SPAMM_CUDA_TRY(cudaEventRecord(p.zf_join, p.zf_stream));
+    SPAMM_CUDA_TRY(cudaStreamWaitEvent(s, p.zf_join, 0));
+  }
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
 #ifdef SPAMM_PROFILE

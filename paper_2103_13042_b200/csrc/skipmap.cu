@@ -267,9 +267,12 @@ __device__ __forceinline__ T agg_inc(T* cnt, int64_t key, bool active) {
   return base + static_cast<T>(__popc(peers & ((1u << lane) - 1u)));
 }
 
+// super-block of macro-tile t in the range starting at tile t0 (32-bit arithmetic: tile ids < 2^31)
 __device__ __forceinline__ int64_t sb_of(int64_t t, int64_t t0, int64_t GN) {
-  const int64_t li = (t - t0) / GN, lj = t % GN, nsbc = (GN + kOrdS - 1) / kOrdS;
-  return (li / kOrdS) * nsbc + lj / kOrdS;
+  const uint32_t gn = static_cast<uint32_t>(GN), nsbc = (gn + kOrdS - 1) / kOrdS;
+  const uint32_t rel = static_cast<uint32_t>(t - t0), row0 = static_cast<uint32_t>(t0) / gn;
+  const uint32_t li = rel / gn, lj = (static_cast<uint32_t>(t) - row0 * gn - li * gn);
+  return static_cast<int64_t>((li / static_cast<uint32_t>(kOrdS)) * nsbc + lj / static_cast<uint32_t>(kOrdS));
 }
 
 // The multiply's claim order of the macro-tiles [t0, t1): a bucket sort by one CTA (the last to
@@ -340,7 +343,19 @@ __device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t*
       if (tt[r] >= 0) oa.order[slot] = tt[r];
     }
   }
-  for (int64_t i = threadIdx.x; i < n_empty; i += blockDim.x) oa.order[n_work + i] = oa.empty[i];
+  for (int64_t base = 0; base < n_empty; base += static_cast<int64_t>(blockDim.x) * kBatch) {
+    int32_t v[kBatch];
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const int64_t i = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+      v[r] = i < n_empty ? oa.empty[i] : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const int64_t i = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
+      if (i < n_empty) oa.order[n_work + i] = v[r];
+    }
+  }
   if (threadIdx.x == 0) oa.totals[2] = n_empty;
 }
 
