@@ -130,16 +130,13 @@ spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, 
 
 static void free_plan(Plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->nA, p->nBt, p->pyr, p->V, p->U, p->L, p->leaf_start, p->row_work, p->ticket, p->sched,
+  void* ptrs[] = {p->nA, p->nBt, p->pyr, p->V, p->U, p->L, p->leaf_start, p->row_work, p->sched,
                   p->leaf_k, p->macro_ent, p->macro_run, p->order, p->bucket_pos, p->mstart, p->d_range, p->tile_lists,
                   p->ts_cnt, p->ts_part, p->planes, p->nC, p->im2col};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
-  if (p->zf_fork) cudaEventDestroy(p->zf_fork);
-  if (p->zf_join) cudaEventDestroy(p->zf_join);
-  if (p->zf_stream) cudaStreamDestroy(p->zf_stream);
   delete p;
 }
 
@@ -246,7 +243,6 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->NSB = ((p->GM + 11) / 12) * ((p->GN + 11) / 12);
   ALLOC(row_work, int64_t, ws_words(*p));
   ALLOC(tile_lists, int32_t, 2 * nmac);
-  ALLOC(ticket, unsigned int, 1);
   ALLOC(sched, unsigned int, 4);   // [0] tile claims, [1] zero-fill unit claims
   ALLOC(order, int32_t, nmac);
   ALLOC(bucket_pos, int64_t, std::max<int64_t>(BK + 2, p->NSB + 1));
@@ -262,10 +258,10 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     p->totals = p->hist + BK + 2;
     p->hist_sb = p->totals + 4;
     p->ws_cnt = reinterpret_cast<unsigned int*>(p->hist_sb + p->NSB);
+    p->bucket_cnt = p->hist_sb + p->NSB + 2;
   }
   if (st == SPAMM_OK && (cudaMemset(p->U, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||
                          cudaMemset(p->L, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||
-                         cudaMemset(p->ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
                          cudaMemset(p->sched, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
                          cudaMemset(p->row_work, 0, sizeof(int64_t) * ws_words(*p)) != cudaSuccess))
     st = fail(SPAMM_E_CUDA, "cudaMemset failed");

@@ -66,14 +66,15 @@ struct Plan {
   int64_t* leaf_start = nullptr;  // [BM*BN] start of each C tile's k list (leaf view, on request)
   int64_t* row_work = nullptr;    // [ws_words()]: row work, then the claim order's counters (one memset)
   // workspace counters, one zeroed region (the norm kernel zeroes it inside spamm_run):
-  //   row_work[BM] | hist[BK+2] | totals[4] | hist_sb[NSB] | ws_cnt[2] (uint32, one int64 word)
+  //   row_work[BM] | hist[BK+2] | totals[4] | hist_sb[NSB] | ws_cnt[4] (uint32, two int64 words) |
+  //   bucket_cnt[NB], NB = max(BK + 2, NSB + 1)
   int64_t* hist = nullptr;        // LPT bucket counts of the claim order (key BK - U)
   int64_t* totals = nullptr;      // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
   int64_t* hist_sb = nullptr;     // super-block bucket counts of the claim order
-  unsigned int* ws_cnt = nullptr; // [0] work-list length, [1] empty-list length
+  unsigned int* ws_cnt = nullptr; // [0] work-list length, [1] empty-list length, [2], [3] skip-map tile claims
+  int64_t* bucket_cnt = nullptr;  // claim-order slots taken per bucket
   int64_t NSB = 0;                // 12 x 12 super-blocks of macro-tiles
   int32_t* tile_lists = nullptr;  // [2 * GM*GN]: macro-tiles with kept pairs, then those without
-  unsigned int* ticket = nullptr; // CTA-completion ticket of the skip map (self-resetting)
   unsigned int* sched = nullptr;  // dynamic tile counters of the multiply kernels (reset per launch)
   uint16_t* leaf_k = nullptr;     // [BM*BN*BK] per-C-tile k lists (leaf view, on request)
   void* macro_ent = nullptr;      // [GM*GN*BK] (k, mask) entries, 8 B (4 x 4) or 16 B (8 x 8)
@@ -106,11 +107,6 @@ struct Plan {
   int64_t row_begin_macro = 0, row_end_macro = 0;   // macro-row range the skip map / multiply covers
   std::vector<int64_t> last_partition;
   cudaStream_t last_stream = nullptr;
-
-  // zero-fill of the macro-tiles without kept pairs on a side stream, concurrent with the tensor
-  // multiply (created on first use): fork / join events
-  cudaStream_t zf_stream = nullptr;
-  cudaEvent_t zf_fork = nullptr, zf_join = nullptr;
 
   // timing
   cudaEvent_t ev[6] = {};
@@ -149,7 +145,8 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 
 void count_launch(int n = 1);
 
-inline int64_t ws_words(const Plan& p) { return p.BM + p.BK + 2 + 4 + p.NSB + 1; }
+inline int64_t ws_buckets(const Plan& p) { return p.BK + 2 > p.NSB + 1 ? p.BK + 2 : p.NSB + 1; }
+inline int64_t ws_words(const Plan& p) { return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p); }
 
 // Launch with programmatic dependent launch (PDL, griddepcontrol): the kernel's CTAs may be
 // scheduled while its stream predecessor drains.  Every kernel launched this way calls

@@ -96,8 +96,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
                           const int32_t* __restrict__ order, int64_t n_tiles,
                           const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
-                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int use3d,
-                          int zero_fill) {
+                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int use3d) {
   // claims follow the skip map's order (skipmap.cu order_pass: LPT for few tiles per CTA, ascending
   // first kept k for many); the tiles without kept pairs come last and are zero-filled by the
   // epilogue warps (plain epilogue), or go through the pipeline (n_empty_p == nullptr)
@@ -161,7 +160,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
   // counter, so the CTAs that finish their MMA work early absorb it (the slowest one takes
   // none).  Done greedily at the start instead, the 141 MB of zero writes at the bench point
   // compete with the operand loads' first DRAM touches (multiply 165 vs 152 us without them).
-  const int64_t n_units = zero_fill ? n_empty * 8 : 0;   // else zerofill_kernel on a side stream
+  const int64_t n_units = n_empty * 8;
   auto zero_unit = [&]() -> bool {
     unsigned int u32 = 0;
     if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
@@ -298,25 +297,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
                 }
               }
             }
-#ifdef SPAMM_PF_DIST
-            // experiment: L2 prefetch of the A boxes SPAMM_PF_DIST k-steps beyond this stage
-            for (int j = 0; j < np; ++j) {
-              const int64_t ep = eb + q + j + SPAMM_PF_DIST;
-              if (ep >= cur.e1) break;
-              uint32_t p0 = 0, p1 = 0;
-              if (lane == 0) {
-                p0 = ment[2 * ep].x;
-                p1 = ment[2 * ep + 1].x;
-              }
-              p0 = __shfl_sync(0xffffffffu, p0, 0);
-              p1 = __shfl_sync(0xffffffffu, p1, 0);
-              const int32_t kp = static_cast<int32_t>(p0 & 0xFFFFu) * 32;
-              if (elect_one()) {
-                if ((p0 >> 16) & 15u) tma_prefetch_2d(&mp.a1, kp, I * 256);
-                if ((p1 >> 16) & 15u) tma_prefetch_2d(&mp.a1, kp, I * 256 + 128);
-              }
-            }
-#endif
             if (++s == kDStages) {
               s = 0;
               ph ^= 1;
@@ -412,32 +392,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
                 }
               }
             }
-#ifdef SPAMM_PF_DIST
-            // experiment: L2 prefetch of the B column boxes SPAMM_PF_DIST k-steps beyond this stage
-            for (int j = 0; j < np && use3d; ++j) {
-              const int64_t ep = eb + q + j + SPAMM_PF_DIST;
-              if (ep >= cur.e1) break;
-              uint32_t p0 = 0, p1 = 0;
-              if (lane == 0) {
-                p0 = ment[2 * ep].x;
-                p1 = ment[2 * ep + 1].x;
-              }
-              p0 = __shfl_sync(0xffffffffu, p0, 0);
-              p1 = __shfl_sync(0xffffffffu, p1, 0);
-              const uint32_t cols = (p0 >> 24) | (p1 >> 24);
-              const int32_t kp = static_cast<int32_t>(p0 & 0xFFFFu) * 32;
-              const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
-              if (elect_one()) {
-                int off = c0;
-                if (len == 8) tma_prefetch_3d(&mp.b1[0], 0, kp, jb);
-                else {
-                  if (len & 4) { tma_prefetch_3d(&mp.b1[1], 0, kp, jb + off); off += 4; }
-                  if (len & 2) { tma_prefetch_3d(&mp.b1[2], 0, kp, jb + off); off += 2; }
-                  if (len & 1) { tma_prefetch_3d(&mp.b1[3], 0, kp, jb + off); }
-                }
-              }
-            }
-#endif
             if (++s == kDStages) {
               s = 0;
               ph ^= 1;
@@ -711,43 +665,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
   if (tl && threadIdx.x == 0) stamp(5);
 }
 
-// Zero-fill of the macro-tiles without kept pairs (the tail of the claim order: totals[2] of them),
-// run on a side stream concurrently with the multiply: its CTAs need no shared memory and co-reside
-// with the multiply's one CTA per SM, so C's zero rows stream to HBM while the tensor pipes work
-// instead of after them.  A warp zeroes a (macro-tile, 32-row strip) unit: one order lookup, then
-// 32 rows x 1 KB of 16-byte streaming stores in flight.
-__global__ void __launch_bounds__(256)
-    zerofill_kernel(const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ rng,
-                    const int64_t* __restrict__ n_empty_p, int64_t GN, float* __restrict__ C, int64_t ldc, int64_t M,
-                    int64_t N) {
-  pdl_wait();
-  if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;
-  const int64_t n_empty = *n_empty_p, n_work = n_tiles - n_empty;
-  const int64_t units = n_empty * 8;
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  const bool vec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
-  for (int64_t u = w0; u < units; u += nw) {
-    const int64_t t = order[n_work + u / 8];
-    const int64_t r0 = (t / GN) * 256 + (u % 8) * 32, c0 = (t % GN) * 256;
-    const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
-    if (vec && ncol == 256) {
-#pragma unroll 4
-      for (int r = 0; r < 32; ++r) {
-        if (r0 + r >= M) break;
-        float4* dst = reinterpret_cast<float4*>(C + (r0 + r) * ldc + c0);
-        __stcs(dst + lane, z);
-        __stcs(dst + 32 + lane, z);
-      }
-    } else {
-      for (int r = 0; r < 32 && r0 + r < M; ++r)
-        for (int64_t c = lane; c < ncol; c += 32) C[(r0 + r) * ldc + c0 + c] = 0.f;
-    }
-  }
-}
-
 #ifdef SPAMM_PROFILE
 // per-CTA issuer counters and a globaltimer timeline (compile with -DSPAMM_PROFILE)
 static void print_profile(const unsigned long long* hp, int grid) {
@@ -780,15 +697,6 @@ static void print_profile(const unsigned long long* hp, int grid) {
 }
 #endif
 
-// experiment switch while it is measured (build-time): zero-fill on a side stream
-inline bool zf_side_enabled() {
-#ifdef SPAMM_ZF_SIDE
-  return true;
-#else
-  return false;
-#endif
-}
-
 template <uint32_t kFmt, bool kGen>
 spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                            cudaStream_t s, CUtensorMapDataType dt) {
@@ -819,17 +727,6 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
   if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, 2 * sizeof(unsigned int), s));
   p.sched_zeroed = false;
-  // the plain epilogue's zero-fill of empty macro-tiles runs on a side stream, concurrently
-  const bool side_zf = !kGen && zf_side_enabled();
-  if (side_zf) {
-    if (!p.zf_stream) {
-      SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&p.zf_stream, cudaStreamNonBlocking));
-      SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&p.zf_fork, cudaEventDisableTiming));
-      SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&p.zf_join, cudaEventDisableTiming));
-    }
-    SPAMM_CUDA_TRY(cudaEventRecord(p.zf_fork, s));
-    SPAMM_CUDA_TRY(cudaStreamWaitEvent(p.zf_stream, p.zf_fork, 0));
-  }
   unsigned long long* prof = nullptr;
 #ifdef SPAMM_PROFILE
   static unsigned long long* prof_buf = nullptr;
@@ -844,23 +741,7 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
                             static_cast<const int64_t*>(kGen ? nullptr : p.totals + 2), p.GN, C, ldc, p.M, p.N, p.sched,
                             Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                             DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
-                            prof, p.N % 32 == 0 ? 1 : 0, side_zf ? 0 : 1));
-  if (side_zf) {
-    // launched after the multiply so its CTAs take the SMs first; the zero-fill CTAs (no shared
-    // memory) keep the SMs' maximum shared-memory carveout so both kernels co-reside
-    static std::atomic<unsigned long long> carve{0};
-    if (!(carve.load() & (1ull << (p.device & 63)))) {
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(zerofill_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      carve.fetch_or(1ull << (p.device & 63));
-    }
-    zerofill_kernel<<<2 * p.num_sms, 256, 0, p.zf_stream>>>(p.order, n_tiles,
-                                                           p.range_on_device ? p.d_range : nullptr, p.totals + 2,
-                                                           p.GN, C, ldc, p.M, p.N);
-    count_launch();
-    SPAMM_CUDA_TRY(cudaGetLastError());
-    SPAMM_CUDA_TRY(cudaEventRecord(p.zf_join, p.zf_stream));
-    SPAMM_CUDA_TRY(cudaStreamWaitEvent(s, p.zf_join, 0));
-  }
+                            prof, p.N % 32 == 0 ? 1 : 0));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
 #ifdef SPAMM_PROFILE

@@ -19,10 +19,10 @@
 //             (lane = k); the 8 warps of a CTA take 8 surviving chunks at a time in ascending k
 //             and write, at offsets scanned across the warps, the macro-tile's (k, keep mask)
 //             list and, for the tensor path, each k-step's MMA runs pre-decoded per 128-row half;
-//   order   : the last CTA (threadfence + ticket) histograms the union lengths of the range's
-//             macro-tiles, scans the histogram in descending order and scatters every
-//             macro-tile into its bucket: a longest-processing-time-first schedule without a
-//             sort, plus the totals (kept pairs, k-steps).
+//   order   : the main loop appends every macro-tile to a work or an empty list and counts two
+//             histograms (LPT key BK - U; 12 x 12 super-block); a grid-wide scatter kernel places the
+//             work list by bucket (a bucket sort, no comparison sort) and appends the empty tiles:
+//             the multiply's claim order, plus the totals (kept pairs, k-steps).
 // Row work (Sec. 3.5.1's V summed over a row) and kept counts are popcounts of the masks.
 // The per-C-tile k lists are expanded from the macro lists only on request (leaf_expand).
 #include <algorithm>
@@ -229,25 +229,23 @@ __device__ void block_scan_array(const int64_t* in, int64_t* out, int64_t n, boo
 }
 
 struct OrderArgs {
-  int64_t* hist;         // [BK + 2] LPT bucket counts (key BK - U), accumulated by the main loop
-  int64_t* hist_sb;      // [NSB] super-block bucket counts, accumulated by the main loop
-  int64_t* bucket_pos;   // [max(BK + 2, NSB + 1)]
-  int64_t nsb;           // super-blocks of the range (12 x 12 macro-tiles each)
+  int64_t* hist;         // [BK + 2] LPT bucket counts (key BK - U)
+  int64_t* hist_sb;      // [NSB] super-block bucket counts
+  int64_t* bucket_cnt;   // [max(BK + 2, NSB + 1)] slots taken per bucket (zeroed with the workspace)
+  int64_t* bucket_pos;   // [max(BK + 2, NSB + 1)] bucket starts (only when they exceed shared memory)
+  int64_t nsb;
   const int64_t* U;
   const int64_t* L;
   int64_t BK, GN;
   int num_sms;
-  int32_t* work;         // [GM*GN] macro-tiles with kept pairs, appended by the main loop
-  int32_t* empty;        // [GM*GN] macro-tiles without kept pairs, appended by the main loop
-  unsigned int* cnt;     // [0] work list length, [1] empty list length
+  int32_t* work;         // [GM*GN] macro-tiles with kept pairs
+  int32_t* empty;        // [GM*GN] macro-tiles without kept pairs
+  unsigned int* cnt;     // [0] work-list length, [1] empty-list length, [2] skip-map tile claims
   int32_t* order;
   int64_t* totals;       // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
-  unsigned int* ticket;
-  unsigned int* sched;   // the multiply's claim counters [4], zeroed by the last CTA
-  int mode;              // 0 none (multi-GPU provisional pass), 1 lists built by this launch,
-                         // 2 scan U over the range (multi-GPU final pass: part of the range came
-                         //   from the provisional launch)
-  unsigned long long* prof;   // SPAMM_PROFILE: [0] first CTA start, [1] last CTA enters the order pass, [2] end
+  unsigned int* sched;   // the multiply's claim counters [4]
+  const int64_t* d_range;   // multi-GPU: range [d_range[0], d_range[1]) of macro rows, else t0 / t1
+  int64_t t0, t1;
 };
 constexpr int kSmemBuckets = 4096;
 constexpr int64_t kOrdS = 12;   // 12 x 12 super-blocks of macro-tiles
@@ -275,88 +273,97 @@ __device__ __forceinline__ int64_t sb_of(int64_t t, int64_t t0, int64_t GN) {
   return static_cast<int64_t>((li / static_cast<uint32_t>(kOrdS)) * nsbc + lj / static_cast<uint32_t>(kOrdS));
 }
 
-// The multiply's claim order of the macro-tiles [t0, t1): a bucket sort by one CTA (the last to
-// finish the skip map; `sbuf` = dynamic shared memory of kSmemBuckets words):
+__device__ __forceinline__ void order_range(const OrderArgs& oa, int64_t& t0, int64_t& t1) {
+  t0 = oa.t0;
+  t1 = oa.t1;
+  if (oa.d_range) {
+    t0 = oa.d_range[0] * oa.GN;
+    t1 = oa.d_range[1] * oa.GN;
+  }
+}
+
+// The multiply's claim order of the macro-tiles of the range (a parallel bucket sort):
 //   * few tiles per CTA (n_work < 16 per SM): longest processing time first -- key BK - U, so the
 //     long tiles start first and the short ones fill the tail (Sec. 3.5.1's balance goal);
 //   * many tiles per CTA (balance is free): by 12 x 12 super-block, so the ~148 tiles in flight
-//     share A row strips and B column strips in L2 (measured at N = 65536: 244-298 GB of DRAM reads
-//     for 728 GB of operand loads; ordering by the first kept k instead put tiles of one
-//     anti-diagonal -- no shared strips -- in flight together: 645 GB, multiply 68 -> 103 ms,
-//     profiles/r02c_kstart_*);
+//     share A row strips and B column strips in L2 (ordering by the first kept k instead put tiles
+//     of one anti-diagonal -- no shared strips -- in flight together: 645 vs 244-298 GB of DRAM
+//     reads at N = 65536, multiply 68 -> 103 ms, profiles/r02c_kstart_*);
 //   * macro-tiles without kept pairs last (zero-filled by the multiply).
-// Mode 1: the main loop already appended the tiles to the work / empty lists and counted both
-// histograms, so only the scan and one pass over the work list are serial.  Mode 2 (multi-GPU final
-// pass) rebuilds lists and histograms from U over the range first.
-__device__ void order_pass(const OrderArgs& oa, int64_t t0, int64_t t1, int64_t* s_warp, unsigned long long* sbuf) {
-  constexpr int kBatch = 8;
-  if (oa.mode == 2) {   // lists and histograms of the range from U (loads batched ahead of the atomics)
-    for (int64_t base = t0; base < t1; base += static_cast<int64_t>(blockDim.x) * kBatch) {
-      int64_t u[kBatch];
-#pragma unroll
-      for (int r = 0; r < kBatch; ++r) {
-        const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
-        u[r] = t < t1 ? oa.U[t] : -1;
-      }
-#pragma unroll
-      for (int r = 0; r < kBatch; ++r) {   // every lane calls every agg_inc (warp-synchronous)
-        const int64_t t = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
-        const bool isw = u[r] > 0, ise = u[r] == 0;
-        const unsigned w = agg_inc<unsigned>(oa.cnt, 0, isw);
-        const unsigned e = agg_inc<unsigned>(oa.cnt + 1, 0, ise);
-        agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist), isw ? oa.BK - u[r] : 0, isw);
-        agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist_sb), isw ? sb_of(t, t0, oa.GN) : 0,
-                                    isw);
-        if (isw) oa.work[w] = static_cast<int32_t>(t);
-        if (ise) oa.empty[e] = static_cast<int32_t>(t);
-      }
+// The skip map's main loop appends the tiles to a work or an empty list and counts both
+// histograms; order_lists_kernel does that from U instead on the multi-GPU final pass (part of the
+// range was decided by the provisional launch).  order_scatter_kernel: every CTA scans the chosen
+// histogram into shared memory and places its share of the work list with one atomic per bucket
+// and lane group (global per-bucket counters).  Ties (same bucket) are in arbitrary order.
+__global__ void __launch_bounds__(256) order_lists_kernel(const OrderArgs oa) {
+  sm100::pdl_wait();
+  sm100::pdl_trigger();
+  int64_t t0, t1;
+  order_range(oa, t0, t1);
+  int64_t kept = 0, ents = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t base = t0 + static_cast<int64_t>(blockIdx.x) * blockDim.x; base < t1; base += stride) {
+    const int64_t t = base + threadIdx.x;
+    const int64_t u = t < t1 ? oa.U[t] : -1;
+    if (t < t1) {
+      kept += oa.L[t];
+      ents += u;
     }
-    __threadfence_block();
-    __syncthreads();
+    const bool isw = u > 0, ise = u == 0;   // every lane calls every agg_inc (warp-synchronous)
+    const unsigned w = agg_inc<unsigned>(oa.cnt, 0, isw);
+    const unsigned e = agg_inc<unsigned>(oa.cnt + 1, 0, ise);
+    agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist), isw ? oa.BK - u : 0, isw);
+    agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist_sb), isw ? sb_of(t, t0, oa.GN) : 0, isw);
+    if (isw) oa.work[w] = static_cast<int32_t>(t);
+    if (ise) oa.empty[e] = static_cast<int32_t>(t);
   }
-  const int64_t n_work = *reinterpret_cast<volatile unsigned int*>(oa.cnt);
-  const int64_t n_empty = *reinterpret_cast<volatile unsigned int*>(oa.cnt + 1);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    ents += __shfl_xor_sync(0xffffffffu, ents, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (kept || ents)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals), static_cast<unsigned long long>(kept));
+    atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals) + 1, static_cast<unsigned long long>(ents));
+  }
+}
+
+__global__ void __launch_bounds__(1024) order_scan_kernel(const OrderArgs oa) {   // > kSmemBuckets buckets only
+  __shared__ int64_t s_warp[33];
+  sm100::pdl_wait();
+  sm100::pdl_trigger();
+  const int64_t n_work = oa.cnt[0];
+  const bool blocked = n_work >= 16 * static_cast<int64_t>(oa.num_sms);
+  block_scan_array(blocked ? oa.hist_sb : oa.hist, oa.bucket_pos, blocked ? oa.nsb : oa.BK + 1, false, s_warp);
+}
+
+__global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa) {
+  __shared__ int64_t s_warp[33];
+  __shared__ int64_t s_pos[kSmemBuckets + 1];
+  sm100::pdl_wait();
+  sm100::pdl_trigger();
+  int64_t t0, t1;
+  order_range(oa, t0, t1);
+  const int64_t n_work = oa.cnt[0], n_empty = oa.cnt[1];
   const bool blocked = n_work >= 16 * static_cast<int64_t>(oa.num_sms);
   const int64_t nbucket = blocked ? oa.nsb : oa.BK + 1;
-  int64_t* hist = blocked ? oa.hist_sb : oa.hist;
-  // ascending bucket starts
-  block_scan_array(hist, oa.bucket_pos, nbucket, false, s_warp);
-  const bool in_smem = nbucket <= kSmemBuckets;
-  unsigned long long* pos = in_smem ? sbuf : reinterpret_cast<unsigned long long*>(oa.bucket_pos);
-  if (in_smem)
-    for (int64_t b = threadIdx.x; b < nbucket; b += blockDim.x) pos[b] = static_cast<unsigned long long>(oa.bucket_pos[b]);
-  __syncthreads();
-  // one slot per working tile (work-list loads batched ahead of the atomics); then the empty tiles
-  for (int64_t base = 0; base < n_work; base += static_cast<int64_t>(blockDim.x) * kBatch) {
-    int64_t tt[kBatch], key[kBatch];
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r) {
-      const int64_t i = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
-      tt[r] = i < n_work ? oa.work[i] : -1;
-    }
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r)
-      key[r] = tt[r] < 0 ? 0 : (blocked ? sb_of(tt[r], t0, oa.GN) : oa.BK - oa.U[tt[r]]);
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r) {
-      const unsigned long long slot = agg_inc<unsigned long long>(pos, key[r], tt[r] >= 0);
-      if (tt[r] >= 0) oa.order[slot] = tt[r];
-    }
+  const int64_t* base = oa.bucket_pos;
+  if (nbucket <= kSmemBuckets) {   // every CTA scans the (small) histogram itself
+    block_scan_array(blocked ? oa.hist_sb : oa.hist, s_pos, nbucket, false, s_warp);
+    base = s_pos;
   }
-  for (int64_t base = 0; base < n_empty; base += static_cast<int64_t>(blockDim.x) * kBatch) {
-    int32_t v[kBatch];
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r) {
-      const int64_t i = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
-      v[r] = i < n_empty ? oa.empty[i] : -1;
-    }
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r) {
-      const int64_t i = base + static_cast<int64_t>(r) * blockDim.x + threadIdx.x;
-      if (i < n_empty) oa.order[n_work + i] = v[r];
-    }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; b0 < n_work; b0 += stride) {
+    const int64_t i = b0 + threadIdx.x;
+    const int64_t t = i < n_work ? oa.work[i] : -1;
+    const int64_t key = t < 0 ? 0 : (blocked ? sb_of(t, t0, oa.GN) : oa.BK - oa.U[t]);
+    const unsigned long long r = agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.bucket_cnt), key, t >= 0);
+    if (t >= 0) oa.order[base[key] + static_cast<int64_t>(r)] = static_cast<int32_t>(t);
   }
-  if (threadIdx.x == 0) oa.totals[2] = n_empty;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_empty; i += stride)
+    oa.order[n_work + i] = oa.empty[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) oa.totals[2] = n_empty;
+  if (blockIdx.x == 0 && threadIdx.x < 4 && oa.sched) oa.sched[threadIdx.x] = 0u;
 }
 
 struct SkipArgs {
@@ -372,29 +379,22 @@ struct SkipArgs {
   unsigned long long* row_work; // nullptr: not accumulated (second multi-GPU pass)
   void* macro_ent;
   uint4* macro_run;             // nullptr: FP32 paths
+  unsigned int* claim;          // tile-claim counter (zeroed with the workspace; a second launch on the
+                                // same workspace -- the multi-GPU final pass -- uses its own)
 };
 
-// One WARP per macro-tile (32 macro-tiles in flight per SM, no block-level barriers in the main
-// loop): lane c classifies k chunk c from the pyramid, then the surviving chunks are decided one at a
-// time in ascending k (lane = k), each writing its entries at warp-scanned offsets.
+// One WARP per macro-tile (32 macro-tiles in flight per SM, no block-level barriers): warps claim
+// macro-tiles from a counter (a banded product's tiles differ widely in work); lane c classifies
+// k chunk c from the pyramid, then the surviving chunks are decided one at a time in ascending k
+// (lane = k), each writing its entries at warp-scanned offsets.
 template <int MI, int MJ>
-__global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a, const OrderArgs oa) {
+__global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a, const OrderArgs oa, int lists) {
   using M_ = mask_t<MI, MJ>;
   constexpr bool kMask64 = MI * MJ > 32;          // 8 x 8 tiles: (k, mask_lo, mask_hi, 0) entries
-  __shared__ int64_t s_warp[33];
-  __shared__ int s_last;
-  extern __shared__ unsigned long long s_dyn[];   // last CTA: bucket positions
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   sm100::pdl_wait();
   sm100::pdl_trigger();
-#ifdef SPAMM_PROFILE
-  if (oa.prof && threadIdx.x == 0) {
-    unsigned long long g;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-    atomicMin(oa.prof, g);
-  }
-#endif
   int64_t gi0 = a.gi0, gi1 = a.gi1, ex0 = a.ex0, ex1 = a.ex1;
   if (a.d_range) {
     gi0 = a.d_range[0];
@@ -411,10 +411,13 @@ __global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a,
   const double* __restrict__ pbMax = a.pyr + 2 * a.GM * a.NC;
   const double* __restrict__ pbMin = pbMax + a.GN * a.NC;
   const double tau = a.tau;
-  const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
   int64_t w_kept = 0, w_ents = 0;   // this warp's totals (lane 0)
 
-  for (int64_t m = static_cast<int64_t>(blockIdx.x) * kWarps + warp; m < n_macro; m += nw) {
+  for (;;) {
+    unsigned int mc = 0;
+    if (lane == 0) mc = atomicAdd(a.claim, 1u);
+    const int64_t m = __shfl_sync(0xffffffffu, mc, 0);
+    if (m >= n_macro) break;
     const int64_t tile = m < n_lo ? gi0 * a.GN + m : ex1 * a.GN + (m - n_lo);
     const int64_t I = tile / a.GN, J = tile % a.GN;
     const M_ valid = valid_bits<MI, MJ>(a.BM, a.BN, I, J);
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a,
         mbase += __popc(any);
       }
     }
-    // ---- per-macro-tile counts: union length U, kept pairs L, row work; order bookkeeping
+    // ---- per-macro-tile counts: union length U, kept pairs L, row work; the order's lists
     uint32_t lsum = 0;
 #pragma unroll
     for (int li = 0; li < MI; ++li) {
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a,
       a.L[tile] = lsum;
       w_kept += lsum;
       w_ents += u;
-      if (oa.mode == 1) {
+      if (lists) {
         if (u > 0) {
           oa.work[atomicAdd(oa.cnt, 1u)] = static_cast<int32_t>(tile);
           atomicAdd(reinterpret_cast<unsigned long long*>(oa.hist) + (a.BK - u), 1ull);
@@ -503,47 +506,10 @@ __global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a,
       }
     }
   }
-  if (oa.mode == 0) return;
-  if (lane == 0 && oa.mode == 1 && (w_kept || w_ents)) {
+  if (lane == 0 && lists && (w_kept || w_ents)) {
     atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals), static_cast<unsigned long long>(w_kept));
     atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals) + 1, static_cast<unsigned long long>(w_ents));
   }
-  // ---- the last CTA to finish builds the claim order of the whole range [gi0, gi1)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int t = atomicAdd(oa.ticket, 1u);
-    s_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-#ifdef SPAMM_PROFILE
-  if (oa.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(oa.prof[1]));
-#endif
-  if (oa.mode == 2) {   // totals of the range (part of it was decided by the provisional launch)
-    int64_t kept = 0, ents = 0;
-    for (int64_t t = gi0 * a.GN + threadIdx.x; t < gi1 * a.GN; t += blockDim.x) {
-      kept += a.L[t];
-      ents += a.U[t];
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      kept += __shfl_xor_sync(0xffffffffu, kept, o);
-      ents += __shfl_xor_sync(0xffffffffu, ents, o);
-    }
-    if (lane == 0) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals), static_cast<unsigned long long>(kept));
-      atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals) + 1, static_cast<unsigned long long>(ents));
-    }
-  }
-  order_pass(oa, gi0 * a.GN, gi1 * a.GN, s_warp, s_dyn);
-  if (threadIdx.x == 0) *oa.ticket = 0u;
-  if (threadIdx.x < 4 && oa.sched) oa.sched[threadIdx.x] = 0u;
-#ifdef SPAMM_PROFILE
-  __syncthreads();
-  if (oa.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(oa.prof[2]));
-#endif
 }
 
 // Per-C-tile k lists (C tile (i,j) owns slots [(i*BN+j)*BK, +V)) expanded from the macro lists:
@@ -650,35 +616,33 @@ template <int MI, int MJ>
 spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool order, bool row_work, cudaStream_t s) {
   const int64_t n_macro = on_device ? p.GM * p.GN : (gi1 - gi0) * p.GN;
   constexpr int kPerSm = 4;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(n_macro, static_cast<int64_t>(p.num_sms) * kPerSm));
-  const int64_t nb_max = std::max<int64_t>(p.BK + 1, p.NSB);
-  const int dyn = order ? static_cast<int>(std::min<int64_t>(nb_max, kSmemBuckets) * sizeof(unsigned long long)) : 0;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n_macro + kWarps - 1) / kWarps,
+                                                                static_cast<int64_t>(p.num_sms) * kPerSm));
   SkipArgs a{p.nA, p.nBt, p.pyr, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.tau, gi0, gi1, 0, 0,
              on_device ? p.d_range : nullptr, p.U, p.L,
-             row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run};
-  OrderArgs oa{p.hist, p.hist_sb, p.bucket_pos, p.NSB, p.U, p.L, p.BK, p.GN, p.num_sms, p.tile_lists,
-              p.tile_lists + p.GM * p.GN, p.ws_cnt, p.order, p.totals, p.ticket, p.sched,
-              order ? (on_device ? 2 : 1) : 0, nullptr};
-#ifdef SPAMM_PROFILE
-  static unsigned long long* prof = nullptr;
-  if (!prof) cudaMalloc(&prof, 64);
-  const unsigned long long init[3] = {~0ull, 0ull, 0ull};
-  cudaMemcpyAsync(prof, init, sizeof(init), cudaMemcpyHostToDevice, s);
-  oa.prof = prof;
-#endif
-  auto kern = skip_pyr_kernel<MI, MJ>;
-  SPAMM_SET_SMEM(kern, kSmemBuckets * static_cast<int>(sizeof(unsigned long long)), p.device);
-  SPAMM_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(kWarps * 32), dyn, s, a, oa));
+             row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run,
+             p.ws_cnt + (on_device ? 3 : 2)};
+  OrderArgs oa{p.hist, p.hist_sb, p.bucket_cnt, p.bucket_pos, p.NSB, p.U, p.L, p.BK, p.GN, p.num_sms, p.tile_lists,
+               p.tile_lists + p.GM * p.GN, p.ws_cnt, p.order, p.totals, p.sched, on_device ? p.d_range : nullptr,
+               gi0 * p.GN, gi1 * p.GN};
+  // the main loop builds the order's lists unless part of the range came from another launch
+  const int lists = order && !on_device ? 1 : 0;
+  SPAMM_CUDA_TRY(launch_pdl(skip_pyr_kernel<MI, MJ>, dim3(static_cast<unsigned>(blocks)), dim3(kWarps * 32), 0, s, a,
+                            oa, lists));
   count_launch();
-#ifdef SPAMM_PROFILE
   if (order) {
-    unsigned long long h[3];
-    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    fprintf(stderr, "[skip prof] main part %.2f us, order pass %.2f us (%lld macro-tiles)\n", (h[1] - h[0]) * 1e-3,
-            (h[2] - h[1]) * 1e-3, static_cast<long long>((gi1 - gi0) * p.GN));
+    const unsigned g = static_cast<unsigned>(p.num_sms);
+    if (on_device) {
+      SPAMM_CUDA_TRY(launch_pdl(order_lists_kernel, dim3(g), dim3(256), 0, s, oa));
+      count_launch();
+    }
+    if (std::max<int64_t>(p.BK + 1, p.NSB) > kSmemBuckets) {
+      SPAMM_CUDA_TRY(launch_pdl(order_scan_kernel, dim3(1), dim3(1024), 0, s, oa));
+      count_launch();
+    }
+    SPAMM_CUDA_TRY(launch_pdl(order_scatter_kernel, dim3(g), dim3(1024), 0, s, oa));
+    count_launch();
   }
-#endif
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
 }
