@@ -259,6 +259,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
     p->hist_sb = p->totals + 4;
     p->ws_cnt = reinterpret_cast<unsigned int*>(p->hist_sb + p->NSB);
     p->bucket_cnt = p->hist_sb + p->NSB + 2;
+    p->sb_bits = reinterpret_cast<unsigned long long*>(p->bucket_cnt + ws_buckets(*p));
   }
   if (st == SPAMM_OK && (cudaMemset(p->U, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||
                          cudaMemset(p->L, 0, sizeof(int64_t) * (nmac + 1)) != cudaSuccess ||

@@ -67,12 +67,13 @@ struct Plan {
   int64_t* row_work = nullptr;    // [ws_words()]: row work, then the claim order's counters (one memset)
   // workspace counters, one zeroed region (the norm kernel zeroes it inside spamm_run):
   //   row_work[BM] | hist[BK+2] | totals[4] | hist_sb[NSB] | ws_cnt[4] (uint32, two int64 words) |
-  //   bucket_cnt[NB], NB = max(BK + 2, NSB + 1)
+  //   bucket_cnt[NB], NB = max(BK + 2, NSB + 1) | sb_bits[3 NSB]
   int64_t* hist = nullptr;        // LPT bucket counts of the claim order (key BK - U)
   int64_t* totals = nullptr;      // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
   int64_t* hist_sb = nullptr;     // super-block bucket counts of the claim order
   unsigned int* ws_cnt = nullptr; // [0] work-list length, [1] empty-list length, [2], [3] skip-map tile claims
   int64_t* bucket_cnt = nullptr;  // claim-order slots taken per bucket
+  unsigned long long* sb_bits = nullptr;   // working macro-tiles per 12 x 12 super-block (144-bit masks)
   int64_t NSB = 0;                // 12 x 12 super-blocks of macro-tiles
   int32_t* tile_lists = nullptr;  // [2 * GM*GN]: macro-tiles with kept pairs, then those without
   unsigned int* sched = nullptr;  // dynamic tile counters of the multiply kernels (reset per launch)
@@ -146,7 +147,7 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 
 inline int64_t ws_buckets(const Plan& p) { return p.BK + 2 > p.NSB + 1 ? p.BK + 2 : p.NSB + 1; }
-inline int64_t ws_words(const Plan& p) { return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p); }
+inline int64_t ws_words(const Plan& p) { return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p) + 3 * p.NSB; }
 
 // Launch with programmatic dependent launch (PDL, griddepcontrol): the kernel's CTAs may be
 // scheduled while its stream predecessor drains.  Every kernel launched this way calls

@@ -233,6 +233,7 @@ struct OrderArgs {
   int64_t* hist_sb;      // [NSB] super-block bucket counts
   int64_t* bucket_cnt;   // [max(BK + 2, NSB + 1)] slots taken per bucket (zeroed with the workspace)
   int64_t* bucket_pos;   // [max(BK + 2, NSB + 1)] bucket starts (only when they exceed shared memory)
+  unsigned long long* sb_bits;   // [NSB][3] working tiles of each 12 x 12 super-block (row-major bit)
   int64_t nsb;
   const int64_t* U;
   const int64_t* L;
@@ -271,6 +272,17 @@ __device__ __forceinline__ int64_t sb_of(int64_t t, int64_t t0, int64_t GN) {
   const uint32_t rel = static_cast<uint32_t>(t - t0), row0 = static_cast<uint32_t>(t0) / gn;
   const uint32_t li = rel / gn, lj = (static_cast<uint32_t>(t) - row0 * gn - li * gn);
   return static_cast<int64_t>((li / static_cast<uint32_t>(kOrdS)) * nsbc + lj / static_cast<uint32_t>(kOrdS));
+}
+
+// bit of macro-tile t inside its super-block (row-major 12 x 12 position)
+__device__ __forceinline__ uint32_t sb_pos(int64_t t, int64_t t0, int64_t GN) {
+  const uint32_t gn = static_cast<uint32_t>(GN);
+  const uint32_t li = static_cast<uint32_t>(t - t0) / gn, lj = static_cast<uint32_t>(t % GN);
+  return (li % static_cast<uint32_t>(kOrdS)) * static_cast<uint32_t>(kOrdS) + lj % static_cast<uint32_t>(kOrdS);
+}
+__device__ __forceinline__ void mark_working(const OrderArgs& oa, int64_t t, int64_t t0) {
+  const uint32_t b = sb_pos(t, t0, oa.GN);
+  atomicOr(oa.sb_bits + sb_of(t, t0, oa.GN) * 3 + b / 64, 1ull << (b % 64));
 }
 
 __device__ __forceinline__ void order_range(const OrderArgs& oa, int64_t& t0, int64_t& t1) {
@@ -314,7 +326,10 @@ __global__ void __launch_bounds__(256) order_lists_kernel(const OrderArgs oa) {
     const unsigned e = agg_inc<unsigned>(oa.cnt + 1, 0, ise);
     agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist), isw ? oa.BK - u : 0, isw);
     agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.hist_sb), isw ? sb_of(t, t0, oa.GN) : 0, isw);
-    if (isw) oa.work[w] = static_cast<int32_t>(t);
+    if (isw) {
+      oa.work[w] = static_cast<int32_t>(t);
+      mark_working(oa, t, t0);
+    }
     if (ise) oa.empty[e] = static_cast<int32_t>(t);
   }
 #pragma unroll
@@ -356,9 +371,21 @@ __global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa)
   for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; b0 < n_work; b0 += stride) {
     const int64_t i = b0 + threadIdx.x;
     const int64_t t = i < n_work ? oa.work[i] : -1;
-    const int64_t key = t < 0 ? 0 : (blocked ? sb_of(t, t0, oa.GN) : oa.BK - oa.U[t]);
-    const unsigned long long r = agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.bucket_cnt), key, t >= 0);
-    if (t >= 0) oa.order[base[key] + static_cast<int64_t>(r)] = static_cast<int32_t>(t);
+    if (blocked) {   // slot = super-block start + rank of the tile among its block's working tiles (row-major)
+      if (t >= 0) {
+        const int64_t sb = sb_of(t, t0, oa.GN);
+        const uint32_t b = sb_pos(t, t0, oa.GN);
+        const unsigned long long* w = oa.sb_bits + sb * 3;
+        int64_t rank = 0;
+        for (uint32_t q = 0; q < b / 64; ++q) rank += __popcll(w[q]);
+        rank += __popcll(w[b / 64] & ((1ull << (b % 64)) - 1ull));
+        oa.order[base[sb] + rank] = static_cast<int32_t>(t);
+      }
+    } else {
+      const int64_t key = t < 0 ? 0 : oa.BK - oa.U[t];
+      const unsigned long long r = agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.bucket_cnt), key, t >= 0);
+      if (t >= 0) oa.order[base[key] + static_cast<int64_t>(r)] = static_cast<int32_t>(t);
+    }
   }
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_empty; i += stride)
     oa.order[n_work + i] = oa.empty[i];
@@ -500,6 +527,7 @@ __global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a,
           oa.work[atomicAdd(oa.cnt, 1u)] = static_cast<int32_t>(tile);
           atomicAdd(reinterpret_cast<unsigned long long*>(oa.hist) + (a.BK - u), 1ull);
           atomicAdd(reinterpret_cast<unsigned long long*>(oa.hist_sb) + sb_of(tile, gi0 * a.GN, a.GN), 1ull);
+          mark_working(oa, tile, gi0 * a.GN);
         } else {
           oa.empty[atomicAdd(oa.cnt + 1, 1u)] = static_cast<int32_t>(tile);
         }
@@ -622,7 +650,7 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
              on_device ? p.d_range : nullptr, p.U, p.L,
              row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run,
              p.ws_cnt + (on_device ? 3 : 2)};
-  OrderArgs oa{p.hist, p.hist_sb, p.bucket_cnt, p.bucket_pos, p.NSB, p.U, p.L, p.BK, p.GN, p.num_sms, p.tile_lists,
+  OrderArgs oa{p.hist, p.hist_sb, p.bucket_cnt, p.bucket_pos, p.sb_bits, p.NSB, p.U, p.L, p.BK, p.GN, p.num_sms, p.tile_lists,
                p.tile_lists + p.GM * p.GN, p.ws_cnt, p.order, p.totals, p.sched, on_device ? p.d_range : nullptr,
                gi0 * p.GN, gi1 * p.GN};
   // the main loop builds the order's lists unless part of the range came from another launch
