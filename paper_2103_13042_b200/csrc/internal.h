@@ -67,7 +67,7 @@ struct Plan {
   int64_t* row_work = nullptr;    // [ws_words()]: row work, then the claim order's counters (one memset)
   // workspace counters, one zeroed region (the norm kernel zeroes it inside spamm_run):
   //   row_work[BM] | hist[BK+2] | totals[4] | hist_sb[NSB] | ws_cnt[4] (uint32, two int64 words) |
-  //   bucket_cnt[NB], NB = max(BK + 2, NSB + 1) | sb_bits[3 NSB]
+  //   bucket_cnt[NB], NB = max(BK + 2, NSB + 1) | sb_bits[3 NSB] (144-bit masks)
   int64_t* hist = nullptr;        // LPT bucket counts of the claim order (key BK - U)
   int64_t* totals = nullptr;      // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
   int64_t* hist_sb = nullptr;     // super-block bucket counts of the claim order
@@ -147,7 +147,12 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 
 inline int64_t ws_buckets(const Plan& p) { return p.BK + 2 > p.NSB + 1 ? p.BK + 2 : p.NSB + 1; }
-inline int64_t ws_words(const Plan& p) { return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p) + 3 * p.NSB; }
+#ifndef SPAMM_ORD_S
+#define SPAMM_ORD_S 12   // side of the claim order's super-blocks in macro-tiles (skipmap.cu)
+#endif
+inline int64_t ws_words(const Plan& p) {
+  return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p) + (SPAMM_ORD_S * SPAMM_ORD_S + 63) / 64 * p.NSB;
+}
 
 // Launch with programmatic dependent launch (PDL, griddepcontrol): the kernel's CTAs may be
 // scheduled while its stream predecessor drains.  Every kernel launched this way calls

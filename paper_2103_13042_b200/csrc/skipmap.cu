@@ -233,7 +233,7 @@ struct OrderArgs {
   int64_t* hist_sb;      // [NSB] super-block bucket counts
   int64_t* bucket_cnt;   // [max(BK + 2, NSB + 1)] slots taken per bucket (zeroed with the workspace)
   int64_t* bucket_pos;   // [max(BK + 2, NSB + 1)] bucket starts (only when they exceed shared memory)
-  unsigned long long* sb_bits;   // [NSB][3] working tiles of each 12 x 12 super-block (row-major bit)
+  unsigned long long* sb_bits;   // [NSB][kSbWords] working tiles of each 12 x 12 super-block (row-major bit)
   int64_t nsb;
   const int64_t* U;
   const int64_t* L;
@@ -249,7 +249,8 @@ struct OrderArgs {
   int64_t t0, t1;
 };
 constexpr int kSmemBuckets = 4096;
-constexpr int64_t kOrdS = 12;   // 12 x 12 super-blocks of macro-tiles
+constexpr int64_t kOrdS = SPAMM_ORD_S;   // 12 x 12 super-blocks of macro-tiles (build-time for experiments)
+constexpr int64_t kSbWords = (kOrdS * kOrdS + 63) / 64;   // 64-bit words of a super-block's tile mask
 
 // warp-aggregated atomicAdd of 1 per lane on cnt[key]: lanes with equal keys share one atomic;
 // returns each lane's old value + its rank among the equal lanes
@@ -282,7 +283,7 @@ __device__ __forceinline__ uint32_t sb_pos(int64_t t, int64_t t0, int64_t GN) {
 }
 __device__ __forceinline__ void mark_working(const OrderArgs& oa, int64_t t, int64_t t0) {
   const uint32_t b = sb_pos(t, t0, oa.GN);
-  atomicOr(oa.sb_bits + sb_of(t, t0, oa.GN) * 3 + b / 64, 1ull << (b % 64));
+  atomicOr(oa.sb_bits + sb_of(t, t0, oa.GN) * kSbWords + b / 64, 1ull << (b % 64));
 }
 
 __device__ __forceinline__ void order_range(const OrderArgs& oa, int64_t& t0, int64_t& t1) {
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa)
       if (t >= 0) {
         const int64_t sb = sb_of(t, t0, oa.GN);
         const uint32_t b = sb_pos(t, t0, oa.GN);
-        const unsigned long long* w = oa.sb_bits + sb * 3;
+        const unsigned long long* w = oa.sb_bits + sb * kSbWords;
         int64_t rank = 0;
         for (uint32_t q = 0; q < b / 64; ++q) rank += __popcll(w[q]);
         rank += __popcll(w[b / 64] & ((1ull << (b % 64)) - 1ull));

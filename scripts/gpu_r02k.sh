@@ -1,0 +1,15 @@
+#!/bin/bash
+# Round-2 GPU session K: super-block side of the many-tile claim order (build-time SPAMM_ORD_S).
+OUT=gpurun_out/r02k
+mkdir -p $OUT
+for S in 12 8 16 24 12; do
+  SPAMM_NVCC_FLAGS="-DSPAMM_ORD_S=$S" python -m paper_2103_13042_b200.build --force > /dev/null
+  timeout 300 python bench.py --steps 6 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > $OUT/b$S.json 2> $OUT/b$S.err
+  python -c "import json; d=json.load(open('$OUT/b$S.json')); print('S=$S', d['config']['N'], round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['stages_ms'].items()}, d['clocks']['sm_mhz'], round(d['stages_ms']['multiply']*d['clocks']['sm_mhz']/1000,1))"
+done
+SPAMM_NVCC_FLAGS="-DSPAMM_ORD_S=16" python -m paper_2103_13042_b200.build --force > /dev/null
+timeout 1500 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:spamm_mul_dual -s 3 -c 1 \
+   python bench.py --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > $OUT/ncu16.log 2>&1; grep -E "dram__bytes|duration|hit_rate" $OUT/ncu16.log
+python -m paper_2103_13042_b200.build --force > /dev/null
+timeout 1500 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:spamm_mul_dual -s 3 -c 1 \
+   python bench.py --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > $OUT/ncu12.log 2>&1; grep -E "dram__bytes|duration|hit_rate" $OUT/ncu12.log
