@@ -81,3 +81,34 @@ def test_partition_rejects_bad_input(sp):
         sp.spamm_partition_rows([1, -1, 2], 2)
     with pytest.raises(sp.SpammError):
         sp.spamm_partition_rows([1, 2], 0)
+
+
+def test_product_path_never_touches_the_oracle():
+    """The oracle is test infrastructure: the package neither imports it nor shares code with it,
+    and importing the binding leaves it unloaded (checked in a fresh interpreter)."""
+    import glob
+    import subprocess
+    import sys
+    pkg = os.path.join(ROOT, "paper_2103_13042_b200")
+    for f in glob.glob(os.path.join(pkg, "**", "*.py"), recursive=True) + glob.glob(os.path.join(pkg, "csrc", "*")):
+        txt = open(f, errors="ignore").read()
+        assert "import oracle" not in txt and "from oracle" not in txt, f
+    code = ("import sys; sys.path.insert(0, %r); from paper_2103_13042_b200 import spamm; "
+            "print('oracle' in sys.modules)" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd="/tmp")
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip().endswith("False")
+
+
+def test_binding_refuses_to_load_without_the_library(tmp_path):
+    """No fallback: a copy of the binding next to no libspamm.so raises ImportError on import."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "paper_2103_13042_b200"
+    pkg.mkdir()
+    shutil.copy(os.path.join(ROOT, "paper_2103_13042_b200", "spamm.py"), pkg / "spamm.py")
+    (pkg / "__init__.py").write_text("")
+    code = "import sys; sys.path.insert(0, %r); from paper_2103_13042_b200 import spamm" % str(tmp_path)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert out.returncode != 0 and "ImportError" in out.stderr
