@@ -240,7 +240,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   ALLOC(leaf_start, int64_t, nleaf);
   ALLOC(U, int64_t, nmac + 1);
   ALLOC(L, int64_t, nmac + 1);
-  p->NSB = ((p->GM + SPAMM_ORD_S - 1) / SPAMM_ORD_S) * ((p->GN + SPAMM_ORD_S - 1) / SPAMM_ORD_S);
+  p->NSB = ((p->GM + SPAMM_ORD_R - 1) / SPAMM_ORD_R) * ((p->GN + SPAMM_ORD_C - 1) / SPAMM_ORD_C);
   ALLOC(row_work, int64_t, ws_words(*p));
   ALLOC(tile_lists, int32_t, 2 * nmac);
   ALLOC(sched, unsigned int, 4);   // [0] tile claims, [1] zero-fill unit claims

@@ -147,11 +147,16 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 
 inline int64_t ws_buckets(const Plan& p) { return p.BK + 2 > p.NSB + 1 ? p.BK + 2 : p.NSB + 1; }
-#ifndef SPAMM_ORD_S
-#define SPAMM_ORD_S 12   // side of the claim order's super-blocks in macro-tiles (skipmap.cu)
+// the many-tile claim order visits super-blocks of SPAMM_ORD_R x SPAMM_ORD_C macro-tiles row-major
+// (skipmap.cu; measured at N = 65536)
+#ifndef SPAMM_ORD_R
+#define SPAMM_ORD_R 6
+#endif
+#ifndef SPAMM_ORD_C
+#define SPAMM_ORD_C 6
 #endif
 inline int64_t ws_words(const Plan& p) {
-  return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p) + (SPAMM_ORD_S * SPAMM_ORD_S + 63) / 64 * p.NSB;
+  return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p) + (SPAMM_ORD_R * SPAMM_ORD_C + 63) / 64 * p.NSB;
 }
 
 // Launch with programmatic dependent launch (PDL, griddepcontrol): the kernel's CTAs may be

@@ -249,8 +249,8 @@ struct OrderArgs {
   int64_t t0, t1;
 };
 constexpr int kSmemBuckets = 4096;
-constexpr int64_t kOrdS = SPAMM_ORD_S;   // 12 x 12 super-blocks of macro-tiles (build-time for experiments)
-constexpr int64_t kSbWords = (kOrdS * kOrdS + 63) / 64;   // 64-bit words of a super-block's tile mask
+constexpr uint32_t kOrdR = SPAMM_ORD_R, kOrdC = SPAMM_ORD_C;   // super-block of kOrdR x kOrdC macro-tiles
+constexpr int64_t kSbWords = (kOrdR * kOrdC + 63) / 64;        // 64-bit words of a super-block's tile mask
 
 // warp-aggregated atomicAdd of 1 per lane on cnt[key]: lanes with equal keys share one atomic;
 // returns each lane's old value + its rank among the equal lanes
@@ -269,17 +269,17 @@ __device__ __forceinline__ T agg_inc(T* cnt, int64_t key, bool active) {
 
 // super-block of macro-tile t in the range starting at tile t0 (32-bit arithmetic: tile ids < 2^31)
 __device__ __forceinline__ int64_t sb_of(int64_t t, int64_t t0, int64_t GN) {
-  const uint32_t gn = static_cast<uint32_t>(GN), nsbc = (gn + kOrdS - 1) / kOrdS;
+  const uint32_t gn = static_cast<uint32_t>(GN), nsbc = (gn + kOrdC - 1) / kOrdC;
   const uint32_t rel = static_cast<uint32_t>(t - t0), row0 = static_cast<uint32_t>(t0) / gn;
   const uint32_t li = rel / gn, lj = (static_cast<uint32_t>(t) - row0 * gn - li * gn);
-  return static_cast<int64_t>((li / static_cast<uint32_t>(kOrdS)) * nsbc + lj / static_cast<uint32_t>(kOrdS));
+  return static_cast<int64_t>((li / kOrdR) * nsbc + lj / kOrdC);
 }
 
 // bit of macro-tile t inside its super-block (row-major 12 x 12 position)
 __device__ __forceinline__ uint32_t sb_pos(int64_t t, int64_t t0, int64_t GN) {
   const uint32_t gn = static_cast<uint32_t>(GN);
   const uint32_t li = static_cast<uint32_t>(t - t0) / gn, lj = static_cast<uint32_t>(t % GN);
-  return (li % static_cast<uint32_t>(kOrdS)) * static_cast<uint32_t>(kOrdS) + lj % static_cast<uint32_t>(kOrdS);
+  return (li % kOrdR) * kOrdC + lj % kOrdC;
 }
 __device__ __forceinline__ void mark_working(const OrderArgs& oa, int64_t t, int64_t t0) {
   const uint32_t b = sb_pos(t, t0, oa.GN);
