@@ -147,13 +147,14 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 void count_launch(int n = 1);
 
 inline int64_t ws_buckets(const Plan& p) { return p.BK + 2 > p.NSB + 1 ? p.BK + 2 : p.NSB + 1; }
-// the many-tile claim order visits super-blocks of SPAMM_ORD_R x SPAMM_ORD_C macro-tiles row-major
-// (skipmap.cu; measured at N = 65536)
+// the many-tile claim order visits super-blocks of SPAMM_ORD_R x SPAMM_ORD_C macro-tiles row-major:
+// by default bands of 6 macro rows walked column by column (skipmap.cu; measured at N = 65536,
+// DESIGN.md "claim order")
 #ifndef SPAMM_ORD_R
 #define SPAMM_ORD_R 6
 #endif
 #ifndef SPAMM_ORD_C
-#define SPAMM_ORD_C 6
+#define SPAMM_ORD_C 1
 #endif
 inline int64_t ws_words(const Plan& p) {
   return p.BM + p.BK + 2 + 4 + p.NSB + 2 + ws_buckets(p) + (SPAMM_ORD_R * SPAMM_ORD_C + 63) / 64 * p.NSB;

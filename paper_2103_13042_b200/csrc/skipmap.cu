@@ -20,7 +20,7 @@
 //             and write, at offsets scanned across the warps, the macro-tile's (k, keep mask)
 //             list and, for the tensor path, each k-step's MMA runs pre-decoded per 128-row half;
 //   order   : the main loop appends every macro-tile to a work or an empty list and counts two
-//             histograms (LPT key BK - U; 12 x 12 super-block); a grid-wide scatter kernel places the
+//             histograms (LPT key BK - U; super-block); a grid-wide scatter kernel places the
 //             work list by bucket (a bucket sort, no comparison sort) and appends the empty tiles:
 //             the multiply's claim order, plus the totals (kept pairs, k-steps).
 // Row work (Sec. 3.5.1's V summed over a row) and kept counts are popcounts of the masks.
@@ -233,7 +233,7 @@ struct OrderArgs {
   int64_t* hist_sb;      // [NSB] super-block bucket counts
   int64_t* bucket_cnt;   // [max(BK + 2, NSB + 1)] slots taken per bucket (zeroed with the workspace)
   int64_t* bucket_pos;   // [max(BK + 2, NSB + 1)] bucket starts (only when they exceed shared memory)
-  unsigned long long* sb_bits;   // [NSB][kSbWords] working tiles of each 12 x 12 super-block (row-major bit)
+  unsigned long long* sb_bits;   // [NSB][kSbWords] working tiles of each super-block (row-major bit)
   int64_t nsb;
   const int64_t* U;
   const int64_t* L;
@@ -275,7 +275,7 @@ __device__ __forceinline__ int64_t sb_of(int64_t t, int64_t t0, int64_t GN) {
   return static_cast<int64_t>((li / kOrdR) * nsbc + lj / kOrdC);
 }
 
-// bit of macro-tile t inside its super-block (row-major 12 x 12 position)
+// bit of macro-tile t inside its super-block (row-major position)
 __device__ __forceinline__ uint32_t sb_pos(int64_t t, int64_t t0, int64_t GN) {
   const uint32_t gn = static_cast<uint32_t>(GN);
   const uint32_t li = static_cast<uint32_t>(t - t0) / gn, lj = static_cast<uint32_t>(t % GN);
@@ -298,10 +298,13 @@ __device__ __forceinline__ void order_range(const OrderArgs& oa, int64_t& t0, in
 // The multiply's claim order of the macro-tiles of the range (a parallel bucket sort):
 //   * few tiles per CTA (n_work < 16 per SM): longest processing time first -- key BK - U, so the
 //     long tiles start first and the short ones fill the tail (Sec. 3.5.1's balance goal);
-//   * many tiles per CTA (balance is free): by 12 x 12 super-block, so the ~148 tiles in flight
-//     share A row strips and B column strips in L2 (ordering by the first kept k instead put tiles
-//     of one anti-diagonal -- no shared strips -- in flight together: 645 vs 244-298 GB of DRAM
-//     reads at N = 65536, multiply 68 -> 103 ms, profiles/r02c_kstart_*);
+//   * many tiles per CTA (balance is free): by super-block of kOrdR x kOrdC macro-tiles, row-major,
+//     default bands of 6 macro rows walked column by column: the tiles claimed together share a B
+//     column strip and start their k-lists within a few k-steps of each other (on a band, the first
+//     kept k moves by 4 k-tiles per macro row), so their operand loads hit in L2.  Measured at
+//     N = 65536 (DRAM reads of the multiply / its time): 12 x 12 blocks 266 GB / 66 ms, 8 x 8 170 GB,
+//     6 x 6 115 GB / 60 ms, 6 x 1 58 ms; ordering by the first kept k instead put tiles of one
+//     anti-diagonal -- no shared strips -- in flight together: 645 GB / 103 ms;
 //   * macro-tiles without kept pairs last (zero-filled by the multiply).
 // The skip map's main loop appends the tiles to a work or an empty list and counts both
 // histograms; order_lists_kernel does that from U instead on the multi-GPU final pass (part of the
