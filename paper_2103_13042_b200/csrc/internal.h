@@ -73,8 +73,8 @@ struct Plan {
   int64_t* hist_sb = nullptr;     // super-block bucket counts of the claim order
   unsigned int* ws_cnt = nullptr; // [0] work-list length, [1] empty-list length, [2], [3] skip-map tile claims
   int64_t* bucket_cnt = nullptr;  // claim-order slots taken per bucket
-  unsigned long long* sb_bits = nullptr;   // working macro-tiles per 12 x 12 super-block (144-bit masks)
-  int64_t NSB = 0;                // 12 x 12 super-blocks of macro-tiles
+  unsigned long long* sb_bits = nullptr;   // working macro-tiles per claim-order super-block (bit masks)
+  int64_t NSB = 0;                // claim-order super-blocks of macro-tiles (SPAMM_ORD_R x SPAMM_ORD_C)
   int32_t* tile_lists = nullptr;  // [2 * GM*GN]: macro-tiles with kept pairs, then those without
   unsigned int* sched = nullptr;  // dynamic tile counters of the multiply kernels (reset per launch)
   uint16_t* leaf_k = nullptr;     // [BM*BN*BK] per-C-tile k lists (leaf view, on request)
