@@ -67,7 +67,7 @@ struct Plan {
   int64_t* row_work = nullptr;    // [ws_words()]: row work, then the claim order's counters (one memset)
   // workspace counters, one zeroed region (the norm kernel zeroes it inside spamm_run):
   //   row_work[BM] | hist[BK+2] | totals[4] | hist_sb[NSB] | ws_cnt[4] (uint32, two int64 words) |
-  //   bucket_cnt[NB], NB = max(BK + 2, NSB + 1) | sb_bits[3 NSB] (144-bit masks)
+  //   bucket_cnt[NB], NB = max(BK + 2, NSB + 1) | sb_bits[ceil(R*C/64) NSB]
   int64_t* hist = nullptr;        // LPT bucket counts of the claim order (key BK - U)
   int64_t* totals = nullptr;      // [0] kept pairs, [1] macro entries, [2] macro-tiles without kept pairs
   int64_t* hist_sb = nullptr;     // super-block bucket counts of the claim order
