@@ -481,6 +481,21 @@ def _cublas(A, flush, stream, reps):
                                                 else f"{str(A.dtype)[6:]} in, FP32 accumulate")}
 
 
+def _low_only_point(sp, A, N, tau, flush, stream):
+    """SPAMM_MUL_LOW_ONLY: the same SpAMM with the result written only as BF16
+    (half the output bytes; C-write-bound at N = 16384), through spamm_multiply_chain."""
+    Cl = torch.empty((N, N), dtype=A.dtype, device=A.device)
+    with sp.Plan(N, N, N, tau, "bf16") as plan:
+        fl = sp.SPAMM_MUL_AUTO | sp.SPAMM_MUL_LOW_ONLY
+        ms = statistics.median(_timed(lambda: sp.spamm_multiply_chain(plan.handle, A, A, None, Cl, flags=fl),
+                                      5, 2, flush, stream))
+        st = plan.stats()
+    return {"N": N, "precision": "bf16", "output": "bf16 only (SPAMM_MUL_LOW_ONLY)", "tau": tau, "ms": ms,
+            "valid_ratio": st["valid_ratio"], "kept": st["kept"],
+            "tflops_dense_equiv": 2.0 * N ** 3 / (ms / 1e3) / 1e12,
+            "tflops_kept": 2.0 * TILE ** 3 * st["kept"] / (ms / 1e3) / 1e12}
+
+
 def _sweeps(sp, A, N, prec, args, flush, stream, dev):
     """tau sweeps on configs[4] (the headline size), the north_star's N = 16384 exponential-decay
     target and configs[1] N = 8192, with cuBLAS dense GEMM on the same box and inputs."""
@@ -494,8 +509,13 @@ def _sweeps(sp, A, N, prec, args, flush, stream, dev):
             res += _sweep_one(sp, A2, n2, p2, taus, small_flush, stream)
             if p2 != "fp32x3":
                 cublas[f"N={n2} {p2}"] = _cublas(A2, small_flush, stream, 3)
+            if p2 == "bf16" and n2 == 16384:
+                res.append(_low_only_point(sp, A2, n2, 1e-6, small_flush, stream))
             del A2
     for r in res:
+        if "output" in r:
+            r["speedup_vs_cublas"] = cublas[f"N={r['N']} bf16"]["ms"] / r["ms"]
+            continue
         key = f"N={r['N']}" if r["N"] == N else f"N={r['N']} {'fp32' if r['precision'] == 'fp32x3' else r['precision']}"
         if key in cublas and (r["N"] != N or r["precision"] == prec):
             r["speedup_vs_cublas"] = cublas[key]["ms"] / r["ms"]
