@@ -352,6 +352,15 @@ def run_ours(args, rank, world, local_rank):
         threads, model = _cpu_info()
         cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "cpu": model, "kind": "oracle",
                "sample": f"{desc}; {dt:.2f} s"}
+        try:   # the same oracle on one host thread (BLAS pinned to 1 thread), a quarter of the sample
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                dt1, fl1, _ = oracle_sample(N, args.lam, prec, tau, rows=4, cols=48)
+            cpu["value_1_thread"] = fl1 / dt1 / 1e12
+            cpu["sample_1_thread"] = f"4 middle tile rows x 48 random tile columns; {dt1:.2f} s"
+        except Exception as exc:   # noqa: BLE001 (reporting only)
+            cpu["value_1_thread"] = None
+            cpu["sample_1_thread"] = f"unavailable: {exc}"
     plan.close()
     if comm is not None:
         sp.spamm_nccl_comm_destroy(comm)
