@@ -663,7 +663,9 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
                             oa, lists));
   count_launch();
   if (order) {
-    const unsigned g = static_cast<unsigned>(p.num_sms);
+    // one CTA per 1024 macro-tiles of the range, at most one per SM
+    const unsigned g = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>(p.num_sms, ((on_device ? p.GM : gi1 - gi0) * p.GN + 1023) / 1024)));
     if (on_device) {
       SPAMM_CUDA_TRY(launch_pdl(order_lists_kernel, dim3(g), dim3(256), 0, s, oa));
       count_launch();
