@@ -372,23 +372,30 @@ __global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa)
     base = s_pos;
   }
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; b0 < n_work; b0 += stride) {
-    const int64_t i = b0 + threadIdx.x;
-    const int64_t t = i < n_work ? oa.work[i] : -1;
-    if (blocked) {   // slot = super-block start + rank of the tile among its block's working tiles (row-major)
-      if (t >= 0) {
-        const int64_t sb = sb_of(t, t0, oa.GN);
-        const uint32_t b = sb_pos(t, t0, oa.GN);
-        const unsigned long long* w = oa.sb_bits + sb * kSbWords;
-        int64_t rank = 0;
-        for (uint32_t q = 0; q < b / 64; ++q) rank += __popcll(w[q]);
-        rank += __popcll(w[b / 64] & ((1ull << (b % 64)) - 1ull));
-        oa.order[base[sb] + rank] = static_cast<int32_t>(t);
-      }
-    } else {
-      const int64_t key = t < 0 ? 0 : oa.BK - oa.U[t];
-      const unsigned long long r = agg_inc<unsigned long long>(reinterpret_cast<unsigned long long*>(oa.bucket_cnt), key, t >= 0);
-      if (t >= 0) oa.order[base[key] + static_cast<int64_t>(r)] = static_cast<int32_t>(t);
+  if (blocked) {   // slot = super-block start + rank of the tile among its block's working tiles (row-major)
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_work; i += stride) {
+      const int64_t t = oa.work[i];
+      const int64_t sb = sb_of(t, t0, oa.GN);
+      const uint32_t b = sb_pos(t, t0, oa.GN);
+      const unsigned long long* w = oa.sb_bits + sb * kSbWords;
+      int64_t rank = 0;
+      for (uint32_t q = 0; q < b / 64; ++q) rank += __popcll(w[q]);
+      rank += __popcll(w[b / 64] & ((1ull << (b % 64)) - 1ull));
+      oa.order[base[sb] + rank] = static_cast<int32_t>(t);
+    }
+  } else if (blockIdx.x == 0) {
+    // LPT: one CTA walks the range in tile order, one 1024-tile window at a time, so equal keys
+    // (Toeplitz bands have many equal U) keep row-major order -- neighbouring tiles run together
+    unsigned long long* pos = nbucket <= kSmemBuckets ? reinterpret_cast<unsigned long long*>(s_pos)
+                                                      : reinterpret_cast<unsigned long long*>(oa.bucket_cnt);
+    for (int64_t c0 = t0; c0 < t1; c0 += blockDim.x) {
+      const int64_t t = c0 + threadIdx.x;
+      const int64_t u = t < t1 ? oa.U[t] : 0;
+      const int64_t key = u > 0 ? oa.BK - u : 0;
+      const unsigned long long slot = agg_inc<unsigned long long>(pos, key, u > 0);
+      if (u > 0) oa.order[nbucket <= kSmemBuckets ? static_cast<int64_t>(slot) : base[key] + static_cast<int64_t>(slot)] =
+          static_cast<int32_t>(t);
+      __syncthreads();
     }
   }
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_empty; i += stride)
