@@ -137,9 +137,6 @@ static void free_plan(Plan* p) {
     if (q) cudaFree(q);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
-  if (p->zf_fork) cudaEventDestroy(p->zf_fork);
-  if (p->zf_join) cudaEventDestroy(p->zf_join);
-  if (p->zf_stream) cudaStreamDestroy(p->zf_stream);
   delete p;
 }
 

@@ -109,10 +109,6 @@ struct Plan {
   std::vector<int64_t> last_partition;
   cudaStream_t last_stream = nullptr;
 
-  // side-stream zero-fill experiment (-DSPAMM_ZF_SIDE, multiply_dual.cu): fork / join
-  cudaStream_t zf_stream = nullptr;
-  cudaEvent_t zf_fork = nullptr, zf_join = nullptr;
-
   // timing
   cudaEvent_t ev[6] = {};
   bool ev_norms = false, ev_skip = false, ev_mul = false;
@@ -150,16 +146,6 @@ spamm_status cuda_fail(cudaError_t e, const char* where);
 
 void count_launch(int n = 1);
 
-// keep the maximum shared-memory carveout for a kernel that co-resides with a large-smem kernel
-#define SPAMM_SET_CARVEOUT(kern, dev)                                                                     \
-  do {                                                                                                  \
-    static std::atomic<unsigned long long> _done{0};                                                    \
-    const unsigned long long _bit = 1ull << ((dev) & 63);                                               \
-    if (!(_done.load(std::memory_order_relaxed) & _bit)) {                                              \
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));    \
-      _done.fetch_or(_bit, std::memory_order_relaxed);                                                  \
-    }                                                                                                   \
-  } while (0)
 
 inline int64_t ws_buckets(const Plan& p) { return p.BK + 2 > p.NSB + 1 ? p.BK + 2 : p.NSB + 1; }
 // the many-tile claim order visits super-blocks of SPAMM_ORD_R x SPAMM_ORD_C macro-tiles row-major:

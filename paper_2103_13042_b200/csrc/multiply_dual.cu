@@ -96,8 +96,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
                           const int32_t* __restrict__ order, int64_t n_tiles,
                           const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p, int64_t GN,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched,
-                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int use3d,
-                          int zero_fill) {
+                          const Axpby ab, const DChain co, unsigned long long* __restrict__ prof, int use3d) {
   // claims follow the skip map's order (skipmap.cu order_pass: LPT for few tiles per CTA, ascending
   // first kept k for many); the tiles without kept pairs come last and are zero-filled by the
   // epilogue warps (plain epilogue), or go through the pipeline (n_empty_p == nullptr)
@@ -161,7 +160,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
   // counter, so the CTAs that finish their MMA work early absorb it (the slowest one takes
   // none).  Done greedily at the start instead, the 141 MB of zero writes at the bench point
   // compete with the operand loads' first DRAM touches (multiply 165 vs 152 us without them).
-  const int64_t n_units = zero_fill ? n_empty * 8 : 0;   // else zerofill_kernel (side stream)
+  const int64_t n_units = n_empty * 8;
   auto zero_unit = [&]() -> bool {
     unsigned int u32 = 0;
     if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
@@ -666,39 +665,6 @@ __global__ void __launch_bounds__(kDThreads, 1)
   if (tl && threadIdx.x == 0) stamp(5);
 }
 
-// Zero-fill of the macro-tiles without kept pairs on a side stream, concurrently with the multiply
-// (experiment, -DSPAMM_ZF_SIDE=<warps per SM>): few warps, 16-byte LSU streaming stores -- light on
-// issue slots (the multiply's issuer warps are latency-critical) and off the TMA unit (which serves
-// the operand loads).  A warp zeroes one (macro-tile, 32-row strip) unit at a time.
-__global__ void __launch_bounds__(32)
-    zerofill_kernel(const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ rng,
-                    const int64_t* __restrict__ n_empty_p, int64_t GN, float* __restrict__ C, int64_t ldc, int64_t M,
-                    int64_t N) {
-  if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;
-  const int64_t n_empty = *n_empty_p, n_work = n_tiles - n_empty;
-  const int64_t units = n_empty * 8;
-  const int lane = threadIdx.x & 31;
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  const bool vec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int64_t t = order[n_work + u / 8];
-    const int64_t r0 = (t / GN) * 256 + (u % 8) * 32, c0 = (t % GN) * 256;
-    const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
-    if (vec && ncol == 256) {
-#pragma unroll 4
-      for (int r = 0; r < 32; ++r) {
-        if (r0 + r >= M) break;
-        float4* dst = reinterpret_cast<float4*>(C + (r0 + r) * ldc + c0);
-        __stcs(dst + lane, z);
-        __stcs(dst + 32 + lane, z);
-      }
-    } else {
-      for (int r = 0; r < 32 && r0 + r < M; ++r)
-        for (int64_t c = lane; c < ncol; c += 32) C[(r0 + r) * ldc + c0 + c] = 0.f;
-    }
-  }
-}
-
 #ifdef SPAMM_PROFILE
 // per-CTA issuer counters and a globaltimer timeline (compile with -DSPAMM_PROFILE)
 static void print_profile(const unsigned long long* hp, int grid) {
@@ -761,20 +727,6 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
   const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
   if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, 2 * sizeof(unsigned int), s));
   p.sched_zeroed = false;
-#ifdef SPAMM_ZF_SIDE
-  const bool side_zf = !kGen;
-#else
-  const bool side_zf = false;
-#endif
-  if (side_zf) {
-    if (!p.zf_stream) {
-      SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&p.zf_stream, cudaStreamNonBlocking));
-      SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&p.zf_fork, cudaEventDisableTiming));
-      SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&p.zf_join, cudaEventDisableTiming));
-    }
-    SPAMM_CUDA_TRY(cudaEventRecord(p.zf_fork, s));
-    SPAMM_CUDA_TRY(cudaStreamWaitEvent(p.zf_stream, p.zf_fork, 0));
-  }
   unsigned long long* prof = nullptr;
 #ifdef SPAMM_PROFILE
   static unsigned long long* prof_buf = nullptr;
@@ -789,21 +741,9 @@ spamm_status launch_dual_t(Plan& p, const void* A, int64_t lda, const void* B, i
                             static_cast<const int64_t*>(kGen ? nullptr : p.totals + 2), p.GN, C, ldc, p.M, p.N, p.sched,
                             Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                             DChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
-                            prof, p.N % 32 == 0 ? 1 : 0, side_zf ? 0 : 1));
+                            prof, p.N % 32 == 0 ? 1 : 0));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
-#ifdef SPAMM_ZF_SIDE
-  if (side_zf) {   // after the multiply's launch, so its CTAs take the SMs first
-    SPAMM_SET_CARVEOUT(zerofill_kernel, p.device);
-    zerofill_kernel<<<p.num_sms * SPAMM_ZF_SIDE, 32, 0, p.zf_stream>>>(p.order, n_tiles,
-                                                                   p.range_on_device ? p.d_range : nullptr,
-                                                                   p.totals + 2, p.GN, C, ldc, p.M, p.N);
-    count_launch();
-    SPAMM_CUDA_TRY(cudaGetLastError());
-    SPAMM_CUDA_TRY(cudaEventRecord(p.zf_join, p.zf_stream));
-    SPAMM_CUDA_TRY(cudaStreamWaitEvent(s, p.zf_join, 0));
-  }
-#endif
 #ifdef SPAMM_PROFILE
   static unsigned long long hp[1024 * 24];
   cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, s);
