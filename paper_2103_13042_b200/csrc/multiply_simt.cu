@@ -50,7 +50,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   float4* sAcc = reinterpret_cast<float4*>(smem + static_cast<size_t>(kStages) * kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(kStages) * kStageBytes + kAccBytes);
   uint64_t* empty = full + kStages;
-  uint32_t* smask = reinterpret_cast<uint32_t*>(empty + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -79,7 +78,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t e = e0; e < e1; ++e) {
           const uint2 en = ment[e];
           mbar_wait(&empty[s], ph ^ 1);
-          smask[s] = en.y;
           mbar_arrive_expect_tx(&full[s], kStageBytes);
           tma_load_2d(sA + s * kAFloats, &tA, &full[s], static_cast<int32_t>(en.x) * 32, I * 128);
           tma_load_2d(sB + s * kBFloats, &tB, &full[s], J * 128, static_cast<int32_t>(en.x) * 32);
@@ -108,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t e0 = mstart[t], e1 = e0 + mcount[t];
     for (int64_t e = e0; e < e1; ++e) {
       mbar_wait(&full[s], ph);
-      const uint32_t mask = smask[s];
+      const uint32_t mask = __ldg(&ment[e].y);   // the k-step's keep bits (read-only, L1-resident)
       if ((mask >> bit) & 1u) {
         const float* a_base = sA + s * kAFloats + (li * 32 + g) * 32;
         const float* b_base = sB + s * kBFloats + lj * 32 + cg * 8;
