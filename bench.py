@@ -471,11 +471,17 @@ def _sweep_one(sp, A, N, prec, taus, flush, stream, reps=3):
                         stages[k].append(s["ms_" + k])
             s = plan.stats()
             ms = statistics.median(ms_list)
+            ms_mul = statistics.median(stages["multiply"])
+            roof, _, _ = _roofline(s, prec, ms_mul, statistics.median(stages["norms"]), N, _peaks(),
+                                   4 if prec in ("fp32", "fp32x3") else 2, None)
             out.append({"N": N, "precision": prec, "tau": tau, "ms": ms, "valid_ratio": s["valid_ratio"],
                         "kept": s["kept"], "stages_ms": {k: statistics.median(v) for k, v in stages.items()},
                         "tflops_dense_equiv": 2.0 * N ** 3 / (ms / 1e3) / 1e12,
                         "tflops_kept": 2.0 * TILE ** 3 * s["kept"] / (ms / 1e3) / 1e12,
-                        "multiply_tflops_kept": 2.0 * TILE ** 3 * s["kept"] / (statistics.median(stages["multiply"]) / 1e3) / 1e12})
+                        "multiply_tflops_kept": 2.0 * TILE ** 3 * s["kept"] / (ms_mul / 1e3) / 1e12,
+                        # multiply floor = max(kept MMA FLOPs / peak, (C write + A read) / HBM peak)
+                        "multiply_roofline": {"bound": roof["bound"], "floor_ms": roof["floor_ms"],
+                                              "frac": roof["floor_ms"] / ms_mul}})
     del C
     return out
 
