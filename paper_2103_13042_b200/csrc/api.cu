@@ -198,7 +198,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   if (!tau_ok(tau)) return fail(SPAMM_E_INVALID, "tau must be finite and >= 0");
   if (prec != SPAMM_FP32 && prec != SPAMM_BF16 && prec != SPAMM_FP16 && prec != SPAMM_FP32X3)
     return fail(SPAMM_E_INVALID, "unknown precision");
-  if (flags & ~SPAMM_FLAG_TIMING) return fail(SPAMM_E_INVALID, "unknown plan flag");
+  if (flags & ~(SPAMM_FLAG_TIMING | SPAMM_FLAG_LARGE_TILES)) return fail(SPAMM_E_INVALID, "unknown plan flag");
   if (tile != kTile) {
     if (tile == 64 || tile == 128) return fail(SPAMM_E_UNSUPPORTED, "only tile (LoNum) = 32 is implemented");
     return fail(SPAMM_E_INVALID, "tile must be 32, 64 or 128");
@@ -219,15 +219,19 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->BM = BM;
   p->BK = BK;
   p->BN = BN;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
   const bool tc = !f32_inputs(prec);   // BF16/FP16: 256 x 256 two-issuer tensor path
-  p->MI = p->MJ = tc ? kMacroTC : kMacroF32;
+  // ... unless the problem has fewer 256 x 256 macro-tiles than SMs: then 128 x 128 tiles (4x the CTAs)
+  const int64_t tiles256 = ((BM + kMacroTC - 1) / kMacroTC) * ((BN + kMacroTC - 1) / kMacroTC);
+  p->x1 = tc && !(flags & SPAMM_FLAG_LARGE_TILES) && tiles256 < p->num_sms;
+  const bool dual = tc && !p->x1;
+  p->MI = p->MJ = dual ? kMacroTC : kMacroF32;
   p->GM = (BM + p->MI - 1) / p->MI;
   p->GN = (BN + p->MJ - 1) / p->MJ;
   p->NC = (BK + kChunk - 1) / kChunk;
   p->device = dev;
   p->row_begin_macro = 0;
   p->row_end_macro = p->GM;
-  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nleaf = BM * BN, nmac = p->GM * p->GN;
   spamm_status st = SPAMM_OK;
 #define ALLOC(field, type, count)                                                                   \
@@ -250,8 +254,8 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   ALLOC(d_range, int64_t, kRangeWords);
   // macro lists at their worst case (macro-tile t owns entries [t*BK, t*BK + U[t])): the skip map
   // is one stream-ordered pass with no host synchronisation
-  ALLOC(macro_ent, uint8_t, static_cast<size_t>(tc ? 16 : 8) * static_cast<size_t>(nmac * BK));
-  if (tc) ALLOC(macro_run, uint4, 2 * nmac * BK);   // one 4 x 8 run entry per 128-row half and k-step
+  ALLOC(macro_ent, uint8_t, static_cast<size_t>(dual ? 16 : 8) * static_cast<size_t>(nmac * BK));
+  if (dual) ALLOC(macro_run, uint4, 2 * nmac * BK);   // one 4 x 8 run entry per 128-row half and k-step
 #undef ALLOC
   if (st == SPAMM_OK) {
     p->hist = p->row_work + BM;
@@ -362,7 +366,8 @@ static spamm_status do_skipmap(Plan& p, cudaStream_t s) {
   if (!p.norms_ready) return fail(SPAMM_E_STATE, "spamm_build_skipmap before spamm_norms");
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
-  if (!p.pyr_ready) SPAMM_TRY(launch_pyramid(p, s));
+  // the norm pyramid pays off once there are chunks to skip: K of more than two 32-tile chunks
+  if (!p.pyr_ready && p.NC > 2) SPAMM_TRY(launch_pyramid(p, s));
   // row_work [BM], hist [BK+2] and totals [2] are contiguous in one allocation
   if (!p.ws_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.row_work, 0, sizeof(int64_t) * ws_words(p), s));
   p.ws_zeroed = false;
@@ -392,6 +397,8 @@ spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int
   } else if (p.prec == SPAMM_FP32) {
     SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
                                    s));
+  } else if (p.x1) {
+    SPAMM_TRY(launch_multiply_x1(p, A, lda, B, ldb, C, ldc, s));
   } else {
     SPAMM_TRY(launch_multiply_dual(p, A, lda, B, ldb, C, ldc, s));
   }

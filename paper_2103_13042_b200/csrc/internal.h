@@ -92,6 +92,7 @@ struct Plan {
   int64_t ldpa = 0, ldpb = 0;
   void* im2col = nullptr;         // spamm_conv2d_im2col: the K x N im2col matrix (allocated on first use)
   bool b_is_a = false;            // the last spamm_norms saw B == A (planes of A serve both)
+  bool x1 = false;                // BF16/FP16 on 128 x 128 macro-tiles (fewer 256 x 256 tiles than SMs)
   bool leaf_alloc = false;
 
   // workspace zeroing folded into the previous kernel of a spamm_run / AUTO call: the norm kernel
@@ -199,6 +200,9 @@ spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const fl
 spamm_status launch_multiply_dual(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s);   // SPAMM_FP32X3
+// BF16/FP16 plans with 128 x 128 macro-tiles (small problems, Plan::x1)
+spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                                cudaStream_t s);
 spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s);
 
 // 3-D map: dims {inner, mid, outer} with byte strides {mid_stride, outer_stride}.

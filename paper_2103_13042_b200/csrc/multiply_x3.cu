@@ -20,6 +20,9 @@
 // runs of adjacent C-tile columns with equal row patterns and issues, per run, 6 products x 2
 // tcgen05.mma (M = 128, N = 32*run, K = 16) with the disable-output-lane mask of the skipped
 // C-tile rows -- exact leaf-level skipping, as on the BF16 path.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <cstdlib>
 #include <cstring>
 
@@ -31,18 +34,23 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kStages = 4;
 constexpr int kAPlane = 128 * 32 * 2;              // 8 KB
 constexpr int kBBox = 32 * 32 * 2;                 // 2 KB
-constexpr int kBCol = 3 * kBBox;                   // one 32-column tile, 3 planes
-constexpr int kStageA = 3 * kAPlane;               // 24 KB
-constexpr int kStageBytes = kStageA + 4 * kBCol;   // 48 KB
+// P bfloat16/half planes per operand: P = 3 for SPAMM_FP32X3; P = 1 is the BF16/FP16 path of small
+// problems (fewer 256 x 256 macro-tiles than SMs: 128 x 128 tiles keep more SMs busy)
+template <int P>
+struct XCfg {
+  static constexpr int kStages = P == 3 ? 4 : 8;
+  static constexpr int kBCol = P * kBBox;                     // one 32-column tile, P planes
+  static constexpr int kStageA = P * kAPlane;
+  static constexpr int kStageBytes = kStageA + 4 * kBCol;     // 48 KB (P = 3) / 16 KB (P = 1)
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 512 + 1024;
+};
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
 constexpr int kTQ = 4;
 constexpr int kChunk = 4;                          // k-steps per TMEM partial
 constexpr uint32_t kTmemCols = 256;                // 2 buffers x 128 columns
-constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 512 + 1024;
 constexpr uint32_t kFirst = 1u << 29, kLast = 1u << 30, kNoStep = 1u << 28, kEnd = 1u << 27;
 
 struct TileQ {
@@ -53,13 +61,23 @@ struct X3Maps {
   CUtensorMap a, b;   // 3-D: {cols, rows, plane}
 };
 
+struct XChain {       // chained outputs (P = 1): tile norms of the stored C, a rounded copy, C_low only
+  double* nC;
+  int64_t ldn;
+  void* clow;
+  int64_t ldl;
+  int low_only;
+};
+
+template <int P, uint32_t kFmt, bool kGen>
 __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_x3_kernel(const __grid_constant__ X3Maps mp, const int64_t* __restrict__ mstart,
                         const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
                         const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
                         int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab,
-                        const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p) {
-  if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU: range decided on the device
+                        const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p, const XChain co) {
+  constexpr int kStages = XCfg<P>::kStages, kStageBytes = XCfg<P>::kStageBytes;
+  constexpr int kStageA = XCfg<P>::kStageA, kBCol = XCfg<P>::kBCol;
   // claims follow the skip map's order (skipmap.cu order_pass); every tile, with or without
   // k-steps, goes through the pipeline (the tiles without kept pairs are last)
   (void)n_empty_p;
@@ -99,6 +117,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_wait();      // the skip map (order, lists) and the claim counter are ready
+  pdl_trigger();
+  if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU: range decided on the device
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -186,7 +207,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       const uint32_t base_addr = smem_u32(smem);
       const uint64_t zdesc = smem_desc(smem_u32(sZero), 0, 0, kLayoutSW64);
-      const uint32_t idesc_zero = idesc_f16(1, 128, 128, 0, 1);
+      const uint32_t idesc_zero = idesc_f16(kFmt, 128, 128, 0, 1);
+      constexpr int kProd = P == 3 ? 6 : 1;   // products per kept pair (plane pairs)
       const uint32_t pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0};
       uint32_t ph = 0, ub[2] = {0, 0};
       int buf = 0;
@@ -231,13 +253,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               if (pat) {
                 const uint32_t len = j1 - j;
-                const uint32_t idesc = idesc_f16(1, 128, 0, 0, 1) | ((len * 4u) << 17);   // N = 32 len
+                const uint32_t idesc = idesc_f16(kFmt, 128, 0, 0, 1) | ((len * 4u) << 17);   // N = 32 len
                 const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
                 const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
                 const uint32_t d = dcol + j * 32u;
                 if (elect_one()) {
 #pragma unroll
-                  for (int p = 0; p < 6; ++p) {
+                  for (int p = 0; p < kProd; ++p) {
                     const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
                     const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
                     umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
@@ -305,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         buf ^= 1;
       }
       const int64_t I = cur.t / GN, J = cur.t % GN;
+      double tsum[2] = {0.0, 0.0};   // kGen: sums of squares of the two C tiles of this warp's slice
 #pragma unroll
       for (int lh = 0; lh < 2; ++lh) {
         const int64_t ra = I * 128 + q * 32 + 16 * lh + t1, rb = ra + 8;
@@ -315,12 +338,62 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float v2 = acc[32 * lh + 4 * i + 2], v3 = acc[32 * lh + 4 * i + 3];
           float* ca = C + ra * ldc + col;
           float* cb = C + rb * ldc + col;
-          if (col + 1 < N) {
-            if (ra < M) __stcs(reinterpret_cast<float2*>(ca), axpby2(ab, make_float2(v0, v1), ca));
-            if (rb < M) __stcs(reinterpret_cast<float2*>(cb), axpby2(ab, make_float2(v2, v3), cb));
-          } else if (col < N) {
-            if (ra < M) *ca = axpby1(ab, v0, ca);
-            if (rb < M) *cb = axpby1(ab, v2, cb);
+          if constexpr (!kGen) {
+            if (col + 1 < N) {
+              if (ra < M) __stcs(reinterpret_cast<float2*>(ca), axpby2(ab, make_float2(v0, v1), ca));
+              if (rb < M) __stcs(reinterpret_cast<float2*>(cb), axpby2(ab, make_float2(v2, v3), cb));
+            } else if (col < N) {
+              if (ra < M) *ca = axpby1(ab, v0, ca);
+              if (rb < M) *cb = axpby1(ab, v2, cb);
+            }
+          } else {
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+              const int64_t row = rr ? rb : ra;
+              if (row >= M || col >= N) continue;
+              const bool two = col + 1 < N;
+              float* cp = rr ? cb : ca;
+              float2 x = rr ? make_float2(v2, v3) : make_float2(v0, v1);
+              if (co.low_only) {   // alpha only (beta = 0 is required): no FP32 C exists
+                x = make_float2(ab.alpha * x.x, two ? ab.alpha * x.y : 0.f);
+              } else if (two) {
+                x = axpby2(ab, x, cp);
+                __stcs(reinterpret_cast<float2*>(cp), x);
+              } else {
+                x.x = axpby1(ab, x.x, cp);
+                x.y = 0.f;
+                *cp = x.x;
+              }
+              if (co.clow != nullptr) {   // round to the input type; norms of what is stored (R4)
+                if (kFmt == 1) {
+                  __nv_bfloat16* lp = static_cast<__nv_bfloat16*>(co.clow) + row * co.ldl + col;
+                  const __nv_bfloat16 l0 = __float2bfloat16_rn(x.x), l1 = __float2bfloat16_rn(x.y);
+                  lp[0] = l0;
+                  if (two) lp[1] = l1;
+                  x = make_float2(__bfloat162float(l0), __bfloat162float(l1));
+                } else {
+                  __half* lp = static_cast<__half*>(co.clow) + row * co.ldl + col;
+                  const __half l0 = __float2half_rn(x.x), l1 = __float2half_rn(x.y);
+                  lp[0] = l0;
+                  if (two) lp[1] = l1;
+                  x = make_float2(__half2float(l0), __half2float(l1));
+                }
+              }
+              const double d0 = x.x, d1 = two ? static_cast<double>(x.y) : 0.0;
+              tsum[i >> 2] += d0 * d0 + d1 * d1;
+            }
+          }
+        }
+      }
+      if constexpr (kGen) {
+        if (co.nC != nullptr) {
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt) {
+            double x = tsum[tt];
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            const int64_t ti = I * 4 + q, tj = J * 4 + half * 2 + tt;
+            if (lane == 0 && ti * 32 < M && tj * 32 < N) co.nC[ti * co.ldn + tj] = sqrt(x);
           }
         }
       }
@@ -329,6 +402,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<kTmemCols>(tbase);
+}
+
+}  // namespace
+
+namespace {
+
+template <int P, uint32_t kFmt, bool kGen>
+spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStream_t s) {
+  auto kern = spamm_mul_x3_kernel<P, kFmt, kGen>;
+  constexpr size_t kSmem = XCfg<P>::kSmem;
+  SPAMM_SET_SMEM(kern, static_cast<int>(kSmem), p.device);
+  const int64_t n_tiles = p.range_on_device ? 0 : (p.row_end_macro - p.row_begin_macro) * p.GN;
+  if (!p.range_on_device && n_tiles <= 0) return SPAMM_OK;
+  const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
+  if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
+  p.sched_zeroed = false;
+  SPAMM_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, s, mp, static_cast<const int64_t*>(p.mstart),
+                            static_cast<const int64_t*>(p.U), static_cast<const uint2*>(p.macro_ent),
+                            static_cast<const int32_t*>(p.order), n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
+                            Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
+                            static_cast<const int64_t*>(p.range_on_device ? p.d_range : nullptr),
+                            static_cast<const int64_t*>(p.totals + 2),
+                            XChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0}));
+  count_launch();
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
 }
 
 }  // namespace
@@ -346,20 +445,24 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
                            CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_tmap_3d(&mp.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pB, p.N, p.K, 3, static_cast<uint64_t>(ldb) * 2,
                            static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 3, CU_TENSOR_MAP_SWIZZLE_64B));
-  SPAMM_SET_SMEM(spamm_mul_x3_kernel, static_cast<int>(kSmemBytes), p.device);
-  const int64_t n_tiles = p.range_on_device ? 0 : (p.row_end_macro - p.row_begin_macro) * p.GN;
-  if (!p.range_on_device && n_tiles <= 0) return SPAMM_OK;
-  const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
-  if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
-  p.sched_zeroed = false;
-  spamm_mul_x3_kernel<<<grid, kThreads, kSmemBytes, s>>>(mp, p.mstart, p.U, static_cast<const uint2*>(p.macro_ent),
-                                                         p.order, n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
-                                                         Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                                         p.range_on_device ? p.d_range : nullptr,
-                                                         p.totals + 2);
-  count_launch();
-  SPAMM_CUDA_TRY(cudaGetLastError());
-  return SPAMM_OK;
+  return launch_x<3, 1, false>(p, mp, C, ldc, s);
+}
+
+// BF16/FP16 plans with fewer 256 x 256 macro-tiles than SMs: the same kernel on the inputs
+// themselves (one plane, one product per kept pair) over 128 x 128 macro-tiles
+spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                                cudaStream_t s) {
+  const CUtensorMapDataType dt = p.prec == SPAMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  X3Maps mp;
+  std::memset(&mp, 0, sizeof(mp));
+  SPAMM_TRY(encode_tmap_3d(&mp.a, dt, A, p.K, p.M, 1, static_cast<uint64_t>(lda) * 2,
+                           static_cast<uint64_t>(p.M * lda) * 2, 32, 128, 1, CU_TENSOR_MAP_SWIZZLE_64B));
+  SPAMM_TRY(encode_tmap_3d(&mp.b, dt, B, p.N, p.K, 1, static_cast<uint64_t>(ldb) * 2,
+                           static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 1, CU_TENSOR_MAP_SWIZZLE_64B));
+  const bool gen = p.alpha != 1.0 || p.beta != 0.0 || p.out_norms || p.out_low != nullptr;
+  if (p.prec == SPAMM_BF16)
+    return gen ? launch_x<1, 1, true>(p, mp, C, ldc, s) : launch_x<1, 1, false>(p, mp, C, ldc, s);
+  return gen ? launch_x<1, 0, true>(p, mp, C, ldc, s) : launch_x<1, 0, false>(p, mp, C, ldc, s);
 }
 
 }  // namespace spamm

@@ -249,6 +249,7 @@ struct OrderArgs {
   int64_t t0, t1;
 };
 constexpr int kSmemBuckets = 4096;
+constexpr int64_t kInlineOrderTiles = 4096;   // ranges up to this many macro-tiles: order by the last CTA
 constexpr uint32_t kOrdR = SPAMM_ORD_R, kOrdC = SPAMM_ORD_C;   // super-block of kOrdR x kOrdC macro-tiles
 constexpr int64_t kSbWords = (kOrdR * kOrdC + 63) / 64;        // 64-bit words of a super-block's tile mask
 
@@ -356,13 +357,11 @@ __global__ void __launch_bounds__(1024) order_scan_kernel(const OrderArgs oa) { 
   block_scan_array(blocked ? oa.hist_sb : oa.hist, oa.bucket_pos, blocked ? oa.nsb : oa.BK + 1, false, s_warp);
 }
 
-__global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa) {
-  __shared__ int64_t s_warp[33];
-  __shared__ int64_t s_pos[kSmemBuckets + 1];
-  sm100::pdl_wait();
-  sm100::pdl_trigger();
-  int64_t t0, t1;
-  order_range(oa, t0, t1);
+// Place the work list into the claim order and append the empty tiles.  CTA `cta` of `ncta` (the
+// scatter kernel: one per SM; the skip map's last CTA for small ranges: 1 of 1); s_pos = shared
+// memory of kSmemBuckets + 1 words.
+__device__ void order_place(const OrderArgs& oa, int64_t t0, int64_t t1, int cta, int ncta, int64_t* s_pos,
+                            int64_t* s_warp) {
   const int64_t n_work = oa.cnt[0], n_empty = oa.cnt[1];
   const bool blocked = n_work >= 16 * static_cast<int64_t>(oa.num_sms);
   const int64_t nbucket = blocked ? oa.nsb : oa.BK + 1;
@@ -371,9 +370,9 @@ __global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa)
     block_scan_array(blocked ? oa.hist_sb : oa.hist, s_pos, nbucket, false, s_warp);
     base = s_pos;
   }
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t stride = static_cast<int64_t>(ncta) * blockDim.x;
   if (blocked) {   // slot = super-block start + rank of the tile among its block's working tiles (row-major)
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_work; i += stride) {
+    for (int64_t i = static_cast<int64_t>(cta) * blockDim.x + threadIdx.x; i < n_work; i += stride) {
       const int64_t t = oa.work[i];
       const int64_t sb = sb_of(t, t0, oa.GN);
       const uint32_t b = sb_pos(t, t0, oa.GN);
@@ -383,9 +382,9 @@ __global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa)
       rank += __popcll(w[b / 64] & ((1ull << (b % 64)) - 1ull));
       oa.order[base[sb] + rank] = static_cast<int32_t>(t);
     }
-  } else if (blockIdx.x == 0) {
-    // LPT: one CTA walks the range in tile order, one 1024-tile window at a time, so equal keys
-    // (Toeplitz bands have many equal U) keep row-major order -- neighbouring tiles run together
+  } else if (cta == 0) {
+    // LPT: one CTA walks the range in tile order, one window at a time, so equal keys (Toeplitz
+    // bands have many equal U) keep row-major order -- neighbouring tiles run together
     unsigned long long* pos = nbucket <= kSmemBuckets ? reinterpret_cast<unsigned long long*>(s_pos)
                                                       : reinterpret_cast<unsigned long long*>(oa.bucket_cnt);
     for (int64_t c0 = t0; c0 < t1; c0 += blockDim.x) {
@@ -398,10 +397,20 @@ __global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa)
       __syncthreads();
     }
   }
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_empty; i += stride)
+  for (int64_t i = static_cast<int64_t>(cta) * blockDim.x + threadIdx.x; i < n_empty; i += stride)
     oa.order[n_work + i] = oa.empty[i];
-  if (blockIdx.x == 0 && threadIdx.x == 0) oa.totals[2] = n_empty;
-  if (blockIdx.x == 0 && threadIdx.x < 4 && oa.sched) oa.sched[threadIdx.x] = 0u;
+  if (cta == 0 && threadIdx.x == 0) oa.totals[2] = n_empty;
+  if (cta == 0 && threadIdx.x < 4 && oa.sched) oa.sched[threadIdx.x] = 0u;
+}
+
+__global__ void __launch_bounds__(1024) order_scatter_kernel(const OrderArgs oa) {
+  __shared__ int64_t s_warp[33];
+  __shared__ int64_t s_pos[kSmemBuckets + 1];
+  sm100::pdl_wait();
+  sm100::pdl_trigger();
+  int64_t t0, t1;
+  order_range(oa, t0, t1);
+  order_place(oa, t0, t1, blockIdx.x, gridDim.x, s_pos, s_warp);
 }
 
 struct SkipArgs {
@@ -426,7 +435,11 @@ struct SkipArgs {
 // k chunk c from the pyramid, then the surviving chunks are decided one at a time in ascending k
 // (lane = k), each writing its entries at warp-scanned offsets.
 template <int MI, int MJ>
-__global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a, const OrderArgs oa, int lists) {
+__global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a, const OrderArgs oa, int lists,
+                                                               int inline_order) {
+  __shared__ int64_t s_warp[33];
+  __shared__ int s_last;
+  extern __shared__ int64_t s_dyn[];   // inline order: kSmemBuckets + 1 bucket starts
   using M_ = mask_t<MI, MJ>;
   constexpr bool kMask64 = MI * MJ > 32;          // 8 x 8 tiles: (k, mask_lo, mask_hi, 0) entries
   const int lane = threadIdx.x & 31;
@@ -468,9 +481,13 @@ __global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a,
       const int64_t c = c0 + lane;
       uint32_t cls = 0;
       if (c < a.NC && valid != 0u) {
-        const double amax = paMax[I * a.NC + c], bmax = pbMax[J * a.NC + c];
-        if (!(__dmul_rn(amax, bmax) < tau))
-          cls = __dmul_rn(paMin[I * a.NC + c], pbMin[J * a.NC + c]) >= tau ? 2u : 1u;
+        if (a.pyr == nullptr) {   // small K: no pyramid, every chunk tests its pairs
+          cls = 1u;
+        } else {
+          const double amax = paMax[I * a.NC + c], bmax = pbMax[J * a.NC + c];
+          if (!(__dmul_rn(amax, bmax) < tau))
+            cls = __dmul_rn(paMin[I * a.NC + c], pbMin[J * a.NC + c]) >= tau ? 2u : 1u;
+        }
       }
       uint32_t surv = __ballot_sync(0xffffffffu, cls != 0u);
       const uint32_t full = __ballot_sync(0xffffffffu, cls == 2u);
@@ -549,6 +566,16 @@ __global__ void __launch_bounds__(kWarps * 32) skip_pyr_kernel(const SkipArgs a,
     atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals), static_cast<unsigned long long>(w_kept));
     atomicAdd(reinterpret_cast<unsigned long long*>(oa.totals) + 1, static_cast<unsigned long long>(w_ents));
   }
+  if (!inline_order) return;
+  // small ranges: the last CTA to finish places the claim order itself (saves a launch)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(oa.cnt + 3, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  order_place(oa, gi0 * a.GN, gi1 * a.GN, 0, 1, s_dyn, s_warp);
+  if (threadIdx.x == 0) oa.cnt[3] = 0u;
 }
 
 // Per-C-tile k lists (C tile (i,j) owns slots [(i*BN+j)*BK, +V)) expanded from the macro lists:
@@ -657,19 +684,24 @@ spamm_status skip_t(Plan& p, int64_t gi0, int64_t gi1, bool on_device, bool orde
   constexpr int kPerSm = 4;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n_macro + kWarps - 1) / kWarps,
                                                                 static_cast<int64_t>(p.num_sms) * kPerSm));
-  SkipArgs a{p.nA, p.nBt, p.pyr, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.tau, gi0, gi1, 0, 0,
+  SkipArgs a{p.nA, p.nBt, p.pyr_ready ? p.pyr : nullptr, p.BM, p.BK, p.BN, p.GM, p.GN, p.NC, p.tau, gi0, gi1, 0, 0,
              on_device ? p.d_range : nullptr, p.U, p.L,
              row_work ? reinterpret_cast<unsigned long long*>(p.row_work) : nullptr, p.macro_ent, p.macro_run,
              p.ws_cnt + (on_device ? 3 : 2)};
   OrderArgs oa{p.hist, p.hist_sb, p.bucket_cnt, p.bucket_pos, p.sb_bits, p.NSB, p.U, p.L, p.BK, p.GN, p.num_sms, p.tile_lists,
                p.tile_lists + p.GM * p.GN, p.ws_cnt, p.order, p.totals, p.sched, on_device ? p.d_range : nullptr,
                gi0 * p.GN, gi1 * p.GN};
-  // the main loop builds the order's lists unless part of the range came from another launch
+  // the main loop builds the order's lists unless part of the range came from another launch; small
+  // ranges get their order from the skip kernel's last CTA (no scatter launch)
   const int lists = order && !on_device ? 1 : 0;
-  SPAMM_CUDA_TRY(launch_pdl(skip_pyr_kernel<MI, MJ>, dim3(static_cast<unsigned>(blocks)), dim3(kWarps * 32), 0, s, a,
-                            oa, lists));
+  const bool inl = lists && n_macro <= kInlineOrderTiles && std::max<int64_t>(p.BK + 1, p.NSB) <= kSmemBuckets;
+  const int dyn = inl ? static_cast<int>((kSmemBuckets + 1) * sizeof(int64_t)) : 0;
+  auto kern = skip_pyr_kernel<MI, MJ>;
+  SPAMM_SET_SMEM(kern, static_cast<int>((kSmemBuckets + 1) * sizeof(int64_t)), p.device);
+  SPAMM_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(kWarps * 32), dyn, s, a, oa, lists,
+                            inl ? 1 : 0));
   count_launch();
-  if (order) {
+  if (order && !inl) {
     // one CTA per 1024 macro-tiles of the range, at most one per SM
     const unsigned g = static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(p.num_sms, ((on_device ? p.GM : gi1 - gi0) * p.GN + 1023) / 1024)));

@@ -1,8 +1,9 @@
-"""GPU parity of the BF16/FP16 tensor-core multiply (multiply_dual.cu: 256 x 256 macro-tiles,
-two MMA issuers) on shapes that exercise its schedule -- ragged edges, N % 32 != 0 (2-D B boxes,
-clipped stores), K much larger than M, one-tile grids, banded products with mostly empty
-macro-tiles (zero-filled by the epilogue warps) -- and its general epilogue (alpha / beta,
-chained outputs, BF16/FP16-only output).  Bars: skip map bit-exact outside the 1e-6 tie band,
+"""GPU parity of the BF16/FP16 tensor-core multiplies -- multiply_dual.cu (256 x 256 macro-tiles,
+two MMA issuers; forced with SPAMM_FLAG_LARGE_TILES on small shapes) and the 128 x 128 path of
+small problems (multiply_x3.cu with one plane: "auto" on these shapes) -- on shapes that exercise
+their schedules -- ragged edges, N % 32 != 0 (2-D B boxes, clipped stores), K much larger than M,
+one-tile grids, banded products with mostly empty macro-tiles -- and their general epilogues
+(alpha / beta, chained outputs, BF16/FP16-only output).  Bars: skip map bit-exact outside the 1e-6 tie band,
 C within 2e-2 (north_star) and 1e-5 (FP32 accumulation of the same rounded inputs).
 PAPER.md:127 (the product), 187 (FP32 accumulation), 47 (alpha, beta)."""
 import numpy as np
@@ -19,22 +20,27 @@ SHAPES = [(256, 256, 256), (300, 512, 129), (1000, 768, 600), (64, 256, 4096), (
           (300, 257, 129), (129, 1000, 384)]   # the last two: N % 32 != 0
 
 
+TILES = {"large": 2, "auto": 0}   # plan flags: SPAMM_FLAG_LARGE_TILES / automatic choice
+
+
 def _tau_at(nA, nB, q):
     prods = np.unique(nA[:, :, None] * nB[None, :, :])
     i = min(int(q * (len(prods) - 1)), len(prods) - 2)
     return float(0.5 * (prods[i] + prods[i + 1]))
 
 
+@pytest.mark.parametrize("tiles", ["large", "auto"])
 @pytest.mark.parametrize("prec", ["bf16", "fp16"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("q", [0.0, 0.5, 0.9])
-def test_dual_parity(sp, prec, shape, q):
+def test_dual_parity(sp, prec, shape, q, tiles):
     M, N, K = shape
     A = _rounded(synth.perturbed_decay_matrix(K, 0.97, seed=11, m=M), prec)
     B = _rounded(synth.perturbed_decay_matrix(N, 0.97, seed=12, m=K), prec)
     nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
     tau = 0.0 if q == 0.0 else _tau_at(nA, nB, q)
-    plan = sp.Plan(M, N, K, tau, prec)
+    plan = sp.Plan(M, N, K, tau, prec, flags=TILES[tiles])
+    assert plan.stats()["macro_i"] == (8 if tiles == "large" else 4)
     Ad, Bd = _dev(A, prec), _dev(B, prec)
     Cbuf = torch.full((M, -(-N // 4) * 4), float("nan"), dtype=torch.float32, device="cuda")
     C = Cbuf[:, :N]
@@ -52,15 +58,16 @@ def test_dual_parity(sp, prec, shape, q):
     assert _rel_fro(C.cpu().numpy(), ref) <= 1e-5
 
 
+@pytest.mark.parametrize("tiles", ["large", "auto"])
 @pytest.mark.parametrize("prec", ["bf16", "fp16"])
-def test_dual_decay_band(sp, prec):
+def test_dual_decay_band(sp, prec, tiles):
     """A banded exponential-decay product (the bench workload's structure, N = 2048): most
     macro-tiles are empty (zero-filled by the epilogue warps), the band's are dense."""
     N = 2048
     A = _rounded(synth.decay_matrix(N, "exp", 0.99), prec)
     nA = oracle.tile_norms(A, T)
     tau = 1e-6
-    plan = sp.Plan(N, N, N, tau, prec)
+    plan = sp.Plan(N, N, N, tau, prec, flags=TILES[tiles])
     Ad = _dev(A, prec)
     C = torch.full((N, N), float("nan"), dtype=torch.float32, device="cuda")
     plan.run(Ad, Ad, C)
@@ -70,8 +77,9 @@ def test_dual_decay_band(sp, prec):
     assert err <= 1e-5, err
 
 
+@pytest.mark.parametrize("tiles", ["large", "auto"])
 @pytest.mark.parametrize("alpha,beta", [(-0.5, 0.0), (2.0, 1.5), (0.0, 0.5)])
-def test_dual_alpha_beta(sp, alpha, beta):
+def test_dual_alpha_beta(sp, alpha, beta, tiles):
     M, N, K = 300, 512, 129
     prec = "bf16"
     A = _rounded(synth.perturbed_decay_matrix(K, 0.95, seed=91, m=M), prec)
@@ -79,7 +87,7 @@ def test_dual_alpha_beta(sp, alpha, beta):
     C0 = synth.random_matrix(M, N, seed=93)
     nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
     tau = _tau_at(nA, nB, 0.7)
-    plan = sp.Plan(M, N, K, tau, prec)
+    plan = sp.Plan(M, N, K, tau, prec, flags=TILES[tiles])
     plan.set_scalars(alpha, beta)
     Cbuf = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
     if beta != 0.0:
@@ -90,7 +98,8 @@ def test_dual_alpha_beta(sp, alpha, beta):
     assert _rel_fro(Cbuf.cpu().numpy(), ref) <= 5e-6
 
 
-def test_dual_chain(sp):
+@pytest.mark.parametrize("tiles", ["large", "auto"])
+def test_dual_chain(sp, tiles):
     """Chained outputs: C, C_low = RNE(C), nC = Eq. 2 of C_low."""
     M, N, K = 300, 512, 129
     prec = "bf16"
@@ -98,7 +107,7 @@ def test_dual_chain(sp):
     B = _rounded(synth.perturbed_decay_matrix(N, 0.95, seed=102, m=K), prec)
     nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
     tau = _tau_at(nA, nB, 0.4)
-    plan = sp.Plan(M, N, K, tau, prec)
+    plan = sp.Plan(M, N, K, tau, prec, flags=TILES[tiles])
     C = torch.empty((M, N), dtype=torch.float32, device="cuda")
     Cl = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
     plan.multiply_chain(_dev(A, prec), _dev(B, prec), C, Cl, flags=sp.SPAMM_MUL_AUTO | sp.SPAMM_MUL_OUTPUT_NORMS)
@@ -110,9 +119,10 @@ def test_dual_chain(sp):
                                rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("tiles", ["large", "auto"])
 @pytest.mark.parametrize("prec", ["bf16", "fp16"])
 @pytest.mark.parametrize("alpha", [1.0, -2.0])
-def test_dual_low_precision_output_only(sp, prec, alpha):
+def test_dual_low_precision_output_only(sp, prec, alpha, tiles):
     """SPAMM_MUL_LOW_ONLY: the result is written only as BF16/FP16 (RNE of the
     FP32 accumulator times alpha); no FP32 C is passed or written.  Equals rounding the oracle's
     product up to the FP32 accumulation (compared after rounding both: the bits may differ only
@@ -123,7 +133,7 @@ def test_dual_low_precision_output_only(sp, prec, alpha):
     nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
     tau = _tau_at(nA, nB, 0.5)
     dt = torch.bfloat16 if prec == "bf16" else torch.float16
-    plan = sp.Plan(M, N, K, tau, prec)
+    plan = sp.Plan(M, N, K, tau, prec, flags=TILES[tiles])
     plan.set_scalars(alpha, 0.0)
     Cl = torch.full((M, -(-N // 8) * 8), float("nan"), dtype=dt, device="cuda")[:, :N]
     sp.spamm_multiply_chain(plan.handle, _dev(A, prec), _dev(B, prec), None, Cl,
