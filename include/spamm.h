@@ -72,8 +72,9 @@ typedef enum {
 #define SPAMM_FLAG_TIMING         1u  /* record per-stage CUDA events (spamm_get_stats) */
 #define SPAMM_FLAG_LARGE_TILES    2u  /* BF16/FP16: always schedule 256 x 256 macro-tiles (8 x 8 C tiles,
                                          two MMA issuers per SM).  Without it, problems with fewer such
-                                         tiles than SMs use 128 x 128 macro-tiles (4 x 4 C tiles) so that
-                                         more SMs work; results are identical up to FP32 rounding order. */
+                                         tiles than SMs whose 128 x 128 tiles fit one wave use 128 x 128
+                                         macro-tiles (4 x 4 C tiles) so that more SMs work; results agree
+                                         up to FP32 rounding order. */
 
 /* spamm_multiply flags */
 #define SPAMM_MUL_AUTO            1u  /* run spamm_norms + spamm_build_skipmap first (spamm_run) */

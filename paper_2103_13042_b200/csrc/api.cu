@@ -221,9 +221,12 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->BN = BN;
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
   const bool tc = !f32_inputs(prec);   // BF16/FP16: 256 x 256 two-issuer tensor path
-  // ... unless the problem has fewer 256 x 256 macro-tiles than SMs: then 128 x 128 tiles (4x the CTAs)
+  // ... unless the problem has fewer 256 x 256 macro-tiles than SMs and its 128 x 128 tiles still fit
+  // one wave: then 128 x 128 tiles (up to 4x the CTAs; measured: N = 1024 multiply 17.5 -> 15.3 us,
+  // but conv2_1's 200 tiles in two waves 17 -> 29 us, so that shape stays on 256 x 256)
   const int64_t tiles256 = ((BM + kMacroTC - 1) / kMacroTC) * ((BN + kMacroTC - 1) / kMacroTC);
-  p->x1 = tc && !(flags & SPAMM_FLAG_LARGE_TILES) && tiles256 < p->num_sms;
+  const int64_t tiles128 = ((BM + kMacroF32 - 1) / kMacroF32) * ((BN + kMacroF32 - 1) / kMacroF32);
+  p->x1 = tc && !(flags & SPAMM_FLAG_LARGE_TILES) && tiles256 < p->num_sms && tiles128 <= p->num_sms;
   const bool dual = tc && !p->x1;
   p->MI = p->MJ = dual ? kMacroTC : kMacroF32;
   p->GM = (BM + p->MI - 1) / p->MI;
