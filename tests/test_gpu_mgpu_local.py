@@ -34,10 +34,12 @@ def _leaf_lists(sp, plan, rows, BN):
     return {(i, j): tuple(kidx[start[i * BN + j]:start[i * BN + j] + V[i, j]]) for i in rows for j in range(BN)}
 
 
-@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp32x3"])
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp32x3", "bf16-small"])
 @pytest.mark.parametrize("nranks", [2, 3, 8])
 def test_p4_ranks_equal_single_gpu(sp, prec, nranks):
-    M = N = K = 2080 if prec != "bf16" else 4100   # several macro rows per rank, ragged edge
+    # several macro rows per rank, ragged edge; "bf16-small": the 128 x 128 BF16 path (tiles fit one wave)
+    M = N = K = {"bf16": 4100, "bf16-small": 1000}.get(prec, 2080)
+    prec = "bf16" if prec == "bf16-small" else prec
     lam = 0.995
     A = _rounded(synth.perturbed_decay_matrix(K, lam, seed=131, m=M), prec)
     B = _rounded(synth.perturbed_decay_matrix(N, lam, seed=132, m=K), prec)
