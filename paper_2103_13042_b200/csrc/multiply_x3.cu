@@ -7,7 +7,7 @@
 // pair contributes the six products whose order is at most 2^-16 relative to a0 b0:
 //   a0b0 + a0b1 + a1b0 + a0b2 + a1b1 + a2b0      (dropped: a1b2, a2b1 ~2^-24, a2b2 ~2^-32)
 // so every product is FP32-accurate.  Accumulation is two-level: the tensor core's FP32
-// accumulator in TMEM only ever sums kChunk k-steps (6 x 2 MMAs each); the epilogue adds the
+// accumulator in TMEM only ever sums 4 k-steps (6 x 2 MMAs each); the epilogue adds the
 // chunk partials into a per-thread FP32 running sum with IEEE adds, alternating between two
 // TMEM buffers so the next chunk's MMAs overlap the add.  (A single TMEM accumulation over
 // thousands of MMAs drifts by ~2^-24 per MMA: measured 4e-5 at K = 16384 on the BF16 path.)
@@ -23,6 +23,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -49,9 +51,44 @@ struct XCfg {
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
 constexpr int kTQ = 4;
-constexpr int kChunk = 4;                          // k-steps per TMEM partial
+// k-steps per TMEM partial: 4 for FP32X3 (FP32 accuracy, above); the one-plane BF16/FP16 path
+// accumulates a whole tile in TMEM like the 256 x 256 kernel (one epilogue read per tile)
+template <int P>
+constexpr uint32_t kChunkOf = P == 3 ? 4u : 0x40000000u;
 constexpr uint32_t kTmemCols = 256;                // 2 buffers x 128 columns
 constexpr uint32_t kFirst = 1u << 29, kLast = 1u << 30, kNoStep = 1u << 28, kEnd = 1u << 27;
+
+// Runs of a 4 x 4 keep mask (bit 4 li + lj: C-tile row li, column lj): maximal groups of adjacent
+// kept columns with equal row patterns, one MMA group each (N = 32 len, disable-output-lane masks
+// from the pattern).  8 bits per run (j0: 2, len - 1: 2, row pattern: 4); .x runs 0-3, .y = count |
+// needed-columns << 4.  Encoded by the producer warp, one entry per lane, so the MMA thread only
+// unpacks (decoding the mask there cost ~700 cycles per k-step of a single warp's dependent chain,
+// measured with -DSPAMM_PROFILE on configs[0]).
+__device__ __forceinline__ uint2 encode_runs4(uint32_t mask) {
+  if (mask == 0xFFFFu) return make_uint2((3u << 2) | (15u << 4), 1u | (15u << 4));
+  const uint32_t d = (mask ^ (mask >> 1)) & 0x7777u;   // col lj differs from lj+1 in some row
+  const uint32_t bnd = (d | (d >> 4) | (d >> 8) | (d >> 12)) & 0x7u;
+  const uint32_t nz = (mask | (mask >> 4) | (mask >> 8) | (mask >> 12)) & 0xFu;
+  uint32_t w = 0u, nr = 0u, j = 0u;
+  while (j < 4u) {
+    const uint32_t b = bnd >> j;
+    const uint32_t j1 = b ? j + static_cast<uint32_t>(__ffs(b)) : 4u;
+    if ((nz >> j) & 1u) {
+      const uint32_t pat = ((mask >> j) & 1u) | (((mask >> (4 + j)) & 1u) << 1) | (((mask >> (8 + j)) & 1u) << 2) |
+                           (((mask >> (12 + j)) & 1u) << 3);
+      w |= (j | ((j1 - j - 1u) << 2) | (pat << 4)) << (8u * nr);
+      ++nr;
+    }
+    j = j1;
+  }
+  return make_uint2(w, nr | (nz << 4));
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
+}
 
 struct TileQ {
   int64_t t, e0, e1;
@@ -68,6 +105,28 @@ struct XChain {       // chained outputs (P = 1): tile norms of the stored C, a 
   int64_t ldl;
   int low_only;
 };
+
+#ifdef SPAMM_PROFILE
+// per-CTA timeline (globaltimer ns) [0] start [1] after griddepcontrol.wait [2] first TMA issued
+// [3] first stage landed (MMA) [4] MMA done [5] epilogue last TMEM read [6] epilogue done;
+// counters (clock64 cycles) [8] MMA full-wait [9] MMA tmem-empty wait [10] epilogue tmem-full wait
+// [11] producer empty-wait [12] k-steps (compile with -DSPAMM_PROFILE)
+__device__ unsigned long long* g_x3_prof;
+#define X3_STAMP(k) do { unsigned long long g_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)); \
+  g_x3_prof[blockIdx.x * 24 + (k)] = g_; } while (0)
+#define X3_CLK() clock64()
+#define X3_ADD(k, v) (pc[(k) - 8] += (v))   // register counters, stored once at the end
+#else
+#define X3_STAMP(k) do { } while (0)
+#define X3_CLK() 0ll
+#define X3_ADD(k, v) do { (void)(v); } while (0)
+#endif
+#ifdef SPAMM_PROFILE
+#define X3_FLUSH() do { for (int k_ = 0; k_ < 12; ++k_) if (pc[k_]) atomicAdd(g_x3_prof + blockIdx.x * 24 + 8 + k_, \
+  static_cast<unsigned long long>(pc[k_])); } while (0)
+#else
+#define X3_FLUSH() do { } while (0)
+#endif
 
 template <int P, uint32_t kFmt, bool kGen>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -95,6 +154,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTQ);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) X3_STAMP(0);
+#ifdef SPAMM_PROFILE
+  long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool st2 = false, st3 = false;
+#endif
   for (int i = threadIdx.x; i < 512 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
@@ -119,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tbase = *tmem_slot;
   pdl_wait();      // the skip map (order, lists) and the claim counter are ready
   pdl_trigger();
+  if (threadIdx.x == 0) X3_STAMP(1);
   if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU: range decided on the device
 
   if (warp == 0) {
@@ -175,16 +240,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t eb = cur.e0; eb < cur.e1; eb += 32) {
         const int cnt = static_cast<int>(cur.e1 - eb < 32 ? cur.e1 - eb : 32);
         const uint2 en_l = lane < cnt ? ment[eb + lane] : make_uint2(0u, 0u);
+        const uint2 run_l = encode_runs4(en_l.y & 0xFFFFu);
         for (int q = 0; q < cnt; ++q) {
-          const uint32_t ex = __shfl_sync(0xffffffffu, en_l.x, q), ey = __shfl_sync(0xffffffffu, en_l.y, q);
+          const uint32_t ex = __shfl_sync(0xffffffffu, en_l.x, q);
+          const uint32_t rw = __shfl_sync(0xffffffffu, run_l.x, q), rn = __shfl_sync(0xffffffffu, run_l.y, q);
           const int64_t e = eb + q;
-          const uint32_t mask = ey & 0xFFFFu;
-          const uint32_t cols = (mask | (mask >> 4) | (mask >> 8) | (mask >> 12)) & 0xFu;   // needed C-tile columns
+          const uint32_t cols = rn >> 4;   // needed C-tile columns
           const int32_t k0 = static_cast<int32_t>(ex) * 32;
+          const long long tw0 = X3_CLK();
           mbar_wait(&empty[s], ph ^ 1);
+          if (lane == 0) X3_ADD(11, X3_CLK() - tw0);
           uint8_t* st = smem + s * kStageBytes;
+#ifdef SPAMM_PROFILE
+          if (lane == 0 && !st2) {
+            X3_STAMP(2);
+            st2 = true;
+          }
+#endif
           if (elect_one()) {
-            srun[s] = make_uint4(ex, mask, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
+            srun[s] = make_uint4(rw, rn & 0xFu, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
             mbar_arrive_expect_tx(&full[s], kStageA + kBCol * __popc(cols));
             tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
 #pragma unroll
@@ -210,19 +284,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc_zero = idesc_f16(kFmt, 128, 128, 0, 1);
       constexpr int kProd = P == 3 ? 6 : 1;   // products per kept pair (plane pairs)
       const uint32_t pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0};
-      uint32_t ph = 0, ub[2] = {0, 0};
+      uint32_t ph = 0, ub = 0;   // bit b: phase parity of TMEM buffer b (no local-memory array)
       int buf = 0;
-      int64_t kin = 0;   // k-steps of the current tile issued so far
+      uint32_t kin = 0;   // k-steps of the current tile issued so far
       bool fin = false;
       while (!fin) {
 #pragma unroll 1
         for (int st = 0; st < kStages; ++st) {
+          const long long tw0 = X3_CLK();
           mbar_wait(&full[st], ph);
+          if (lane == 0) X3_ADD(8, X3_CLK() - tw0);
+#ifdef SPAMM_PROFILE
+          if (lane == 0 && !st3) {
+            X3_STAMP(3);
+            st3 = true;
+          }
+#endif
           tc_fence_after();
-          uint4 rs = srun[st];
-          rs.x = __shfl_sync(0xffffffffu, rs.x, 0);
-          rs.y = __shfl_sync(0xffffffffu, rs.y, 0);
-          rs.w = __shfl_sync(0xffffffffu, rs.w, 0);
+          const uint4 rs = lds128(smem_u32(srun + st));   // (runs, run count, -, flags): same for all lanes
           const uint32_t fl = rs.w;
           if (fl & kEnd) {
             fin = true;
@@ -230,8 +309,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (fl & kFirst) kin = 0;
           const uint32_t dcol = tbase + static_cast<uint32_t>(buf) * 128u;
-          if ((kin % kChunk) == 0) {   // chunk start: a drained buffer, zeroed
-            mbar_wait(&tempty[buf], ub[buf] & 1u);
+          if ((kin % kChunkOf<P>) == 0) {   // chunk start: a drained buffer, zeroed
+            const long long tw1 = X3_CLK();
+            mbar_wait(&tempty[buf], (ub >> buf) & 1u);
+            if (lane == 0) X3_ADD(9, X3_CLK() - tw1);
             tc_fence_after();
             if (elect_one()) umma_f16(dcol, zdesc, zdesc, idesc_zero, 0u, 0u, 0u, 0u, 0u);
           }
@@ -239,48 +320,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t a_addr = base_addr + st * kStageBytes, b_addr = a_addr + kStageA;
             const uint64_t ad = smem_desc(a_addr, 16, 512, kLayoutSW64);
             const uint64_t bd = smem_desc(b_addr, kBCol, 512, kLayoutSW64);
-            const uint32_t mask = rs.y;
-            uint32_t j = 0;
-            while (j < 4) {
-              const uint32_t pat = ((mask >> j) & 1u) | (((mask >> (4 + j)) & 1u) << 1) |
-                                   (((mask >> (8 + j)) & 1u) << 2) | (((mask >> (12 + j)) & 1u) << 3);
-              uint32_t j1 = j + 1;
-              while (j1 < 4) {
-                const uint32_t p1 = ((mask >> j1) & 1u) | (((mask >> (4 + j1)) & 1u) << 1) |
-                                    (((mask >> (8 + j1)) & 1u) << 2) | (((mask >> (12 + j1)) & 1u) << 3);
-                if (p1 != pat) break;
-                ++j1;
-              }
-              if (pat) {
-                const uint32_t len = j1 - j;
-                const uint32_t idesc = idesc_f16(kFmt, 128, 0, 0, 1) | ((len * 4u) << 17);   // N = 32 len
-                const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
-                const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
-                const uint32_t d = dcol + j * 32u;
-                if (elect_one()) {
 #pragma unroll
-                  for (int p = 0; p < kProd; ++p) {
-                    const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
-                    const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
-                    umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
-                    umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
-                  }
+            for (uint32_t r = 0; r < 4; ++r) {
+              if (r >= rs.y) break;
+              const uint32_t run = (rs.x >> (8u * r)) & 0xFFu;
+              const uint32_t j = run & 3u, len = ((run >> 2) & 3u) + 1u, pat = run >> 4;
+              const uint32_t idesc = idesc_f16(kFmt, 128, 0, 0, 1) | ((len * 4u) << 17);   // N = 32 len
+              const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
+              const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
+              const uint32_t d = dcol + j * 32u;
+              const long long ti0 = X3_CLK();
+              if (elect_one()) {
+#pragma unroll
+                for (int p = 0; p < kProd; ++p) {
+                  const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
+                  const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
+                  umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
+                  umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
                 }
               }
-              j = j1;
+              __syncwarp();
+              if (lane == 0) X3_ADD(14, X3_CLK() - ti0);
             }
           }
+          const long long tc0 = X3_CLK();
           if (elect_one()) umma_commit(&empty[st]);
+          __syncwarp();
+          if (lane == 0) X3_ADD(15, X3_CLK() - tc0);
+          if (lane == 0 && !(fl & kNoStep)) X3_ADD(12, 1);
+          if (lane == 0) X3_ADD(13, X3_CLK() - tw0);
           ++kin;
-          if ((fl & kLast) || (kin % kChunk) == 0) {   // chunk complete: hand the buffer over
+          if ((fl & kLast) || (kin % kChunkOf<P>) == 0) {   // chunk complete: hand the buffer over
             if (elect_one()) umma_commit(&tfull[buf]);
-            ++ub[buf];
+            ub ^= 1u << buf;
             buf ^= 1;
           }
         }
         ph ^= 1;
       }
     }
+    if (lane == 0) X3_STAMP(4);
     __syncwarp();
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
@@ -293,11 +372,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&tempty[1]);
     }
     const int t0 = lane & 3, t1 = lane >> 2;
-    uint32_t eu[2] = {0, 0};
+    uint32_t eu = 0;   // bit b: phase parity of TMEM buffer b
     int buf = 0, tq_s = 0;
     uint32_t tq_ph = 0;
     for (;;) {
+      const long long tq0 = X3_CLK();
       mbar_wait(&tq_full[tq_s], tq_ph);
+      if (warp == 4 && lane == 0) X3_ADD(17, X3_CLK() - tq0);
       const TileQ cur = tq[tq_s];
       __syncwarp();
       if (lane == 0) mbar_arrive(&tq_empty[tq_s]);
@@ -307,10 +388,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (cur.t < 0) break;
       const int64_t U = cur.e1 - cur.e0;
-      const int64_t nch = U > 0 ? (U + kChunk - 1) / kChunk : 1;
+      const int64_t nch = U > 0 ? (U + kChunkOf<P> - 1) / kChunkOf<P> : 1;
       float acc[64];
       for (int64_t c = 0; c < nch; ++c) {
-        mbar_wait(&tfull[buf], eu[buf] & 1u);
+        const long long tw0 = X3_CLK();
+        mbar_wait(&tfull[buf], (eu >> buf) & 1u);
+        if (warp == 4 && lane == 0) X3_ADD(10, X3_CLK() - tw0);
         tc_fence_after();
 #pragma unroll
         for (int lh = 0; lh < 2; ++lh) {
@@ -323,9 +406,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
-        ++eu[buf];
+        eu ^= 1u << buf;
         buf ^= 1;
       }
+      if (warp == 4 && lane == 0) X3_STAMP(5);
+      const long long tst0 = X3_CLK();
       const int64_t I = cur.t / GN, J = cur.t % GN;
       double tsum[2] = {0.0, 0.0};   // kGen: sums of squares of the two C tiles of this warp's slice
 #pragma unroll
@@ -385,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (warp == 4 && lane == 0) X3_ADD(16, X3_CLK() - tst0);
       if constexpr (kGen) {
         if (co.nC != nullptr) {
 #pragma unroll
@@ -399,6 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (warp == 4 && lane == 0) X3_STAMP(6);
+  if (lane == 0) X3_FLUSH();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<kTmemCols>(tbase);
@@ -407,6 +495,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 namespace {
+
+#ifdef SPAMM_PROFILE
+static void print_x3_profile(const unsigned long long* hp, int grid, int P) {
+  unsigned long long g0 = ~0ull;
+  for (int c = 0; c < grid; ++c) g0 = std::min(g0, hp[c * 24]);
+  double m[7] = {0}, mx[7] = {0}, cn[12] = {0};
+  for (int c = 0; c < grid; ++c) {
+    for (int k = 0; k < 7; ++k) {
+      const double v = hp[c * 24 + k] ? (static_cast<double>(hp[c * 24 + k]) - static_cast<double>(g0)) * 1e-3 : 0.0;
+      m[k] += v / grid;
+      mx[k] = std::max(mx[k], v);
+    }
+    for (int k = 0; k < 12; ++k) cn[k] += static_cast<double>(hp[c * 24 + 8 + k]) / grid;
+  }
+  fprintf(stderr, "[x3 tl P=%d grid %d] us from first CTA start (mean/max): start %.2f/%.2f pdl %.2f/%.2f tma0 %.2f/%.2f "
+          "land0 %.2f/%.2f mma-done %.2f/%.2f epi-read %.2f/%.2f epi-done %.2f/%.2f\n", P, grid, m[0], mx[0], m[1], mx[1],
+          m[2], mx[2], m[3], mx[3], m[4], mx[4], m[5], mx[5], m[6], mx[6]);
+  fprintf(stderr, "[x3 prof] cycles/CTA: mma full-wait %.0f tmem-empty %.0f | epi tmem-full %.0f | producer empty %.0f | "
+          "k-steps %.1f | mma loop incl. waits %.0f (mma issue %.0f, commit %.0f) | epi stores %.0f tile-queue %.0f\n", cn[0],
+          cn[1], cn[2], cn[3], cn[4], cn[5], cn[6], cn[7], cn[8], cn[9]);
+}
+#endif
 
 template <int P, uint32_t kFmt, bool kGen>
 spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStream_t s) {
@@ -418,6 +528,14 @@ spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStre
   const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
   if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
   p.sched_zeroed = false;
+#ifdef SPAMM_PROFILE
+  static unsigned long long* prof_buf = nullptr;
+  if (!prof_buf) {
+    cudaMalloc(&prof_buf, 1024 * 24 * 8);
+    cudaMemcpyToSymbol(g_x3_prof, &prof_buf, sizeof(prof_buf));
+  }
+  cudaMemsetAsync(prof_buf, 0, 1024 * 24 * 8, s);
+#endif
   SPAMM_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, s, mp, static_cast<const int64_t*>(p.mstart),
                             static_cast<const int64_t*>(p.U), static_cast<const uint2*>(p.macro_ent),
                             static_cast<const int32_t*>(p.order), n_tiles, p.GN, C, ldc, p.M, p.N, p.sched,
@@ -427,6 +545,12 @@ spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStre
                             XChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0}));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
+#ifdef SPAMM_PROFILE
+  static unsigned long long hp[1024 * 24];
+  cudaMemcpyAsync(hp, prof_buf, sizeof(hp), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  print_x3_profile(hp, grid, P);
+#endif
   return SPAMM_OK;
 }
 
