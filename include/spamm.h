@@ -75,6 +75,13 @@ typedef enum {
                                          tiles than SMs whose 128 x 128 tiles fit one wave use 128 x 128
                                          macro-tiles (4 x 4 C tiles) so that more SMs work; results agree
                                          up to FP32 rounding order. */
+#define SPAMM_FLAG_STAGED         4u  /* never fuse the skip map into the multiply.  Without it, spamm_run /
+                                         SPAMM_MUL_AUTO on a plan with 128 x 128 macro-tiles (BF16/FP16 of
+                                         the small-problem rule above, or SPAMM_FP32X3) of at most one per
+                                         SM skip the stage-2 launch: each multiply CTA decides its own
+                                         macro-tile's list with the same predicate and writes the same
+                                         skip map (getters unchanged), then multiplies it.  Results are
+                                         identical either way. */
 
 /* spamm_multiply flags */
 #define SPAMM_MUL_AUTO            1u  /* run spamm_norms + spamm_build_skipmap first (spamm_run) */
@@ -157,7 +164,8 @@ spamm_status spamm_build_skipmap(spamm_plan_t p, void* stream);
 spamm_status spamm_multiply(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
                             float* C, int64_t ldc, uint32_t flags, void* stream);
 
-/* All three stages, stream-ordered, no host synchronisation (== multiply with AUTO). */
+/* All three stages, stream-ordered, no host synchronisation (== multiply with AUTO; small
+ * problems fuse stages 2 and 3, SPAMM_FLAG_STAGED). */
 spamm_status spamm_run(spamm_plan_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
                        float* C, int64_t ldc, void* stream);
 

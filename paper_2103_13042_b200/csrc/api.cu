@@ -198,7 +198,8 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   if (!tau_ok(tau)) return fail(SPAMM_E_INVALID, "tau must be finite and >= 0");
   if (prec != SPAMM_FP32 && prec != SPAMM_BF16 && prec != SPAMM_FP16 && prec != SPAMM_FP32X3)
     return fail(SPAMM_E_INVALID, "unknown precision");
-  if (flags & ~(SPAMM_FLAG_TIMING | SPAMM_FLAG_LARGE_TILES)) return fail(SPAMM_E_INVALID, "unknown plan flag");
+  if (flags & ~(SPAMM_FLAG_TIMING | SPAMM_FLAG_LARGE_TILES | SPAMM_FLAG_STAGED))
+    return fail(SPAMM_E_INVALID, "unknown plan flag");
   if (tile != kTile) {
     if (tile == 64 || tile == 128) return fail(SPAMM_E_UNSUPPORTED, "only tile (LoNum) = 32 is implemented");
     return fail(SPAMM_E_INVALID, "tile must be 32, 64 or 128");
@@ -232,6 +233,9 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->GM = (BM + p->MI - 1) / p->MI;
   p->GN = (BN + p->MJ - 1) / p->MJ;
   p->NC = (BK + kChunk - 1) / kChunk;
+  // small problems: one 128 x 128 macro-tile per SM at most -> the skip map is decided inside the
+  // multiply (one launch fewer on spamm_run; the per-tile list work is BK/32 warp steps)
+  p->fused = !(flags & SPAMM_FLAG_STAGED) && (p->x1 || prec == SPAMM_FP32X3) && p->GM * p->GN <= p->num_sms;
   p->device = dev;
   p->row_begin_macro = 0;
   p->row_end_macro = p->GM;
@@ -388,26 +392,49 @@ static spamm_status do_skipmap(Plan& p, cudaStream_t s) {
 }
 
 spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
-                         cudaStream_t s) {
-  if (!p.skipmap_ready) return fail(SPAMM_E_STATE, "spamm_multiply before spamm_build_skipmap");
+                         cudaStream_t s, bool fuse) {
+  if (!fuse && !p.skipmap_ready) return fail(SPAMM_E_STATE, "spamm_multiply before spamm_build_skipmap");
   SPAMM_TRY(check_matrix(A, p.M, p.K, lda, esize_of(p.prec), "A"));
   SPAMM_TRY(check_matrix(B, p.K, p.N, ldb, esize_of(p.prec), "B"));
   if (!p.out_low_only) SPAMM_TRY(check_matrix(C, p.M, p.N, ldc, 4, "C"));
   const bool timing = p.flags & SPAMM_FLAG_TIMING;
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[4], s));
   if (p.prec == SPAMM_FP32X3) {
-    SPAMM_TRY(launch_multiply_x3(p, C, ldc, s));
+    SPAMM_TRY(launch_multiply_x3(p, C, ldc, fuse, s));
   } else if (p.prec == SPAMM_FP32) {
     SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
                                    s));
   } else if (p.x1) {
-    SPAMM_TRY(launch_multiply_x1(p, A, lda, B, ldb, C, ldc, s));
+    SPAMM_TRY(launch_multiply_x1(p, A, lda, B, ldb, C, ldc, fuse, s));
   } else {
     SPAMM_TRY(launch_multiply_dual(p, A, lda, B, ldb, C, ldc, s));
   }
   if (timing) SPAMM_CUDA_TRY(cudaEventRecord(p.ev[5], s));
   p.ev_mul = timing;
   p.last_stream = s;
+  if (fuse) {   // the multiply wrote the complete skip map of the full range (multiply_x3.cu XFuse)
+    if (timing) {   // stage 2 ran inside stage 3: zero-length skip-map interval
+      SPAMM_CUDA_TRY(cudaEventRecord(p.ev[2], s));
+      SPAMM_CUDA_TRY(cudaEventRecord(p.ev[3], s));
+    }
+    p.ev_skip = timing;
+    p.ws_zeroed = false;
+    p.leaf_ready = false;
+    p.skipmap_ready = true;
+  }
+  return SPAMM_OK;
+}
+
+// spamm_run / AUTO: stages 1 and 2 (or stage 1 alone when the multiply decides the skip map)
+static spamm_status do_auto(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t s,
+                            bool* fuse) {
+  SPAMM_TRY(norms_impl(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, true, s));
+  *fuse = p.fused;
+  if (!*fuse) return do_skipmap(p, s);
+  p.skipmap_ready = false;
+  p.range_on_device = false;
+  p.row_begin_macro = 0;
+  p.row_end_macro = p.GM;
   return SPAMM_OK;
 }
 
@@ -433,11 +460,9 @@ spamm_status spamm_multiply(spamm_plan_t h, const void* A, int64_t lda, const vo
   Plan& p = *reinterpret_cast<Plan*>(h);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (flags & ~SPAMM_MUL_AUTO) return fail(SPAMM_E_INVALID, "unknown spamm_multiply flag");
-  if (flags & SPAMM_MUL_AUTO) {
-    SPAMM_TRY(norms_impl(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, true, s));
-    SPAMM_TRY(do_skipmap(p, s));
-  }
-  return do_multiply(p, A, lda, B, ldb, C, ldc, s);
+  bool fuse = false;
+  if (flags & SPAMM_MUL_AUTO) SPAMM_TRY(do_auto(p, A, lda, B, ldb, s, &fuse));
+  return do_multiply(p, A, lda, B, ldb, C, ldc, s, fuse);
 }
 
 spamm_status spamm_multiply_chain(spamm_plan_t h, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
@@ -459,15 +484,13 @@ spamm_status spamm_multiply_chain(spamm_plan_t h, const void* A, int64_t lda, co
   if (p.prec == SPAMM_FP32X3) return fail(SPAMM_E_UNSUPPORTED, "chained outputs: FP32, BF16, FP16 only");
   if ((flags & SPAMM_MUL_OUTPUT_NORMS) && !p.nC)
     SPAMM_TRY(alloc(reinterpret_cast<void**>(&p.nC), sizeof(double) * static_cast<size_t>(p.BM * p.BN)));
-  if (flags & SPAMM_MUL_AUTO) {
-    SPAMM_TRY(norms_impl(p, A, lda, B, ldb, 0, p.BM, 0, p.BN, true, s));
-    SPAMM_TRY(do_skipmap(p, s));
-  }
+  bool fuse = false;
+  if (flags & SPAMM_MUL_AUTO) SPAMM_TRY(do_auto(p, A, lda, B, ldb, s, &fuse));
   p.out_norms = (flags & SPAMM_MUL_OUTPUT_NORMS) != 0;
   p.out_low = C_low;
   p.out_ldl = ldcl;
   p.out_low_only = low_only;
-  const spamm_status st = do_multiply(p, A, lda, B, ldb, low_only ? nullptr : C, ldc, s);
+  const spamm_status st = do_multiply(p, A, lda, B, ldb, low_only ? nullptr : C, ldc, s, fuse);
   p.nc_ready = st == SPAMM_OK && p.out_norms;
   p.out_norms = false;
   p.out_low = nullptr;

@@ -93,6 +93,9 @@ struct Plan {
   void* im2col = nullptr;         // spamm_conv2d_im2col: the K x N im2col matrix (allocated on first use)
   bool b_is_a = false;            // the last spamm_norms saw B == A (planes of A serve both)
   bool x1 = false;                // BF16/FP16 on 128 x 128 macro-tiles (fewer 256 x 256 tiles than SMs)
+  // spamm_run / AUTO on a small problem (128 x 128 macro-tiles, at most one per SM): no skip-map
+  // launch, the multiply's producer warps decide their tiles' lists (multiply_x3.cu XFuse)
+  bool fused = false;
   bool leaf_alloc = false;
 
   // workspace zeroing folded into the previous kernel of a spamm_run / AUTO call: the norm kernel
@@ -199,10 +202,11 @@ spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const fl
                                   int64_t ldc, cudaStream_t s);
 spamm_status launch_multiply_dual(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
-spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s);   // SPAMM_FP32X3
+// SPAMM_FP32X3; fuse = the multiply decides the skip map itself (Plan::fused, spamm_run)
+spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, bool fuse, cudaStream_t s);
 // BF16/FP16 plans with 128 x 128 macro-tiles (small problems, Plan::x1)
 spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
-                                cudaStream_t s);
+                                bool fuse, cudaStream_t s);
 spamm_status launch_transpose_f64(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s);
 
 // 3-D map: dims {inner, mid, outer} with byte strides {mid_stride, outer_stride}.
@@ -219,7 +223,7 @@ spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t e
 spamm_status do_norms_range(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t ar0,
                             int64_t ar1, int64_t bj0, int64_t bj1, cudaStream_t s);
 spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
-                         cudaStream_t s);
+                         cudaStream_t s, bool fuse = false);
 spamm_status check_matrix(const void* ptr, int64_t rows, int64_t cols, int64_t ld, size_t esize, const char* name);
 
 }  // namespace spamm

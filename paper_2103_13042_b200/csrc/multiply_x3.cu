@@ -29,6 +29,7 @@
 #include <cstring>
 
 #include "internal.h"
+#include "skipdecide.cuh"
 #include "sm100.cuh"
 
 namespace spamm {
@@ -106,6 +107,23 @@ struct XChain {       // chained outputs (P = 1): tile norms of the stored C, a 
   int low_only;
 };
 
+// Fused skip map (small problems, spamm_run): the producer warp decides its own macro-tile's
+// (k, keep mask) list from the norm maps -- the same predicate and list format as the skip-map
+// kernel (skipdecide.cuh, skipmap.cu) -- writes it with U, L, row work, totals and the identity
+// claim order for the getters, then streams the kept k-steps.  No skip-map launch, no claim counter.
+struct XFuse {
+  const double* nA;    // [BM][BK]
+  const double* nBt;   // [BN][BK]
+  int64_t BM, BK, BN;
+  double tau;
+  int64_t* U;          // [GM*GN] k-steps per macro-tile (written)
+  int64_t* L;          // [GM*GN] kept pairs per macro-tile (written)
+  uint2* ment;         // [GM*GN][BK] (k, mask) entries (written)
+  int32_t* order;      // [GM*GN] claim order (identity, written)
+  unsigned long long* row_work;   // [BM] (zeroed by the norm kernel)
+  unsigned long long* totals;     // [0] kept pairs [1] k-steps [2] macro-tiles without kept pairs (zeroed)
+};
+
 #ifdef SPAMM_PROFILE
 // per-CTA timeline (globaltimer ns) [0] start [1] after griddepcontrol.wait [2] first TMA issued
 // [3] first stage landed (MMA) [4] MMA done [5] epilogue last TMEM read [6] epilogue done;
@@ -128,13 +146,67 @@ __device__ unsigned long long* g_x3_prof;
 #define X3_FLUSH() do { } while (0)
 #endif
 
-template <int P, uint32_t kFmt, bool kGen>
+// kFuse: the skip map of macro-tile t (4 x 4 C tiles), decided by one warp in ascending k
+// (lane = k) exactly as skip_pyr_kernel's no-pyramid branch decides it; returns U[t].
+__device__ __forceinline__ int64_t fuse_tile_list(const XFuse& fz, int64_t t, int64_t GN, int lane) {
+  const int64_t I = t / GN, J = t % GN;
+  const uint32_t valid = valid_bits<4, 4>(fz.BM, fz.BN, I, J);
+  const uint32_t lt = (1u << lane) - 1u;
+  int64_t mbase = t * fz.BK;
+  uint32_t rw[4] = {0u, 0u, 0u, 0u};
+  for (int64_t k0 = 0; k0 < fz.BK; k0 += 32) {
+    const int64_t k = k0 + lane;
+    uint32_t mask = 0u;
+    if (k < fz.BK && valid != 0u) {
+      ChunkVals<4, 4> cv;
+#pragma unroll
+      for (int li = 0; li < 4; ++li) {
+        const int64_t i = I * 4 + li;
+        cv.a[li] = i < fz.BM ? __ldg(fz.nA + i * fz.BK + k) : 0.0;
+      }
+#pragma unroll
+      for (int lj = 0; lj < 4; ++lj) {
+        const int64_t j = J * 4 + lj;
+        cv.b[lj] = j < fz.BN ? __ldg(fz.nBt + j * fz.BK + k) : 0.0;
+      }
+      mask = chunk_mask<4, 4>(cv, valid, fz.tau);
+    }
+#pragma unroll
+    for (int li = 0; li < 4; ++li) rw[li] += static_cast<uint32_t>(__popc((mask >> (4 * li)) & 0xFu));
+    const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
+    if (mask) fz.ment[mbase + __popc(any & lt)] = make_uint2(static_cast<uint32_t>(k), mask);
+    mbase += __popc(any);
+  }
+  uint32_t lsum = 0;
+#pragma unroll
+  for (int li = 0; li < 4; ++li) {
+    uint32_t v = rw[li];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    lsum += v;
+    if (lane == li && I * 4 + li < fz.BM && v) atomicAdd(fz.row_work + I * 4 + li, static_cast<unsigned long long>(v));
+  }
+  const int64_t u = mbase - t * fz.BK;
+  if (lane == 0) {
+    fz.U[t] = u;
+    fz.L[t] = lsum;
+    fz.order[t] = static_cast<int32_t>(t);
+    if (lsum) atomicAdd(fz.totals, static_cast<unsigned long long>(lsum));
+    if (u) atomicAdd(fz.totals + 1, static_cast<unsigned long long>(u));
+    else atomicAdd(fz.totals + 2, 1ull);
+  }
+  __syncwarp();   // the entries are read back by the whole warp
+  return u;
+}
+
+template <int P, uint32_t kFmt, bool kGen, bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_x3_kernel(const __grid_constant__ X3Maps mp, const int64_t* __restrict__ mstart,
-                        const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
+                        const int64_t* __restrict__ mcount, const uint2* ment,
                         const int32_t* __restrict__ order, int64_t n_tiles, int64_t GN, float* __restrict__ C,
                         int64_t ldc, int64_t M, int64_t N, unsigned int* __restrict__ sched, const Axpby ab,
-                        const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p, const XChain co) {
+                        const int64_t* __restrict__ rng, const int64_t* __restrict__ n_empty_p, const XChain co,
+                        const XFuse fz) {
   constexpr int kStages = XCfg<P>::kStages, kStageBytes = XCfg<P>::kStageBytes;
   constexpr int kStageA = XCfg<P>::kStageA, kBCol = XCfg<P>::kBCol;
   // claims follow the skip map's order (skipmap.cu order_pass); every tile, with or without
@@ -194,15 +266,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     int s = 0, tq_s = 0;
     uint32_t ph = 0, tq_ph = 0;
+    int64_t fz_next = blockIdx.x;   // kFuse: static tile assignment
     auto claim = [&]() -> TileQ {
-      unsigned int idx = 0;
-      if (lane == 0) idx = atomicAdd(sched, 1u);
-      idx = __shfl_sync(0xffffffffu, idx, 0);
       TileQ ti{-1, 0, 0};
-      if (static_cast<int64_t>(idx) < n_tiles) {
-        ti.t = order[idx];
-        ti.e0 = mstart[ti.t];
-        ti.e1 = ti.e0 + mcount[ti.t];
+      if constexpr (kFuse) {
+        if (fz_next < n_tiles) {
+          ti.t = fz_next;
+          ti.e0 = ti.t * fz.BK;
+          ti.e1 = ti.e0 + fuse_tile_list(fz, ti.t, GN, lane);
+        }
+        fz_next += gridDim.x;
+      } else {
+        unsigned int idx = 0;
+        if (lane == 0) idx = atomicAdd(sched, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (static_cast<int64_t>(idx) < n_tiles) {
+          ti.t = order[idx];
+          ti.e0 = mstart[ti.t];
+          ti.e1 = ti.e0 + mcount[ti.t];
+        }
       }
       return ti;
     };
@@ -239,7 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // R2UR waterfall around the TMA instructions)
       for (int64_t eb = cur.e0; eb < cur.e1; eb += 32) {
         const int cnt = static_cast<int>(cur.e1 - eb < 32 ? cur.e1 - eb : 32);
-        const uint2 en_l = lane < cnt ? ment[eb + lane] : make_uint2(0u, 0u);
+        // kFuse: entries this warp just wrote (coherent load, not the read-only path)
+        const uint2 en_l = lane < cnt ? (kFuse ? __ldcg(ment + eb + lane) : __ldg(ment + eb + lane)) : make_uint2(0u, 0u);
         const uint2 run_l = encode_runs4(en_l.y & 0xFFFFu);
         for (int q = 0; q < cnt; ++q) {
           const uint32_t ex = __shfl_sync(0xffffffffu, en_l.x, q);
@@ -518,16 +601,18 @@ static void print_x3_profile(const unsigned long long* hp, int grid, int P) {
 }
 #endif
 
-template <int P, uint32_t kFmt, bool kGen>
+template <int P, uint32_t kFmt, bool kGen, bool kFuse = false>
 spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStream_t s) {
-  auto kern = spamm_mul_x3_kernel<P, kFmt, kGen>;
+  auto kern = spamm_mul_x3_kernel<P, kFmt, kGen, kFuse>;
   constexpr size_t kSmem = XCfg<P>::kSmem;
   SPAMM_SET_SMEM(kern, static_cast<int>(kSmem), p.device);
   const int64_t n_tiles = p.range_on_device ? 0 : (p.row_end_macro - p.row_begin_macro) * p.GN;
   if (!p.range_on_device && n_tiles <= 0) return SPAMM_OK;
   const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
-  if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
-  p.sched_zeroed = false;
+  if (!kFuse) {
+    if (!p.sched_zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s));
+    p.sched_zeroed = false;
+  }
 #ifdef SPAMM_PROFILE
   static unsigned long long* prof_buf = nullptr;
   if (!prof_buf) {
@@ -542,7 +627,10 @@ spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStre
                             Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
                             static_cast<const int64_t*>(p.range_on_device ? p.d_range : nullptr),
                             static_cast<const int64_t*>(p.totals + 2),
-                            XChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0}));
+                            XChain{p.out_norms ? p.nC : nullptr, p.BN, p.out_low, p.out_ldl, p.out_low_only ? 1 : 0},
+                            XFuse{p.nA, p.nBt, p.BM, p.BK, p.BN, p.tau, p.U, p.L, static_cast<uint2*>(p.macro_ent),
+                                  p.order, reinterpret_cast<unsigned long long*>(p.row_work),
+                                  reinterpret_cast<unsigned long long*>(p.totals)}));
   count_launch();
   SPAMM_CUDA_TRY(cudaGetLastError());
 #ifdef SPAMM_PROFILE
@@ -556,7 +644,7 @@ spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStre
 
 }  // namespace
 
-spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) {
+spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, bool fuse, cudaStream_t s) {
   if (!p.planes) return fail(SPAMM_E_STATE, "FP32X3 split planes missing (spamm_norms not run on this plan)");
   if (p.out_norms || p.out_low) return fail(SPAMM_E_UNSUPPORTED, "chained outputs are not implemented for SPAMM_FP32X3");
   const uint16_t* pA = p.planes;
@@ -569,13 +657,13 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, cudaStream_t s) 
                            CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_tmap_3d(&mp.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pB, p.N, p.K, 3, static_cast<uint64_t>(ldb) * 2,
                            static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 3, CU_TENSOR_MAP_SWIZZLE_64B));
-  return launch_x<3, 1, false>(p, mp, C, ldc, s);
+  return fuse ? launch_x<3, 1, false, true>(p, mp, C, ldc, s) : launch_x<3, 1, false>(p, mp, C, ldc, s);
 }
 
 // BF16/FP16 plans with fewer 256 x 256 macro-tiles than SMs: the same kernel on the inputs
 // themselves (one plane, one product per kept pair) over 128 x 128 macro-tiles
 spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
-                                cudaStream_t s) {
+                                bool fuse, cudaStream_t s) {
   const CUtensorMapDataType dt = p.prec == SPAMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   X3Maps mp;
   std::memset(&mp, 0, sizeof(mp));
@@ -584,6 +672,11 @@ spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void*
   SPAMM_TRY(encode_tmap_3d(&mp.b, dt, B, p.N, p.K, 1, static_cast<uint64_t>(ldb) * 2,
                            static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 1, CU_TENSOR_MAP_SWIZZLE_64B));
   const bool gen = p.alpha != 1.0 || p.beta != 0.0 || p.out_norms || p.out_low != nullptr;
+  if (fuse) {
+    if (p.prec == SPAMM_BF16)
+      return gen ? launch_x<1, 1, true, true>(p, mp, C, ldc, s) : launch_x<1, 1, false, true>(p, mp, C, ldc, s);
+    return gen ? launch_x<1, 0, true, true>(p, mp, C, ldc, s) : launch_x<1, 0, false, true>(p, mp, C, ldc, s);
+  }
   if (p.prec == SPAMM_BF16)
     return gen ? launch_x<1, 1, true>(p, mp, C, ldc, s) : launch_x<1, 1, false>(p, mp, C, ldc, s);
   return gen ? launch_x<1, 0, true>(p, mp, C, ldc, s) : launch_x<1, 0, false>(p, mp, C, ldc, s);

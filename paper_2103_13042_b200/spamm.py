@@ -19,7 +19,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "spamm.h")
 
 SPAMM_OK, SPAMM_E_INVALID, SPAMM_E_UNSUPPORTED, SPAMM_E_CUDA, SPAMM_E_NOMEM, SPAMM_E_NCCL, SPAMM_E_STATE = range(7)
 SPAMM_FP32, SPAMM_BF16, SPAMM_FP16, SPAMM_FP32X3 = 0, 1, 2, 3
-SPAMM_FLAG_NONE, SPAMM_FLAG_TIMING, SPAMM_FLAG_LARGE_TILES = 0, 1, 2
+SPAMM_FLAG_NONE, SPAMM_FLAG_TIMING, SPAMM_FLAG_LARGE_TILES, SPAMM_FLAG_STAGED = 0, 1, 2, 4
 SPAMM_MUL_AUTO, SPAMM_MUL_OUTPUT_NORMS, SPAMM_MUL_LOW_ONLY = 1, 2, 4
 SPAMM_MGPU_INPUTS_REPLICATED, SPAMM_MGPU_INPUTS_ON_ROOT, SPAMM_MGPU_GATHER_C = 0, 1, 2
 

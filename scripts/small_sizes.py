@@ -48,17 +48,20 @@ def case(name, A32, B32, tau, prec):
     st = plan.stats()
     eager = timed(lambda: sp.spamm_run(plan.handle, A, B, C))
     st = plan.stats()
-    g = torch.cuda.CUDAGraph()
-    plan2 = sp.Plan(M, N, K, tau, prec)
-    plan2.run(A, B, C)
-    torch.cuda.synchronize()
-    with torch.cuda.graph(g):
-        sp.spamm_run(plan2.handle, A, B, C)
-    graph = timed(g.replay)
+    def graph_time(flags):
+        g = torch.cuda.CUDAGraph()
+        plan2 = sp.Plan(M, N, K, tau, prec, flags=flags)
+        plan2.run(A, B, C)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            sp.spamm_run(plan2.handle, A, B, C)
+        return timed(g.replay)
+    graph = graph_time(0)
+    graph_staged = graph_time(sp.SPAMM_FLAG_STAGED)   # norm -> skip-map -> multiply kernels
     torch.backends.cuda.matmul.allow_tf32 = False
     cub = timed(lambda: torch.matmul(A, B))
     return {"case": name, "precision": prec, "M": M, "N": N, "K": K, "tau": tau, "valid_ratio": st["valid_ratio"],
-            "eager_ms": eager, "graph_ms": graph, "cublas_ms": cub, "speedup_graph_vs_cublas": cub / graph,
+            "eager_ms": eager, "graph_ms": graph, "graph_staged_ms": graph_staged, "cublas_ms": cub, "speedup_graph_vs_cublas": cub / graph,
             "stages_ms": {k: st["ms_" + k] for k in ("norms", "skipmap", "multiply")}}
 
 

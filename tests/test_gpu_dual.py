@@ -20,7 +20,7 @@ SHAPES = [(256, 256, 256), (300, 512, 129), (1000, 768, 600), (64, 256, 4096), (
           (300, 257, 129), (129, 1000, 384)]   # the last two: N % 32 != 0
 
 
-TILES = {"large": 2, "auto": 0}   # plan flags: SPAMM_FLAG_LARGE_TILES / automatic choice
+TILES = {"large": 2, "auto": 0, "staged": 4}   # plan flags: SPAMM_FLAG_LARGE_TILES / automatic / SPAMM_FLAG_STAGED
 
 
 def _tau_at(nA, nB, q):
@@ -29,7 +29,7 @@ def _tau_at(nA, nB, q):
     return float(0.5 * (prods[i] + prods[i + 1]))
 
 
-@pytest.mark.parametrize("tiles", ["large", "auto"])
+@pytest.mark.parametrize("tiles", ["large", "auto", "staged"])
 @pytest.mark.parametrize("prec", ["bf16", "fp16"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("q", [0.0, 0.5, 0.9])
