@@ -1,7 +1,12 @@
 """compute-sanitizer over every product kernel on small ragged problems (scripts/sanitize.py: norms,
 pyramid, skip map, order kernels, BF16 dual multiply, FP32 SIMT, FP32X3, the two-rank emulation,
 per-C-tile list expansion): memcheck, racecheck and synccheck must report no error (SURVEY.md 5,
-sanitizers row).  Each run also checks its results against the float64 oracle."""
+sanitizers row).  Each run also checks its results against the float64 oracle.
+
+Opt-in (SPAMM_RUN_SANITIZERS=1): the shared GPU pool refuses compute-sanitizer (exit code 86,
+"closed on this pool": runs under it have left GPUs needing a reset), so the default GPU suite
+does not launch it; the committed logs under profiles/ (r02e, r02p) are the evidence of the runs
+made before the pool closed it."""
 import os
 import re
 import shutil
@@ -17,6 +22,8 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer(tool):
+    if os.environ.get("SPAMM_RUN_SANITIZERS") != "1":
+        pytest.skip("opt-in: SPAMM_RUN_SANITIZERS=1 (compute-sanitizer is closed on the shared GPU pool)")
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
     out = subprocess.run([SAN, "--tool", tool, "--print-limit", "20", sys.executable,
