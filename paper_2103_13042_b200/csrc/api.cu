@@ -70,6 +70,19 @@ spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void
   return SPAMM_OK;
 }
 
+spamm_status encode_tmap_4d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, const uint64_t dims[4],
+                            const uint64_t stride_bytes[3], const uint32_t box[4], CUtensorMapSwizzle swz) {
+  if (!resolve_encode()) return fail(SPAMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t st[3] = {stride_bytes[0], stride_bytes[1], stride_bytes[2]};
+  cuuint32_t b[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(map, dt, 4, const_cast<void*>(base), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPAMM_E_INVALID, "cuTensorMapEncodeTiled(4d) failed (" + std::to_string(r) + ")");
+  return SPAMM_OK;
+}
+
 // --------------------------------------------------------------- validation
 static size_t esize_of(spamm_precision p) { return f32_inputs(p) ? 4 : 2; }
 

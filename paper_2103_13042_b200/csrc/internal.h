@@ -214,6 +214,10 @@ spamm_status encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dt, const void
                             uint64_t mid, uint64_t outer, uint64_t mid_stride_bytes, uint64_t outer_stride_bytes,
                             uint32_t box0, uint32_t box1, uint32_t box2, CUtensorMapSwizzle swz);
 
+// 4-D map: dims {d0, d1, d2, d3} with byte strides of d1, d2, d3.
+spamm_status encode_tmap_4d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, const uint64_t dims[4],
+                            const uint64_t stride_bytes[3], const uint32_t box[4], CUtensorMapSwizzle swz);
+
 // TMA tensor-map encoder from the driver (resolved once via cudaGetDriverEntryPoint).
 spamm_status encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void* base,
                             uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_inner,

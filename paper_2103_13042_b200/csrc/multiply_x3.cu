@@ -47,7 +47,9 @@ struct XCfg {
   static constexpr int kBCol = P * kBBox;                     // one 32-column tile, P planes
   static constexpr int kStageA = P * kAPlane;
   static constexpr int kStageBytes = kStageA + 4 * kBCol;     // 48 KB (P = 3) / 16 KB (P = 1)
-  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 512 + 1024;
+  // P = 1: a 64 KB staging tile for the TMA-store epilogue (4 boxes of [128 rows x 32] FP32, SWIZZLE_128B)
+  static constexpr int kStageC = P == 1 ? 65536 : 0;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 2048 + kStageC;
 };
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
@@ -97,6 +99,13 @@ struct TileQ {
 
 struct X3Maps {
   CUtensorMap a, b;   // 3-D: {cols, rows, plane}
+  // N % 32 == 0: B viewed as stacked column tiles {32 n, K, plane, N/32}, boxes of 4 / 2 / 1 whole
+  // column tiles with all planes -- the needed column range of a k-step in 1-2 TMAs instead of one
+  // per column tile (the producer's TMA issues bound the small-problem k-step rate)
+  CUtensorMap bs[3];
+  int stacked;
+  CUtensorMap c;      // P = 1, plain epilogue: C (FP32) boxes [128 rows x 32], SWIZZLE_128B, for TMA stores
+  int tstore;
 };
 
 struct XChain {       // chained outputs (P = 1): tile norms of the stored C, a rounded copy, C_low only
@@ -148,7 +157,10 @@ __device__ unsigned long long* g_x3_prof;
 
 // kFuse: the skip map of macro-tile t (4 x 4 C tiles), decided by one warp in ascending k
 // (lane = k) exactly as skip_pyr_kernel's no-pyramid branch decides it; returns U[t].
-__device__ __forceinline__ int64_t fuse_tile_list(const XFuse& fz, int64_t t, int64_t GN, int lane) {
+// With BK <= 32 (one chunk) the lane's entry stays in registers: *reg = (k, mask) of this lane's k,
+// *any = the ballot of non-empty masks (entry q is held by the q-th set lane).
+__device__ __forceinline__ int64_t fuse_tile_list(const XFuse& fz, int64_t t, int64_t GN, int lane, uint2* reg,
+                                                  uint32_t* any_out) {
   const int64_t I = t / GN, J = t % GN;
   const uint32_t valid = valid_bits<4, 4>(fz.BM, fz.BN, I, J);
   const uint32_t lt = (1u << lane) - 1u;
@@ -176,6 +188,8 @@ __device__ __forceinline__ int64_t fuse_tile_list(const XFuse& fz, int64_t t, in
     const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
     if (mask) fz.ment[mbase + __popc(any & lt)] = make_uint2(static_cast<uint32_t>(k), mask);
     mbase += __popc(any);
+    *reg = make_uint2(static_cast<uint32_t>(k), mask);
+    *any_out = any;
   }
   uint32_t lsum = 0;
 #pragma unroll
@@ -195,7 +209,7 @@ __device__ __forceinline__ int64_t fuse_tile_list(const XFuse& fz, int64_t t, in
     if (u) atomicAdd(fz.totals + 1, static_cast<unsigned long long>(u));
     else atomicAdd(fz.totals + 2, 1ull);
   }
-  __syncwarp();   // the entries are read back by the whole warp
+  __syncwarp();   // BK > 32: the entries are read back by the whole warp
   return u;
 }
 
@@ -224,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint4* srun = reinterpret_cast<uint4*>(tq_empty + kTQ);        // [kStages] k-step descriptors
   TileQ* tq = reinterpret_cast<TileQ*>(srun + kStages);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTQ);
+  uint8_t* sC = smem + kStages * kStageBytes + 2048;                // P = 1: C staging (1024-aligned)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) X3_STAMP(0);
@@ -263,17 +278,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       tma_prefetch_desc(&mp.a);
       tma_prefetch_desc(&mp.b);
+      if (mp.stacked)
+        for (int q = 0; q < 3; ++q) tma_prefetch_desc(&mp.bs[q]);
     }
     int s = 0, tq_s = 0;
     uint32_t ph = 0, tq_ph = 0;
     int64_t fz_next = blockIdx.x;   // kFuse: static tile assignment
+    uint2 fz_reg = make_uint2(0u, 0u);
+    uint32_t fz_any = 0u;
     auto claim = [&]() -> TileQ {
       TileQ ti{-1, 0, 0};
       if constexpr (kFuse) {
         if (fz_next < n_tiles) {
           ti.t = fz_next;
           ti.e0 = ti.t * fz.BK;
-          ti.e1 = ti.e0 + fuse_tile_list(fz, ti.t, GN, lane);
+          ti.e1 = ti.e0 + fuse_tile_list(fz, ti.t, GN, lane, &fz_reg, &fz_any);
         }
         fz_next += gridDim.x;
       } else {
@@ -291,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the next tile is claimed once the current one's loads are issued (LPT tail by finish time;
     // claiming at tile start measured 163.5 vs 143.6 us on the 256 x 256 kernel, multiply_dual.cu)
     TileQ cur = claim();
+    if (lane == 0) X3_STAMP(7);   // first tile claimed (kFuse: its list decided)
     for (;;) {
       if (lane == 0) {   // publish the tile (or the end marker) to the epilogue
         mbar_wait(&tq_empty[tq_s], tq_ph ^ 1);
@@ -321,8 +341,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       // R2UR waterfall around the TMA instructions)
       for (int64_t eb = cur.e0; eb < cur.e1; eb += 32) {
         const int cnt = static_cast<int>(cur.e1 - eb < 32 ? cur.e1 - eb : 32);
-        // kFuse: entries this warp just wrote (coherent load, not the read-only path)
-        const uint2 en_l = lane < cnt ? (kFuse ? __ldcg(ment + eb + lane) : __ldg(ment + eb + lane)) : make_uint2(0u, 0u);
+        uint2 en_l = make_uint2(0u, 0u);
+        if (kFuse && fz.BK <= 32) {   // one chunk: entry q from the q-th lane with a kept pair
+          const int src = lane < cnt ? static_cast<int>(__fns(fz_any, 0u, lane + 1)) : 0;
+          en_l.x = __shfl_sync(0xffffffffu, fz_reg.x, src);
+          en_l.y = __shfl_sync(0xffffffffu, fz_reg.y, src);
+          if (lane >= cnt) en_l = make_uint2(0u, 0u);
+        } else if (lane < cnt) {
+          // kFuse: entries this warp just wrote (coherent load, not the read-only path)
+          en_l = kFuse ? __ldcg(ment + eb + lane) : __ldg(ment + eb + lane);
+        }
         const uint2 run_l = encode_runs4(en_l.y & 0xFFFFu);
         for (int q = 0; q < cnt; ++q) {
           const uint32_t ex = __shfl_sync(0xffffffffu, en_l.x, q);
@@ -342,11 +370,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
           if (elect_one()) {
             srun[s] = make_uint4(rw, rn & 0xFu, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
-            mbar_arrive_expect_tx(&full[s], kStageA + kBCol * __popc(cols));
-            tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
+            if (mp.stacked) {   // the column range [c0, c0 + len) covering the needed tiles
+              const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
+              mbar_arrive_expect_tx(&full[s], kStageA + kBCol * len);
+              tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
+              int off = c0;
+              if (len == 4) {
+                tma_load_4d(st + kStageA, &mp.bs[0], &full[s], 0, k0, 0, J * 4);
+              } else {
+                if (len & 2) {
+                  tma_load_4d(st + kStageA + off * kBCol, &mp.bs[1], &full[s], 0, k0, 0, J * 4 + off);
+                  off += 2;
+                }
+                if (len & 1) tma_load_4d(st + kStageA + off * kBCol, &mp.bs[2], &full[s], 0, k0, 0, J * 4 + off);
+              }
+            } else {
+              mbar_arrive_expect_tx(&full[s], kStageA + kBCol * __popc(cols));
+              tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
 #pragma unroll
-            for (int lj = 0; lj < 4; ++lj)
-              if ((cols >> lj) & 1u) tma_load_3d(st + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
+              for (int lj = 0; lj < 4; ++lj)
+                if ((cols >> lj) & 1u) tma_load_3d(st + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
+            }
           }
           if (++s == kStages) {
             s = 0;
@@ -495,6 +539,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 4 && lane == 0) X3_STAMP(5);
       const long long tst0 = X3_CLK();
       const int64_t I = cur.t / GN, J = cur.t % GN;
+      if constexpr (P == 1 && !kGen) {
+        if (mp.tstore) {   // stage the tile in shared memory, 4 TMA stores (clipped at M, N)
+          if (warp == 4 && lane == 0) bulk_wait_group_read<0>();   // the previous tile's stores have read sC
+          named_bar_sync(1, kEpiWarps * 32);
+#pragma unroll
+          for (int lh = 0; lh < 2; ++lh) {
+            const uint32_t ra = static_cast<uint32_t>(q * 32 + 16 * lh + t1);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t b = static_cast<uint32_t>(half * 2 + (i >> 2));
+              const uint32_t ch = ((2u * (i & 3) + (t0 >> 1)) ^ (ra & 7u)) << 4;   // rb = ra + 8: same row phase
+              uint8_t* pa = sC + b * 16384u + ra * 128u + ch + ((t0 & 1) << 3);
+              *reinterpret_cast<float2*>(pa) = make_float2(acc[32 * lh + 4 * i], acc[32 * lh + 4 * i + 1]);
+              *reinterpret_cast<float2*>(pa + 8 * 128) = make_float2(acc[32 * lh + 4 * i + 2], acc[32 * lh + 4 * i + 3]);
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, kEpiWarps * 32);
+          if (warp == 4 && lane == 0) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              tma_store_2d(&mp.c, sC + b * 16384, static_cast<int32_t>(J * 128 + b * 32), static_cast<int32_t>(I * 128));
+            bulk_commit_group();
+          }
+          if (warp == 4 && lane == 0) X3_ADD(16, X3_CLK() - tst0);
+          continue;
+        }
+      }
       double tsum[2] = {0.0, 0.0};   // kGen: sums of squares of the two C tiles of this warp's slice
 #pragma unroll
       for (int lh = 0; lh < 2; ++lh) {
@@ -568,6 +640,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if constexpr (P == 1 && !kGen) {
+    if (mp.tstore && warp == 4 && lane == 0) bulk_wait_group<0>();   // C written before the CTA retires
+  }
   if (warp == 4 && lane == 0) X3_STAMP(6);
   if (lane == 0) X3_FLUSH();
   tc_fence_before();
@@ -583,18 +658,18 @@ namespace {
 static void print_x3_profile(const unsigned long long* hp, int grid, int P) {
   unsigned long long g0 = ~0ull;
   for (int c = 0; c < grid; ++c) g0 = std::min(g0, hp[c * 24]);
-  double m[7] = {0}, mx[7] = {0}, cn[12] = {0};
+  double m[8] = {0}, mx[8] = {0}, cn[12] = {0};
   for (int c = 0; c < grid; ++c) {
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 0; k < 8; ++k) {
       const double v = hp[c * 24 + k] ? (static_cast<double>(hp[c * 24 + k]) - static_cast<double>(g0)) * 1e-3 : 0.0;
       m[k] += v / grid;
       mx[k] = std::max(mx[k], v);
     }
     for (int k = 0; k < 12; ++k) cn[k] += static_cast<double>(hp[c * 24 + 8 + k]) / grid;
   }
-  fprintf(stderr, "[x3 tl P=%d grid %d] us from first CTA start (mean/max): start %.2f/%.2f pdl %.2f/%.2f tma0 %.2f/%.2f "
-          "land0 %.2f/%.2f mma-done %.2f/%.2f epi-read %.2f/%.2f epi-done %.2f/%.2f\n", P, grid, m[0], mx[0], m[1], mx[1],
-          m[2], mx[2], m[3], mx[3], m[4], mx[4], m[5], mx[5], m[6], mx[6]);
+  fprintf(stderr, "[x3 tl P=%d grid %d] us from first CTA start (mean/max): start %.2f/%.2f pdl %.2f/%.2f claim0 %.2f/%.2f "
+          "tma0 %.2f/%.2f land0 %.2f/%.2f mma-done %.2f/%.2f epi-read %.2f/%.2f epi-done %.2f/%.2f\n", P, grid, m[0], mx[0],
+          m[1], mx[1], m[7], mx[7], m[2], mx[2], m[3], mx[3], m[4], mx[4], m[5], mx[5], m[6], mx[6]);
   fprintf(stderr, "[x3 prof] cycles/CTA: mma full-wait %.0f tmem-empty %.0f | epi tmem-full %.0f | producer empty %.0f | "
           "k-steps %.1f | mma loop incl. waits %.0f (mma issue %.0f, commit %.0f) | epi stores %.0f tile-queue %.0f\n", cn[0],
           cn[1], cn[2], cn[3], cn[4], cn[5], cn[6], cn[7], cn[8], cn[9]);
@@ -644,6 +719,23 @@ spamm_status launch_x(Plan& p, const X3Maps& mp, float* C, int64_t ldc, cudaStre
 
 }  // namespace
 
+// B (K x N, ld elements, `planes` planes K*ld apart) as stacked 32-column tiles {32, K, planes, N/32}
+// with boxes of 4, 2 and 1 whole tiles (all planes): smem [tile][plane][32 k][32 n], the per-column
+// layout of a stage.  Only when N % 32 == 0 (a partial last tile cannot be a stacked box).
+static spamm_status encode_stacked(X3Maps& mp, CUtensorMapDataType dt, const void* B, int64_t N, int64_t K, int64_t ld,
+                                   int planes) {
+  mp.stacked = N % 32 == 0 ? 1 : 0;
+  if (!mp.stacked) return SPAMM_OK;
+  const uint64_t dims[4] = {32, static_cast<uint64_t>(K), static_cast<uint64_t>(planes), static_cast<uint64_t>(N / 32)};
+  const uint64_t st[3] = {static_cast<uint64_t>(ld) * 2, static_cast<uint64_t>(K * ld) * 2, 64};
+  const uint32_t nb[3] = {4, 2, 1};
+  for (int q = 0; q < 3; ++q) {
+    const uint32_t box[4] = {32, 32, static_cast<uint32_t>(planes), nb[q]};
+    SPAMM_TRY(encode_tmap_4d(&mp.bs[q], dt, B, dims, st, box, CU_TENSOR_MAP_SWIZZLE_64B));
+  }
+  return SPAMM_OK;
+}
+
 spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, bool fuse, cudaStream_t s) {
   if (!p.planes) return fail(SPAMM_E_STATE, "FP32X3 split planes missing (spamm_norms not run on this plan)");
   if (p.out_norms || p.out_low) return fail(SPAMM_E_UNSUPPORTED, "chained outputs are not implemented for SPAMM_FP32X3");
@@ -657,6 +749,7 @@ spamm_status launch_multiply_x3(Plan& p, float* C, int64_t ldc, bool fuse, cudaS
                            CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_tmap_3d(&mp.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pB, p.N, p.K, 3, static_cast<uint64_t>(ldb) * 2,
                            static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 3, CU_TENSOR_MAP_SWIZZLE_64B));
+  SPAMM_TRY(encode_stacked(mp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pB, p.N, p.K, ldb, 3));
   return fuse ? launch_x<3, 1, false, true>(p, mp, C, ldc, s) : launch_x<3, 1, false>(p, mp, C, ldc, s);
 }
 
@@ -671,7 +764,12 @@ spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void*
                            static_cast<uint64_t>(p.M * lda) * 2, 32, 128, 1, CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_tmap_3d(&mp.b, dt, B, p.N, p.K, 1, static_cast<uint64_t>(ldb) * 2,
                            static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 1, CU_TENSOR_MAP_SWIZZLE_64B));
+  SPAMM_TRY(encode_stacked(mp, dt, B, p.N, p.K, ldb, 1));
   const bool gen = p.alpha != 1.0 || p.beta != 0.0 || p.out_norms || p.out_low != nullptr;
+  mp.tstore = !gen && C != nullptr;
+  if (mp.tstore)
+    SPAMM_TRY(encode_tmap_2d(&mp.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, p.N, p.M, ldc, 32, 128,
+                             CU_TENSOR_MAP_SWIZZLE_128B));
   if (fuse) {
     if (p.prec == SPAMM_BF16)
       return gen ? launch_x<1, 1, true, true>(p, mp, C, ldc, s) : launch_x<1, 1, false, true>(p, mp, C, ldc, s);

@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-2 GPU session ZA: stacked B column-tile boxes (1-2 TMAs per k-step instead of one per column
+# tile) in the 128 x 128 kernel -- parity, small sizes, launch lists, per-CTA timeline.
+OUT=gpurun_out/r02za
+mkdir -p $OUT
+python -m paper_2103_13042_b200.build --force > /dev/null
+timeout 1500 python -m pytest -q -m gpu -x tests/test_gpu_fused.py tests/test_gpu_dual.py tests/test_gpu_parity.py tests/test_gpu_conv.py > $OUT/pytest1.log 2>&1; tail -3 $OUT/pytest1.log
+timeout 600 python scripts/small_sizes.py > $OUT/small_sizes.json 2> $OUT/small_sizes.err; tail -2 $OUT/small_sizes.err
+python - <<'PY'
+import json
+for r in json.load(open("gpurun_out/r02za/small_sizes.json")):
+    print(r["case"], r["precision"], "graph %.4f staged %.4f cublas %.4f x%.2f" % (r["graph_ms"], r["graph_staged_ms"], r["cublas_ms"], r["speedup_graph_vs_cublas"]))
+PY
+for w in n1024:0.9 n1024:0.99; do
+  t=${w/:/_}
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$t.csv python scripts/small_one.py $w > /dev/null 2>&1
+  python scripts/ncu_summary.py --launches $OUT/launches_$t.csv --tag r02za_$t | tail -3
+done
+SPAMM_NVCC_FLAGS=-DSPAMM_PROFILE python -m paper_2103_13042_b200.build --force > /dev/null
+for w in n1024:0.9 n1024:0.99; do timeout 120 python scripts/small_one.py $w 2>&1 | tail -3; done
