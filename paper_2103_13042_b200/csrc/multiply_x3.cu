@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             st2 = true;
           }
 #endif
+          const long long ti0 = X3_CLK();
           if (elect_one()) {
             srun[s] = make_uint4(rw, rn & 0xFu, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
             if (mp.stacked) {   // the column range [c0, c0 + len) covering the needed tiles
@@ -391,6 +392,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int lj = 0; lj < 4; ++lj)
                 if ((cols >> lj) & 1u) tma_load_3d(st + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
             }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            X3_ADD(18, X3_CLK() - ti0);   // TMA issue (elected lane's block)
+            X3_ADD(19, X3_CLK() - tw0);   // whole producer k-step
           }
           if (++s == kStages) {
             s = 0;
@@ -671,8 +677,9 @@ static void print_x3_profile(const unsigned long long* hp, int grid, int P) {
           "tma0 %.2f/%.2f land0 %.2f/%.2f mma-done %.2f/%.2f epi-read %.2f/%.2f epi-done %.2f/%.2f\n", P, grid, m[0], mx[0],
           m[1], mx[1], m[7], mx[7], m[2], mx[2], m[3], mx[3], m[4], mx[4], m[5], mx[5], m[6], mx[6]);
   fprintf(stderr, "[x3 prof] cycles/CTA: mma full-wait %.0f tmem-empty %.0f | epi tmem-full %.0f | producer empty %.0f | "
-          "k-steps %.1f | mma loop incl. waits %.0f (mma issue %.0f, commit %.0f) | epi stores %.0f tile-queue %.0f\n", cn[0],
-          cn[1], cn[2], cn[3], cn[4], cn[5], cn[6], cn[7], cn[8], cn[9]);
+          "k-steps %.1f | mma loop incl. waits %.0f (mma issue %.0f, commit %.0f) | epi stores %.0f tile-queue %.0f | "
+          "producer k-steps %.0f (tma issue %.0f)\n", cn[0], cn[1], cn[2], cn[3], cn[4], cn[5], cn[6], cn[7], cn[8], cn[9],
+          cn[11], cn[10]);
 }
 #endif
 

@@ -16,6 +16,7 @@ struct Cfg {
   uint32_t N;
   uint32_t masked;    // disable lanes of quadrants 1 and 3
   uint32_t ksub;      // MMAs per "k-step" cycling over the K sub-blocks
+  uint32_t same_acc;  // 1: every MMA accumulates into the same TMEM tile (a dependent chain)
 };
 
 __global__ void __launch_bounds__(128, 1) rate_kernel(Cfg c, int R, unsigned long long* out) {
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(Cfg c, int R, unsigned lon
         const uint32_t ks = r % c.ksub;
         const uint64_t ad = smem_desc(a0 + ks * c.a_kstep, c.a_lbo, c.a_sbo, c.a_layout);
         const uint64_t bd = smem_desc(b0 + ks * c.b_kstep, c.b_lbo, c.b_sbo, c.b_layout);
-        umma_f16(tb + (r & 1) * 256, ad, bd, idesc, 1u, 0u, m1, 0u, m3);
+        umma_f16(tb + (c.same_acc ? 0u : (r & 1) * 256), ad, bd, idesc, 1u, 0u, m1, 0u, m3);
       }
       umma_commit(&bar);
       mbar_wait(&bar, 0);
@@ -77,6 +78,9 @@ int main() {
       {"A-K-SW128/ B-MN-SW128 N=256", kLayoutSW128, 16, 1024, 32, kLayoutSW128, 8192, 1024, 2048, 1, 256, 0, 4},
       {"A-K-SW128/ B-K-SW128  N=128", kLayoutSW128, 16, 1024, 32, kLayoutSW128, 16, 1024, 32, 0, 128, 0, 4},
       {"A-K-SW128/ B-K-SW128  N=64", kLayoutSW128, 16, 1024, 32, kLayoutSW128, 16, 1024, 32, 0, 64, 0, 4},
+      {"A-K-SW64 / B-MN-SW64  N=256 same acc", kLayoutSW64, 16, 512, 32, kLayoutSW64, 2048, 512, 1024, 1, 256, 0, 2, 1},
+      {"A-K-SW64 / B-MN-SW64  N=128 same acc", kLayoutSW64, 16, 512, 32, kLayoutSW64, 2048, 512, 1024, 1, 128, 0, 2, 1},
+      {"A-K-SW64 / B-MN-SW64  N=128 masked same acc", kLayoutSW64, 16, 512, 32, kLayoutSW64, 2048, 512, 1024, 1, 128, 1, 2, 1},
   };
   for (auto& c : cfgs) {
     for (int grid : {1, 148}) {
