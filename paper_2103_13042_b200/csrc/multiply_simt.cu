@@ -44,7 +44,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           int64_t GN, const Axpby ab, double* __restrict__ nC, int64_t ldn, int64_t BM, int64_t BN) {
   if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU range decided on the device
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned base derived from smem_raw by an offset (not an integer round trip), so the compiler
+  // keeps the shared address space: LDS/STS instead of generic LD/ST for the operand and sum reads
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   float* sA = reinterpret_cast<float*>(smem);
   float* sB = sA + kStages * kAFloats;
   float4* sAcc = reinterpret_cast<float4*>(smem + static_cast<size_t>(kStages) * kStageBytes);
@@ -93,7 +95,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // -------------------------------------------------------- compute warps
   const int li = warp >> 2, lj = warp & 3, bit = li * 4 + lj;
-  const int g = lane & 7, cg = lane >> 3;
+  // lane -> (row g, column group cg) = (lane / 4, lane % 4): the epilogue's row segments are 128-byte
+  // contiguous.  Measured at N = 16384 (profiles/r02zf_*): with LDS (see smem above) 6.26 ms vs 6.47 ms
+  // for (lane % 8, lane / 8) and 6.90 ms with generic loads; the shared pipe stays the limiter (A loads
+  // 2, B loads 4 wavefronts per LDS.128 here; 4 and 2 with the other mapping)
+  const int g = lane >> 2, cg = lane & 3;
   int s = 0;
   uint32_t ph = 0;
   for (int64_t r = 0;; ++r) {
