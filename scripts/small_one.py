@@ -13,8 +13,9 @@ import synth  # noqa: E402
 from paper_2103_13042_b200 import spamm as sp  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "n1024"
-if which.startswith("n1024"):   # n1024 (lambda = 0.9) or n1024:<lambda>
-    A32 = B32 = synth.decay_matrix(1024, "exp", float(which.split(":")[1]) if ":" in which else 0.9)
+if which.startswith("n"):   # n1024 (lambda = 0.9), n<N>:<lambda>
+    n = int(which.split(":")[0][1:])
+    A32 = B32 = synth.decay_matrix(n, "exp", float(which.split(":")[1]) if ":" in which else 0.9)
     tau = 1e-4
 else:
     A32, B32 = synth.im2col_gemm(which)
