@@ -1,9 +1,9 @@
-// multiply_dual.cu -- stage 3, tensor-core path on 256 x 256 macro-tiles with two MMA issuers
-// (SPAMM_UMMA_VARIANT=5).  Same product as multiply_umma.cu:
+// multiply_dual.cu -- stage 3, BF16/FP16 tensor-core path on 256 x 256 macro-tiles with two MMA
+// issuers:
 //   C[i,j] = sum_{kept k, ascending} A[i,k] * B[k,j]   (Alg. 2/3),
 // BF16/FP16 inputs, FP32 accumulation in TMEM (PAPER.md:187's FP32 accumulator fragment).
 //
-// Why a second design: at the bench point the 128 x 256 kernel moves 1.50 GB of operand tiles
+// Why 256 x 256 (round 1; the 128 x 256 kernel has since been removed): at the bench point it moved 1.50 GB of operand tiles
 // L2 -> SMEM per call (24 KB per 32-deep k-step for 2 MMAs of N = 256); ncu shows the SM <-> L2
 // request path busy 68 % of the kernel, i.e. the kernel is fed at ~12 TB/s (the chip's TMA
 // throughput, B300_MICROARCH.md "TMA chip-throughput").  A 256 x 256 macro-tile (8 x 8 C tiles)
@@ -17,11 +17,12 @@
 //   warps 1, 2 (one elected lane): MMA issuer of half h = warp - 1 (C-tile rows 4h .. 4h+3): per run of
 //            adjacent C-tile columns with the same row pattern, 2 x tcgen05.mma M=128 N=32*run
 //            K=16 whose disable-output-lane mask switches off the skipped C-tile rows -- the
-//            4 x 8 run encoding of multiply_umma.cu, one per half.  Two independent issuers
+//            4 x 8 run encoding of skipmap.cu (encode_runs), one per half.  Two independent issuers
 //            on one tensor pipe hide each other's per-k-step bookkeeping (scripts/probe_queue2);
 //   warps 4-11: epilogue, warp w drains rows 128h + 32q .. +32 (h = (w-4)/4, q = w%4, its
-//            TMEM lane quadrant) x 256 columns; while waiting they zero-fill the macro-tiles
-//            without kept pairs (the LPT tail) with bulk stores of a 1 KB zero buffer.
+//            TMEM lane quadrant) x 256 columns; they zero-fill the macro-tiles without kept
+//            pairs (the LPT tail) with evict-first bulk stores of a 1 KB zero buffer -- after
+//            their last tile, and while waiting for an accumulator when empty tiles dominate.
 // Skip map: 8 x 8 macro-tiles; macro_run holds two uint4 per k-step (half 0, half 1), each the
 // 4 x 8 encoding of skipmap.cu encode_runs, at 2 * (t * BK + e) + h.
 #include <cuda.h>
@@ -155,12 +156,21 @@ __global__ void __launch_bounds__(kDThreads, 1)
   const int64_t n_empty = n_empty_p ? *n_empty_p : 0;
   const int64_t n_work = n_tiles - n_empty;
 
-  // Zero-fill of the macro-tiles without kept pairs (the LPT tail of `order`), done LAST: an
-  // epilogue warp whose CTA has no more tiles claims 32-row units (32 KB of C) from a global
-  // counter, so the CTAs that finish their MMA work early absorb it (the slowest one takes
-  // none).  Done greedily at the start instead, the 141 MB of zero writes at the bench point
-  // compete with the operand loads' first DRAM touches (multiply 165 vs 152 us without them).
+  // Zero-fill of the macro-tiles without kept pairs (the LPT tail of `order`): an epilogue warp
+  // claims 32-row units (32 KB of C) from a global counter -- while its accumulator half is not
+  // ready (interleaved, below) and after its CTA's last tile -- so the CTAs that finish their MMA
+  // work early absorb it (the slowest one takes none).  Done greedily at the start instead, the
+  // 141 MB of zero writes at N = 8192 compete with the operand loads' first DRAM touches
+  // (multiply 165 vs 152 us without them).
   const int64_t n_units = n_empty * 8;
+#ifndef SPAMM_ZF_INTERLEAVE
+#define SPAMM_ZF_INTERLEAVE 1
+#endif
+  const uint64_t zf_pol = l2_policy_evict_first();   // zeros are never re-read: keep the operands in L2
+  // Interleaved with the accumulator waits only when the empty tiles dominate (measured, ms of the
+  // multiply, zero-fill last -> interleaved: N = 16384 lambda 0.99 tau 1e-6 0.343 -> 0.318 (3.5 empty
+  // tiles per working tile), N = 8192 0.135 -> 0.141 (1.2), N = 65536 58.8 -> 59.0; scripts/gpu_r02zi.sh)
+  const bool zf_inter = SPAMM_ZF_INTERLEAVE && n_empty >= 2 * n_work;
   auto zero_unit = [&]() -> bool {
     unsigned int u32 = 0;
     if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
@@ -171,7 +181,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
     const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
     const uint32_t bytes = static_cast<uint32_t>(ncol * 4) & ~15u;
     if (row < M) {   // one row per lane: 32 bulk (TMA-engine) stores of the 1 KB zero buffer
-      if (bytes) bulk_store_1d(C + row * ldc + c0, sZero, bytes);
+      if (bytes) bulk_store_1d_hint(C + row * ldc + c0, sZero, bytes, zf_pol);
       for (int64_t cc = bytes / 4; cc < ncol; ++cc) C[row * ldc + c0 + cc] = 0.f;
     }
     bulk_commit_group();
@@ -553,6 +563,14 @@ __global__ void __launch_bounds__(kDThreads, 1)
       if (cur.t < 0) break;
       const int64_t I = cur.t / GN, J = cur.t % GN;
       const unsigned long long tw = prof ? clock64() : 0;
+      if (zf_inter && !kGen) {
+        // while this half's accumulator is not ready, zero-fill units of the macro-tiles without
+        // kept pairs (evict-first bulk stores); the phase is monotone, so any lane seeing it
+        // complete means complete for the warp (zero_unit is warp-collective)
+        while (!__any_sync(0xffffffffu, mbar_try_wait(&tfull[h], par))) {
+          if (!zero_unit()) break;
+        }
+      }
       mbar_wait(&tfull[h], par);
       par ^= 1;
       if (prof && warp == 4 && lane == 0) prof[blockIdx.x * 16 + 12] += clock64() - tw;
