@@ -5,14 +5,14 @@
 //
 // B200 design.  Persistent CTAs (one per SM) walk an LPT-ordered list of 128x128
 // macro-tiles (4x4 C tiles).  For every k in the macro-tile's union list a TMA
-// producer warp stages A[128 x 32] (SWIZZLE_128B) and B[32 x 128] in a 5-deep
+// producer warp stages A[128 x 32] (SWIZZLE_128B) and B[32 x 128] in a 6-deep
 // shared-memory ring guarded by mbarriers (replacing the paper's two half-block
-// double buffer).  Sixteen compute warps each own one 32x32 C tile;
-// the tile's keep bit for this k is warp-uniform, so a skipped pair costs a warp
-// nothing but the barrier.  Each lane computes a 4x8 register micro-tile.
-// Two-level accumulation: a 32-term register partial per kept k-tile is added into a
-// running sum kept in shared memory, which keeps N=65536
-// within 1e-5 and leaves registers for 17 warps (4 SMSPs x <=5 warps x 96 regs).
+// double buffer).  Eight compute warps each own a pair of adjacent 32x32
+// C tiles; the pair's keep bits for this k are warp-uniform, so a skipped pair costs a warp
+// nothing but the barrier.  Each lane computes an 8x8 register micro-tile (4 columns in
+// each tile of the pair).  Two-level accumulation: a 32-term register partial per kept k-tile
+// is added into a running sum, also in registers, which keeps
+// N=65536 within 1e-5.
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -21,14 +21,19 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kStages = 5;
-constexpr int kComputeWarps = 16;
-constexpr int kThreads = (kComputeWarps + 1) * 32;
+#ifndef SPAMM_SIMT_QUNROLL
+#define SPAMM_SIMT_QUNROLL 2
+#endif
+constexpr int kQUnroll = SPAMM_SIMT_QUNROLL;   // k-slice loop unroll (experiments: -DSPAMM_SIMT_QUNROLL)
+constexpr int kStages = 6;
+constexpr int kComputeWarps = 8;   // one C-tile pair (32 x 64) each
+// warpgroup 0: the TMA producer (warp 0; its registers handed to the compute warps with setmaxnreg),
+// warpgroups 1-2: the 8 compute warps (232 registers each: 128 accumulators of the 8 x 8 micro-tile)
+constexpr int kThreads = (4 + kComputeWarps) * 32;
 constexpr int kAFloats = 128 * 32;
 constexpr int kBFloats = 32 * 128;
 constexpr int kStageBytes = (kAFloats + kBFloats) * 4;
-constexpr int kAccBytes = kComputeWarps * 32 * 32 * 4;   // running sums, [warp][8 float4][32 lanes]
-constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + kAccBytes + 256;
+constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 256;
 
 __device__ __forceinline__ int64_t snake(int64_t r, int G, int b) { return r * G + ((r & 1) ? (G - 1 - b) : b); }
 
@@ -49,8 +54,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   float* sA = reinterpret_cast<float*>(smem);
   float* sB = sA + kStages * kAFloats;
-  float4* sAcc = reinterpret_cast<float4*>(smem + static_cast<size_t>(kStages) * kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(kStages) * kStageBytes + kAccBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(kStages) * kStageBytes);
   uint64_t* empty = full + kStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -64,9 +68,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   const int G = gridDim.x, b = blockIdx.x;
 
-  if (warp == kComputeWarps) {
-    // ------------------------------------------------------ TMA producer
-    if (lane == 0) {
+  if (warp < 4) {
+    // ------------------------------------------------------ TMA producer (warpgroup 0)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    if (warp == 0 && lane == 0) {
       tma_prefetch_desc(&tA);
       tma_prefetch_desc(&tB);
       int s = 0;
@@ -93,13 +98,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
 
-  // -------------------------------------------------------- compute warps
-  const int li = warp >> 2, lj = warp & 3, bit = li * 4 + lj;
-  // lane -> (row g, column group cg) = (lane / 4, lane % 4): the epilogue's row segments are 128-byte
-  // contiguous.  Measured at N = 16384 (profiles/r02zf_*): with LDS (see smem above) 6.26 ms vs 6.47 ms
-  // for (lane % 8, lane / 8) and 6.90 ms with generic loads; the shared pipe stays the limiter (A loads
-  // 2, B loads 4 wavefronts per LDS.128 here; 4 and 2 with the other mapping)
-  const int g = lane >> 2, cg = lane & 3;
+  // -------------------------------------------------------- compute warps (warpgroups 1-2)
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+  // Warp w owns the C-tile pair (li, 2 jp), (li, 2 jp + 1), li = w / 2, jp = w % 2: 32 rows x 64
+  // columns.  Lane (g, cg) = (lane / 8, lane % 8) holds rows g + 4 rr (rr < 8) and, in each tile
+  // of the pair, the 4 columns 4 cg .. 4 cg + 3: an 8 x 8 register micro-tile.  Per 4-deep k slice
+  // a warp reads 8 A and 8 B float4 from shared memory for 256 FFMA (the 4 x 8 one-tile-per-warp
+  // layout read 12 for 128 and was bound by the shared pipe).  A k-step is computed when
+  // either tile of the pair is kept (adjacent tiles are kept together: 1-3 % of the pair-steps of
+  // the N = 16384 lambda = 0.99 sweep keep exactly one) and each tile's partial is added only if
+  // kept.  Two-level accumulation in registers: the 32-term partial of a kept k-tile is added into
+  // the running sum (first kept k: the partial itself), in ascending k.
+  const int cw = warp - 4;
+  const int li = cw >> 1, jp = cw & 1;
+  const int bit_a = li * 4 + 2 * jp, bit_b = bit_a + 1;
+  const int g = lane >> 3, cg = lane & 7;
   int s = 0;
   uint32_t ph = 0;
   for (int64_t r = 0;; ++r) {
@@ -107,33 +120,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (idx >= n_tiles) break;
     const int64_t t = order[idx];
     const int64_t I = t / GN, J = t % GN;
-    float4* acc = sAcc + warp * 8 * 32 + lane;   // acc[j4 * 32]: outputs 4*j4 .. 4*j4+3 of this lane
-    bool first = true;
+    float run[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) run[i][j] = 0.f;
+    bool first_a = true, first_b = true;
     const int64_t e0 = mstart[t], e1 = e0 + mcount[t];
     for (int64_t e = e0; e < e1; ++e) {
       mbar_wait(&full[s], ph);
       const uint32_t mask = __ldg(&ment[e].y);   // the k-step's keep bits (read-only, L1-resident)
-      if ((mask >> bit) & 1u) {
+      const bool ka = (mask >> bit_a) & 1u, kb = (mask >> bit_b) & 1u;
+      if (ka || kb) {
         const float* a_base = sA + s * kAFloats + (li * 32 + g) * 32;
-        const float* b_base = sB + s * kBFloats + lj * 32 + cg * 8;
-        float part[4][8];
+        const float* b_base = sB + s * kBFloats + jp * 64 + cg * 4;
+        float part[8][8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
           for (int j = 0; j < 8; ++j) part[i][j] = 0.f;
+#pragma unroll kQUnroll
+        for (int q = 0; q < 8; ++q) {   // partial unroll: the fully unrolled body (2048 FFMA) missed the i-cache
+          float4 a4[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 a4[4];
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr)
-            a4[rr] = *reinterpret_cast<const float4*>(a_base + rr * 8 * 32 + ((q ^ g) << 2));
+          for (int rr = 0; rr < 8; ++rr)   // row li*32 + g + 4 rr: its SWIZZLE_128B chunk is q ^ (row & 7)
+            a4[rr] = *reinterpret_cast<const float4*>(a_base + rr * 4 * 32 + ((q ^ (g + 4 * (rr & 1))) << 2));
 #pragma unroll
           for (int kq = 0; kq < 4; ++kq) {
             const float* brow = b_base + (q * 4 + kq) * 128;
-            const float4 b0 = *reinterpret_cast<const float4*>(brow);
-            const float4 b1 = *reinterpret_cast<const float4*>(brow + 4);
+            const float4 b0 = *reinterpret_cast<const float4*>(brow);        // tile 2 jp
+            const float4 b1 = *reinterpret_cast<const float4*>(brow + 32);   // tile 2 jp + 1
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
+            for (int rr = 0; rr < 8; ++rr) {
               const float av = comp(a4[rr], kq);
               part[rr][0] = fmaf(av, b0.x, part[rr][0]);
               part[rr][1] = fmaf(av, b0.y, part[rr][1]);
@@ -146,21 +164,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // second level: running sum += 32-term partial
+        // second level: running sum += 32-term partial, for each kept tile of the pair
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const int rr = j4 >> 1, c0 = (j4 & 1) * 4;
-          float4 v = make_float4(part[rr][c0], part[rr][c0 + 1], part[rr][c0 + 2], part[rr][c0 + 3]);
-          if (!first) {
-            const float4 o = acc[j4 * 32];
-            v.x += o.x;
-            v.y += o.y;
-            v.z += o.z;
-            v.w += o.w;
+        for (int rr = 0; rr < 8; ++rr)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (ka) run[rr][j] = first_a ? part[rr][j] : run[rr][j] + part[rr][j];
+            if (kb) run[rr][4 + j] = first_b ? part[rr][4 + j] : run[rr][4 + j] + part[rr][4 + j];
           }
-          acc[j4 * 32] = v;
-        }
-        first = false;
+        first_a = first_a && !ka;
+        first_b = first_b && !kb;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -169,41 +182,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         ph ^= 1;
       }
     }
-    // epilogue: rows I*128 + li*32 + g + 8*rr, cols J*128 + lj*32 + cg*8 .. +7
-    const int64_t n0 = J * 128 + lj * 32 + cg * 8;
-    double tsq = 0.0;   // chained SpAMM: this lane's share of the tile's sum of squares
+    // epilogue: rows I*128 + li*32 + g + 4 rr; columns J*128 + jp*64 + 32 h + 4 cg .. + 3 for tile
+    // 2 jp + h -- the 8 lanes of a row write 128 contiguous bytes per tile
+    double tsq[2] = {0.0, 0.0};   // chained SpAMM: this lane's share of each tile's sum of squares
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const int64_t m = I * 128 + li * 32 + g + 8 * rr;
-      const float4 v0 = first ? make_float4(0.f, 0.f, 0.f, 0.f) : acc[(2 * rr) * 32];
-      const float4 v1 = first ? make_float4(0.f, 0.f, 0.f, 0.f) : acc[(2 * rr + 1) * 32];
+    for (int rr = 0; rr < 8; ++rr) {
+      const int64_t m = I * 128 + li * 32 + g + 4 * rr;
       if (m >= M) continue;
-      float* crow = C + m * ldc + n0;
-      if (n0 + 8 <= N) {
-        const float4 w0 = axpby4(ab, v0, crow), w1 = axpby4(ab, v1, crow + 4);
-        __stcs(reinterpret_cast<float4*>(crow), w0);
-        __stcs(reinterpret_cast<float4*>(crow + 4), w1);
-        if (nC != nullptr) {
-          const float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-          for (int j = 0; j < 8; ++j) tsq += static_cast<double>(ww[j]) * static_cast<double>(ww[j]);
+      for (int h = 0; h < 2; ++h) {
+        const int64_t n0 = J * 128 + jp * 64 + 32 * h + 4 * cg;
+        const float4 v = make_float4(run[rr][4 * h], run[rr][4 * h + 1], run[rr][4 * h + 2], run[rr][4 * h + 3]);
+        float* crow = C + m * ldc + n0;
+        if (n0 + 4 <= N) {
+          const float4 w = axpby4(ab, v, crow);
+          __stcs(reinterpret_cast<float4*>(crow), w);
+          if (nC != nullptr)
+            tsq[h] += static_cast<double>(w.x) * static_cast<double>(w.x) + static_cast<double>(w.y) * static_cast<double>(w.y) +
+                      static_cast<double>(w.z) * static_cast<double>(w.z) + static_cast<double>(w.w) * static_cast<double>(w.w);
+        } else {
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (n0 + j < N) {
+              const float w = axpby1(ab, vv[j], crow + j);
+              crow[j] = w;
+              tsq[h] += static_cast<double>(w) * static_cast<double>(w);
+            }
         }
-      } else {
-        const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (n0 + j < N) {
-            const float w = axpby1(ab, vv[j], crow + j);
-            crow[j] = w;
-            tsq += static_cast<double>(w) * static_cast<double>(w);
-          }
       }
     }
     if (nC != nullptr) {
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) tsq += __shfl_xor_sync(0xffffffffu, tsq, o);
-      const int64_t ti = I * 4 + li, tj = J * 4 + lj;
-      if (lane == 0 && ti < BM && tj < BN) nC[ti * ldn + tj] = sqrt(tsq);
+      for (int h = 0; h < 2; ++h) {
+        double x = tsq[h];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        const int64_t ti = I * 4 + li, tj = J * 4 + 2 * jp + h;
+        if (lane == 0 && ti < BM && tj < BN) nC[ti * ldn + tj] = sqrt(x);
+      }
     }
   }
 }
