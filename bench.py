@@ -147,6 +147,30 @@ def _table(N, lam, prec):
     return t
 
 
+def _table_alg(N, prec):
+    """The paper's algebraic-decay dataset a_ij = 0.1/(|i-j|^0.1 + 1) (configs[2])."""
+    t = synth.decay_table("alg", N, 0.1, c=0.1).astype(np.float32)
+    if prec == "bf16":
+        t = synth.round_to_bf16(t)
+    elif prec == "fp16":
+        t = synth.round_to_fp16(t)
+    return t
+
+
+def _table1_taus(N):
+    """(target valid ratio, tau) printed in Table 1 for this N, from the golden file."""
+    path = os.path.join(ROOT, "tests", "golden", "table1_tau.csv")
+    out = []
+    with open(path) as f:
+        for line in f:
+            if line.startswith("#") or line.startswith("N,"):
+                continue
+            n, target, tau = line.strip().split(",")
+            if int(n) == N:
+                out.append((float(target), float(tau)))
+    return out
+
+
 def oracle_sample(N, lam, prec, tau, rows=8, cols=96, seed=0):
     """The float64 oracle (as it stands) on a bounded sample of the workload: the C tiles of
     `rows` middle tile rows x `cols` random tile columns, i.e. oracle.spamm(A[rows, :], B[:, cols])
@@ -448,7 +472,7 @@ def _e2e(sp, plan, A, C, prec, N, args, world, rank, comm):
                     "step; pipelined over upload / compute / download streams with two device buffer sets"}
 
 
-def _sweep_one(sp, A, N, prec, taus, flush, stream, reps=3):
+def _sweep_one(sp, A, N, prec, taus, flush, stream, reps=3, workload=None):
     out = []
     C = torch.empty((N, N), dtype=torch.float32, device=A.device)
     with sp.Plan(N, N, N, taus[0], prec, flags=sp.SPAMM_FLAG_TIMING) as plan:
@@ -474,7 +498,7 @@ def _sweep_one(sp, A, N, prec, taus, flush, stream, reps=3):
             ms_mul = statistics.median(stages["multiply"])
             roof, _, _ = _roofline(s, prec, ms_mul, statistics.median(stages["norms"]), N, _peaks(),
                                    4 if prec in ("fp32", "fp32x3") else 2, None)
-            out.append({"N": N, "precision": prec, "tau": tau, "ms": ms, "valid_ratio": s["valid_ratio"],
+            out.append({"N": N, "workload": workload, "precision": prec, "tau": tau, "ms": ms, "valid_ratio": s["valid_ratio"],
                         "kept": s["kept"], "stages_ms": {k: statistics.median(v) for k, v in stages.items()},
                         "tflops_dense_equiv": 2.0 * N ** 3 / (ms / 1e3) / 1e12,
                         "tflops_kept": 2.0 * TILE ** 3 * s["kept"] / (ms / 1e3) / 1e12,
@@ -515,18 +539,35 @@ def _sweeps(sp, A, N, prec, args, flush, stream, dev):
     """tau sweeps on configs[4] (the headline size), the north_star's N = 16384 exponential-decay
     target and configs[1] N = 8192, with cuBLAS dense GEMM on the same box and inputs."""
     res, cublas = [], {}
-    res += _sweep_one(sp, A, N, prec, TAU5, flush, stream)
+    res += _sweep_one(sp, A, N, prec, TAU5, flush, stream, workload=f"configs[4] lambda={args.lam}")
     cublas[f"N={N}"] = _cublas(A, flush, stream, 3)
     small_flush = _flusher(dev)
     for n2, lam2, precs, taus in ((16384, 0.99, ("bf16", "fp32x3", "fp32"), TAU5), (8192, 0.99, ("bf16", "fp32x3"), TAU9)):
         for p2 in precs:
             A2 = synth.toeplitz_device(_table(n2, lam2, p2), n2, DT[p2], device=dev)
-            res += _sweep_one(sp, A2, n2, p2, taus, small_flush, stream)
+            wl = "north_star target, lambda=0.99" if n2 == 16384 else "configs[1], lambda=0.99"
+            res += _sweep_one(sp, A2, n2, p2, taus, small_flush, stream, workload=wl)
             if p2 != "fp32x3":
                 cublas[f"N={n2} {p2}"] = _cublas(A2, small_flush, stream, 3)
             if p2 == "bf16" and n2 == 16384:
                 res.append(_low_only_point(sp, A2, n2, 1e-6, small_flush, stream))
             del A2
+    # configs[2]: the paper's own Table 2 workload -- N = 16384 algebraic decay at the six Table 1
+    # tau (valid ratio 30 ... 5 %), next to cuBLAS on the same inputs (PAPER.md:257-293)
+    alg = []
+    t1 = _table1_taus(16384)
+    for p2 in ("bf16", "fp32x3", "fp32"):
+        A2 = synth.toeplitz_device(_table_alg(16384, p2), 16384, DT[p2], device=dev)
+        pts = _sweep_one(sp, A2, 16384, p2, [tau for _, tau in t1], small_flush, stream, reps=2,
+                         workload="configs[2] algebraic decay 0.1/(d^0.1+1), Table 1 tau")
+        for r, (target, _) in zip(pts, t1):
+            r["table1_target_valid_ratio"] = target
+        if p2 != "fp32x3":
+            cublas[f"N=16384 alg {p2}"] = _cublas(A2, small_flush, stream, 2)
+        alg += pts
+        del A2
+    for r in alg:
+        r["speedup_vs_cublas"] = cublas[f"N=16384 alg {'fp32' if r['precision'] == 'fp32x3' else r['precision']}"]["ms"] / r["ms"]
     for r in res:
         if "output" in r:
             r["speedup_vs_cublas"] = cublas[f"N={r['N']} bf16"]["ms"] / r["ms"]
@@ -534,10 +575,12 @@ def _sweeps(sp, A, N, prec, args, flush, stream, dev):
         key = f"N={r['N']}" if r["N"] == N else f"N={r['N']} {'fp32' if r['precision'] == 'fp32x3' else r['precision']}"
         if key in cublas and (r["N"] != N or r["precision"] == prec):
             r["speedup_vs_cublas"] = cublas[key]["ms"] / r["ms"]
+    res += alg
     torch.cuda.empty_cache()
     return {"points": res, "cublas": cublas,
             "workloads": {f"N={N}": f"configs[4] lambda={args.lam}", "N=16384": "north_star target, lambda=0.99",
-                          "N=8192": "configs[1], lambda=0.99"}}
+                          "N=8192": "configs[1], lambda=0.99",
+                          "N=16384 alg": "configs[2], the paper's algebraic decay (PAPER.md:257) at the Table 1 tau"}}
 
 
 def _barrier(world):
