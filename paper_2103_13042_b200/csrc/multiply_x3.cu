@@ -43,10 +43,14 @@ constexpr int kBBox = 32 * 32 * 2;                 // 2 KB
 // problems (fewer 256 x 256 macro-tiles than SMs: 128 x 128 tiles keep more SMs busy)
 template <int P>
 struct XCfg {
-  static constexpr int kStages = P == 3 ? 4 : 8;
+  // P = 1: a stage carries up to two k-steps (two 16 KB slots): the per-stage round trip (full /
+  // empty barriers, descriptor, commit) was ~700 cycles for 132 cycles of MMA per k-step
+  static constexpr int kPack = P == 3 ? 1 : 2;
+  static constexpr int kStages = P == 3 ? 4 : 4;
   static constexpr int kBCol = P * kBBox;                     // one 32-column tile, P planes
   static constexpr int kStageA = P * kAPlane;
-  static constexpr int kStageBytes = kStageA + 4 * kBCol;     // 48 KB (P = 3) / 16 KB (P = 1)
+  static constexpr int kSlotBytes = kStageA + 4 * kBCol;      // one k-step: 48 KB (P = 3) / 16 KB (P = 1)
+  static constexpr int kStageBytes = kPack * kSlotBytes;
   // P = 1: a 64 KB staging tile for the TMA-store epilogue (4 boxes of [128 rows x 32] FP32, SWIZZLE_128B)
   static constexpr int kStageC = P == 1 ? 65536 : 0;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 2048 + kStageC;
@@ -223,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const XFuse fz) {
   constexpr int kStages = XCfg<P>::kStages, kStageBytes = XCfg<P>::kStageBytes;
   constexpr int kStageA = XCfg<P>::kStageA, kBCol = XCfg<P>::kBCol;
+  constexpr int kPack = XCfg<P>::kPack, kSlotBytes = XCfg<P>::kSlotBytes;
   // claims follow the skip map's order (skipmap.cu order_pass); every tile, with or without
   // k-steps, goes through the pipeline (the tiles without kept pairs are last)
   (void)n_empty_p;
@@ -352,12 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           en_l = kFuse ? __ldcg(ment + eb + lane) : __ldg(ment + eb + lane);
         }
         const uint2 run_l = encode_runs4(en_l.y & 0xFFFFu);
-        for (int q = 0; q < cnt; ++q) {
-          const uint32_t ex = __shfl_sync(0xffffffffu, en_l.x, q);
-          const uint32_t rw = __shfl_sync(0xffffffffu, run_l.x, q), rn = __shfl_sync(0xffffffffu, run_l.y, q);
+        for (int q = 0; q < cnt; q += kPack) {
+          const int np = cnt - q < kPack ? cnt - q : kPack;   // k-steps in this stage
           const int64_t e = eb + q;
-          const uint32_t cols = rn >> 4;   // needed C-tile columns
-          const int32_t k0 = static_cast<int32_t>(ex) * 32;
           const long long tw0 = X3_CLK();
           mbar_wait(&empty[s], ph ^ 1);
           if (lane == 0) X3_ADD(11, X3_CLK() - tw0);
@@ -369,34 +371,58 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
 #endif
           const long long ti0 = X3_CLK();
-          if (elect_one()) {
-            srun[s] = make_uint4(rw, rn & 0xFu, 0u, (e == cur.e0 ? kFirst : 0u) | (e + 1 == cur.e1 ? kLast : 0u));
-            if (mp.stacked) {   // the column range [c0, c0 + len) covering the needed tiles
-              const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
-              mbar_arrive_expect_tx(&full[s], kStageA + kBCol * len);
-              tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
-              int off = c0;
-              if (len == 4) {
-                tma_load_4d(st + kStageA, &mp.bs[0], &full[s], 0, k0, 0, J * 4);
-              } else {
-                if (len & 2) {
-                  tma_load_4d(st + kStageA + off * kBCol, &mp.bs[1], &full[s], 0, k0, 0, J * 4 + off);
-                  off += 2;
-                }
-                if (len & 1) tma_load_4d(st + kStageA + off * kBCol, &mp.bs[2], &full[s], 0, k0, 0, J * 4 + off);
-              }
-            } else {
-              mbar_arrive_expect_tx(&full[s], kStageA + kBCol * __popc(cols));
-              tma_load_3d(st, &mp.a, &full[s], k0, I * 128, 0);
+          uint32_t rws[kPack], rns[kPack], exs[kPack];
 #pragma unroll
-              for (int lj = 0; lj < 4; ++lj)
-                if ((cols >> lj) & 1u) tma_load_3d(st + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
+          for (int j = 0; j < kPack; ++j) {   // warp-uniform: lane q + j's entry and runs
+            const int src = q + j < cnt ? q + j : q;
+            exs[j] = __shfl_sync(0xffffffffu, en_l.x, src);
+            rws[j] = __shfl_sync(0xffffffffu, run_l.x, src);
+            rns[j] = __shfl_sync(0xffffffffu, run_l.y, src);
+          }
+          if (elect_one()) {
+            // srun: x = runs of slot 0, y = runs of slot 1, z = run counts (8 bits per slot) | slots << 16
+            srun[s] = make_uint4(rws[0], kPack > 1 ? rws[kPack - 1] : 0u,
+                                 (rns[0] & 0xFu) | (kPack > 1 ? (rns[kPack - 1] & 0xFu) << 8 : 0u) |
+                                     (static_cast<uint32_t>(np) << 16),
+                                 (e == cur.e0 ? kFirst : 0u) | (e + np == cur.e1 ? kLast : 0u));
+            uint32_t bytes = 0;
+#pragma unroll
+            for (int j = 0; j < kPack; ++j) {
+              if (j >= np) break;
+              const uint32_t cols = rns[j] >> 4;   // needed C-tile columns
+              bytes += kStageA + kBCol * (mp.stacked ? (32 - __clz(cols)) - (__ffs(cols) - 1) : __popc(cols));
+            }
+            mbar_arrive_expect_tx(&full[s], bytes);
+#pragma unroll
+            for (int j = 0; j < kPack; ++j) {
+              if (j >= np) break;
+              uint8_t* sl = st + j * kSlotBytes;
+              const uint32_t cols = rns[j] >> 4;
+              const int32_t k0 = static_cast<int32_t>(exs[j]) * 32;
+              tma_load_3d(sl, &mp.a, &full[s], k0, I * 128, 0);
+              if (mp.stacked) {   // the column range [c0, c0 + len) covering the needed tiles
+                const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
+                int off = c0;
+                if (len == 4) {
+                  tma_load_4d(sl + kStageA, &mp.bs[0], &full[s], 0, k0, 0, J * 4);
+                } else {
+                  if (len & 2) {
+                    tma_load_4d(sl + kStageA + off * kBCol, &mp.bs[1], &full[s], 0, k0, 0, J * 4 + off);
+                    off += 2;
+                  }
+                  if (len & 1) tma_load_4d(sl + kStageA + off * kBCol, &mp.bs[2], &full[s], 0, k0, 0, J * 4 + off);
+                }
+              } else {
+#pragma unroll
+                for (int lj = 0; lj < 4; ++lj)
+                  if ((cols >> lj) & 1u) tma_load_3d(sl + kStageA + lj * kBCol, &mp.b, &full[s], J * 128 + lj * 32, k0, 0);
+              }
             }
           }
           __syncwarp();
           if (lane == 0) {
             X3_ADD(18, X3_CLK() - ti0);   // TMA issue (elected lane's block)
-            X3_ADD(19, X3_CLK() - tw0);   // whole producer k-step
+            X3_ADD(19, X3_CLK() - tw0);   // whole producer stage
           }
           if (++s == kStages) {
             s = 0;
@@ -450,30 +476,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elect_one()) umma_f16(dcol, zdesc, zdesc, idesc_zero, 0u, 0u, 0u, 0u, 0u);
           }
           if (!(fl & kNoStep)) {
-            const uint32_t a_addr = base_addr + st * kStageBytes, b_addr = a_addr + kStageA;
-            const uint64_t ad = smem_desc(a_addr, 16, 512, kLayoutSW64);
-            const uint64_t bd = smem_desc(b_addr, kBCol, 512, kLayoutSW64);
+            const uint32_t nsl = rs.z >> 16;
 #pragma unroll
-            for (uint32_t r = 0; r < 4; ++r) {
-              if (r >= rs.y) break;
-              const uint32_t run = (rs.x >> (8u * r)) & 0xFFu;
-              const uint32_t j = run & 3u, len = ((run >> 2) & 3u) + 1u, pat = run >> 4;
-              const uint32_t idesc = idesc_f16(kFmt, 128, 0, 0, 1) | ((len * 4u) << 17);   // N = 32 len
-              const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
-              const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
-              const uint32_t d = dcol + j * 32u;
-              const long long ti0 = X3_CLK();
-              if (elect_one()) {
+            for (int sl = 0; sl < kPack; ++sl) {
+              if (static_cast<uint32_t>(sl) >= nsl) break;
+              const uint32_t runs = sl == 0 ? rs.x : rs.y;
+              const uint32_t nrun = (rs.z >> (8 * sl)) & 0xFFu;
+              const uint32_t a_addr = base_addr + st * kStageBytes + sl * kSlotBytes, b_addr = a_addr + kStageA;
+              const uint64_t ad = smem_desc(a_addr, 16, 512, kLayoutSW64);
+              const uint64_t bd = smem_desc(b_addr, kBCol, 512, kLayoutSW64);
 #pragma unroll
-                for (int p = 0; p < kProd; ++p) {
-                  const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
-                  const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
-                  umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
-                  umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
+              for (uint32_t r = 0; r < 4; ++r) {
+                if (r >= nrun) break;
+                const uint32_t run = (runs >> (8u * r)) & 0xFFu;
+                const uint32_t j = run & 3u, len = ((run >> 2) & 3u) + 1u, pat = run >> 4;
+                const uint32_t idesc = idesc_f16(kFmt, 128, 0, 0, 1) | ((len * 4u) << 17);   // N = 32 len
+                const uint32_t m0 = (pat & 1u) - 1u, m1 = ((pat >> 1) & 1u) - 1u;
+                const uint32_t m2 = ((pat >> 2) & 1u) - 1u, m3 = ((pat >> 3) & 1u) - 1u;
+                const uint32_t d = dcol + j * 32u;
+                const long long ti0 = X3_CLK();
+                if (elect_one()) {
+#pragma unroll
+                  for (int p = 0; p < kProd; ++p) {
+                    const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
+                    const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
+                    umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
+                    umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
+                  }
                 }
+                __syncwarp();
+                if (lane == 0) X3_ADD(14, X3_CLK() - ti0);
               }
-              __syncwarp();
-              if (lane == 0) X3_ADD(14, X3_CLK() - ti0);
             }
           }
           const long long tc0 = X3_CLK();
