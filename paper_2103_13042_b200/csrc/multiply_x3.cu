@@ -64,6 +64,11 @@ template <int P>
 constexpr uint32_t kChunkOf = P == 3 ? 4u : 0x40000000u;
 constexpr uint32_t kTmemCols = 256;                // 2 buffers x 128 columns
 constexpr uint32_t kFirst = 1u << 29, kLast = 1u << 30, kNoStep = 1u << 28, kEnd = 1u << 27;
+// P = 1 stage of two consecutive k-steps (k, k+1) loaded as 64-deep boxes: A [128 x 64] SWIZZLE_128B
+// (16 KB), then B boxes [64 k x 32 n] SWIZZLE_64B of 4 KB per column tile -- half the TMA
+// instructions of two 32-deep slots (the producer's ~160 cycles per TMA bound the small-problem
+// stage rate), the layout of multiply_dual.cu's wide stages
+constexpr uint32_t kWide = 1u << 26;
 
 // Runs of a 4 x 4 keep mask (bit 4 li + lj: C-tile row li, column lj): maximal groups of adjacent
 // kept columns with equal row patterns, one MMA group each (N = 32 len, disable-output-lane masks
@@ -110,6 +115,10 @@ struct X3Maps {
   int stacked;
   CUtensorMap c;      // P = 1, plain epilogue: C (FP32) boxes [128 rows x 32], SWIZZLE_128B, for TMA stores
   int tstore;
+  // P = 1 wide stages: A boxes {64 k, 128 rows, 1} SW128; B {32 n, 64 k, 1} per column tile and,
+  // when stacked, {32, 64, 1, 4/2/1 column tiles}
+  CUtensorMap a2, b2, bs2[3];
+  int wide;
 };
 
 struct XChain {       // chained outputs (P = 1): tile norms of the stored C, a rounded copy, C_low only
@@ -285,6 +294,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&mp.b);
       if (mp.stacked)
         for (int q = 0; q < 3; ++q) tma_prefetch_desc(&mp.bs[q]);
+      if (mp.wide) {
+        tma_prefetch_desc(&mp.a2);
+        tma_prefetch_desc(&mp.b2);
+        if (mp.stacked)
+          for (int q = 0; q < 3; ++q) tma_prefetch_desc(&mp.bs2[q]);
+      }
     }
     int s = 0, tq_s = 0;
     uint32_t ph = 0, tq_ph = 0;
@@ -379,12 +394,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             rws[j] = __shfl_sync(0xffffffffu, run_l.x, src);
             rns[j] = __shfl_sync(0xffffffffu, run_l.y, src);
           }
+          const bool wide = kPack == 2 && mp.wide && np == 2 && exs[kPack - 1] == exs[0] + 1u;
           if (elect_one()) {
             // srun: x = runs of slot 0, y = runs of slot 1, z = run counts (8 bits per slot) | slots << 16
             srun[s] = make_uint4(rws[0], kPack > 1 ? rws[kPack - 1] : 0u,
                                  (rns[0] & 0xFu) | (kPack > 1 ? (rns[kPack - 1] & 0xFu) << 8 : 0u) |
                                      (static_cast<uint32_t>(np) << 16),
-                                 (e == cur.e0 ? kFirst : 0u) | (e + np == cur.e1 ? kLast : 0u));
+                                 (e == cur.e0 ? kFirst : 0u) | (e + np == cur.e1 ? kLast : 0u) | (wide ? kWide : 0u));
+          }
+          if (wide) {   // one A box and the union column range of B for both k-steps
+            if (elect_one()) {
+              const uint32_t cols = (rns[0] | rns[kPack - 1]) >> 4;
+              const int c0 = __ffs(cols) - 1, len = (32 - __clz(cols)) - c0;
+              const int32_t k0 = static_cast<int32_t>(exs[0]) * 32;
+              mbar_arrive_expect_tx(&full[s], 2 * kStageA + 2 * kBCol * (mp.stacked ? len : __popc(cols)));
+              tma_load_3d(st, &mp.a2, &full[s], k0, I * 128, 0);
+              uint8_t* sb = st + 2 * kStageA;
+              if (mp.stacked) {
+                int off = c0;
+                if (len == 4) {
+                  tma_load_4d(sb, &mp.bs2[0], &full[s], 0, k0, 0, J * 4);
+                } else {
+                  if (len & 2) {
+                    tma_load_4d(sb + off * 2 * kBCol, &mp.bs2[1], &full[s], 0, k0, 0, J * 4 + off);
+                    off += 2;
+                  }
+                  if (len & 1) tma_load_4d(sb + off * 2 * kBCol, &mp.bs2[2], &full[s], 0, k0, 0, J * 4 + off);
+                }
+              } else {
+#pragma unroll
+                for (int lj = 0; lj < 4; ++lj)
+                  if ((cols >> lj) & 1u) tma_load_3d(sb + lj * 2 * kBCol, &mp.b2, &full[s], J * 128 + lj * 32, k0, 0);
+              }
+            }
+          } else if (elect_one()) {
             uint32_t bytes = 0;
 #pragma unroll
             for (int j = 0; j < kPack; ++j) {
@@ -482,9 +525,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (static_cast<uint32_t>(sl) >= nsl) break;
               const uint32_t runs = sl == 0 ? rs.x : rs.y;
               const uint32_t nrun = (rs.z >> (8 * sl)) & 0xFFu;
-              const uint32_t a_addr = base_addr + st * kStageBytes + sl * kSlotBytes, b_addr = a_addr + kStageA;
-              const uint64_t ad = smem_desc(a_addr, 16, 512, kLayoutSW64);
-              const uint64_t bd = smem_desc(b_addr, kBCol, 512, kLayoutSW64);
+              // 32-deep slot: A K-major SW64 rows of 32 (SBO 512), B MN-major SW64 boxes of 32 n x 32 k
+              // (LBO = kBCol); wide stage: A SW128 rows of 64 (SBO 1024), k-step sl at +64 B; B boxes of
+              // 32 n x 64 k (LBO = 2 kBCol) after both A halves, k-step sl at +2 KB (32 k-rows)
+              const bool wst = (fl & kWide) != 0u;
+              const uint32_t st_addr = base_addr + st * kStageBytes;
+              const uint64_t ad = wst ? smem_desc(st_addr, 16, 1024, kLayoutSW128) + 4u * sl
+                                      : smem_desc(st_addr + sl * kSlotBytes, 16, 512, kLayoutSW64);
+              const uint64_t bd = wst ? smem_desc(st_addr + 2 * kStageA, 2 * kBCol, 512, kLayoutSW64) + 128u * sl
+                                      : smem_desc(st_addr + sl * kSlotBytes + kStageA, kBCol, 512, kLayoutSW64);
+              const uint32_t bcol = wst ? (2 * kBCol) >> 4 : kBCol >> 4;   // descriptor units per column tile
 #pragma unroll
               for (uint32_t r = 0; r < 4; ++r) {
                 if (r >= nrun) break;
@@ -499,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                   for (int p = 0; p < kProd; ++p) {
                     const uint64_t a = ad + ((pa[p] * kAPlane) >> 4);
-                    const uint64_t b = bd + ((j * kBCol + pb[p] * kBBox) >> 4);
+                    const uint64_t b = bd + j * bcol + ((pb[p] * kBBox) >> 4);
                     umma_f16(d, a, b, idesc, 1u, m0, m1, m2, m3);
                     umma_f16(d, a + 2, b + 64, idesc, 1u, m0, m1, m2, m3);
                   }
@@ -805,6 +855,21 @@ spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void*
   SPAMM_TRY(encode_tmap_3d(&mp.b, dt, B, p.N, p.K, 1, static_cast<uint64_t>(ldb) * 2,
                            static_cast<uint64_t>(p.K * ldb) * 2, 32, 32, 1, CU_TENSOR_MAP_SWIZZLE_64B));
   SPAMM_TRY(encode_stacked(mp, dt, B, p.N, p.K, ldb, 1));
+  // wide stages (two consecutive k-steps): A {64, 128} SW128, B {32, 64} per column tile / stacked
+  mp.wide = 1;
+  SPAMM_TRY(encode_tmap_3d(&mp.a2, dt, A, p.K, p.M, 1, static_cast<uint64_t>(lda) * 2,
+                           static_cast<uint64_t>(p.M * lda) * 2, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B));
+  SPAMM_TRY(encode_tmap_3d(&mp.b2, dt, B, p.N, p.K, 1, static_cast<uint64_t>(ldb) * 2,
+                           static_cast<uint64_t>(p.K * ldb) * 2, 32, 64, 1, CU_TENSOR_MAP_SWIZZLE_64B));
+  if (mp.stacked) {
+    const uint64_t dims[4] = {32, static_cast<uint64_t>(p.K), 1, static_cast<uint64_t>(p.N / 32)};
+    const uint64_t st[3] = {static_cast<uint64_t>(ldb) * 2, static_cast<uint64_t>(p.K * ldb) * 2, 64};
+    const uint32_t nb[3] = {4, 2, 1};
+    for (int q = 0; q < 3; ++q) {
+      const uint32_t box[4] = {32, 64, 1, nb[q]};
+      SPAMM_TRY(encode_tmap_4d(&mp.bs2[q], dt, B, dims, st, box, CU_TENSOR_MAP_SWIZZLE_64B));
+    }
+  }
   const bool gen = p.alpha != 1.0 || p.beta != 0.0 || p.out_norms || p.out_low != nullptr;
   mp.tstore = !gen && C != nullptr;
   if (mp.tstore)
