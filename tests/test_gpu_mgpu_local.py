@@ -113,3 +113,26 @@ def test_p4_repeated_steps_and_single_rank(sp):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(C.cpu().numpy(), C1)
     assert sp.spamm_get_partition(plan.handle, 1) == [0, M // T]
+
+
+def test_nccl_communicator_single_rank(sp):
+    """The NCCL plumbing of spamm_multiply_mgpu on real hardware as far as one GPU allows: a
+    communicator from spamm_nccl_unique_id / spamm_nccl_comm_init (NCCL's own bootstrap, one rank),
+    handed to spamm_multiply_mgpu (Alg. 4) with GATHER_C, equals spamm_run; the
+    collectives themselves need nranks > 1, i.e. more than the one GPU of this box (their phases are
+    verified above through spamm_multiply_mgpu_local)."""
+    M = N = K = 1024
+    prec = "bf16"
+    A = _rounded(synth.perturbed_decay_matrix(K, 0.99, seed=161, m=M), prec)
+    Ad = _dev(A, prec)
+    _, C1 = _single(sp, Ad, Ad, 1e-4, prec, M, N, K)
+    comm = sp.spamm_nccl_comm_init(1, 0, sp.spamm_nccl_unique_id())
+    try:
+        plan = sp.Plan(M, N, K, 1e-4, prec)
+        C = torch.zeros((M, N), device="cuda")
+        for _ in range(2):
+            sp.spamm_multiply_mgpu(plan.handle, comm, 0, 1, Ad, Ad, C, sp.SPAMM_MGPU_GATHER_C)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(C.cpu().numpy(), C1)
+    finally:
+        sp.spamm_nccl_comm_destroy(comm)
