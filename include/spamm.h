@@ -77,7 +77,7 @@ typedef enum {
                                          up to FP32 rounding order. */
 #define SPAMM_FLAG_STAGED         4u  /* never fuse the skip map into the multiply.  Without it, spamm_run /
                                          SPAMM_MUL_AUTO on a plan with 128 x 128 macro-tiles (BF16/FP16 of
-                                         the small-problem rule above, or SPAMM_FP32X3) of at most one per
+                                         the small-problem rule above, SPAMM_FP32, SPAMM_FP32X3) of at most one per
                                          SM skip the stage-2 launch: each multiply CTA decides its own
                                          macro-tile's list with the same predicate and writes the same
                                          skip map (getters unchanged), then multiplies it.  Results are

@@ -248,7 +248,7 @@ spamm_status spamm_plan_ex(spamm_plan_t* out, int64_t M, int64_t N, int64_t K, i
   p->NC = (BK + kChunk - 1) / kChunk;
   // small problems: one 128 x 128 macro-tile per SM at most -> the skip map is decided inside the
   // multiply (one launch fewer on spamm_run; the per-tile list work is BK/32 warp steps)
-  p->fused = !(flags & SPAMM_FLAG_STAGED) && (p->x1 || prec == SPAMM_FP32X3) && p->GM * p->GN <= p->num_sms;
+  p->fused = !(flags & SPAMM_FLAG_STAGED) && (p->x1 || f32_inputs(prec)) && p->GM * p->GN <= p->num_sms;
   p->device = dev;
   p->row_begin_macro = 0;
   p->row_end_macro = p->GM;
@@ -416,7 +416,7 @@ spamm_status do_multiply(Plan& p, const void* A, int64_t lda, const void* B, int
     SPAMM_TRY(launch_multiply_x3(p, C, ldc, fuse, s));
   } else if (p.prec == SPAMM_FP32) {
     SPAMM_TRY(launch_multiply_simt(p, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc,
-                                   s));
+                                   fuse, s));
   } else if (p.x1) {
     SPAMM_TRY(launch_multiply_x1(p, A, lda, B, ldb, C, ldc, fuse, s));
   } else {

@@ -93,7 +93,8 @@ struct Plan {
   void* im2col = nullptr;         // spamm_conv2d_im2col: the K x N im2col matrix (allocated on first use)
   bool b_is_a = false;            // the last spamm_norms saw B == A (planes of A serve both)
   bool x1 = false;                // BF16/FP16 on 128 x 128 macro-tiles (fewer 256 x 256 tiles than SMs)
-  // spamm_run / AUTO on a small problem (128 x 128 macro-tiles, at most one per SM): no skip-map
+  // spamm_run / AUTO on a small problem (128 x 128 macro-tiles -- FP32, FP32X3, small BF16/FP16 -- at
+  // most one per SM): no skip-map
   // launch, the multiply's producer warps decide their tiles' lists (multiply_x3.cu XFuse)
   bool fused = false;
   bool leaf_alloc = false;
@@ -199,7 +200,7 @@ spamm_status launch_skipmap(Plan& p, int64_t gi0, int64_t gi1, bool on_device, b
 spamm_status launch_partition(Plan& p, int rank, int nranks, cudaStream_t s);
 spamm_status launch_leaf_expand(Plan& p, cudaStream_t s);   // per-C-tile lists from macro lists
 spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
-                                  int64_t ldc, cudaStream_t s);
+                                  int64_t ldc, bool fuse, cudaStream_t s);
 spamm_status launch_multiply_dual(Plan& p, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                                   int64_t ldc, cudaStream_t s);
 // SPAMM_FP32X3; fuse = the multiply decides the skip map itself (Plan::fused, spamm_run)

@@ -14,6 +14,7 @@
 // is added into a running sum, also in registers, which keeps
 // N=65536 within 1e-5.
 #include "internal.h"
+#include "skipdecide.cuh"
 #include "sm100.cuh"
 
 namespace spamm {
@@ -33,7 +34,7 @@ constexpr int kThreads = (4 + kComputeWarps) * 32;
 constexpr int kAFloats = 128 * 32;
 constexpr int kBFloats = 32 * 128;
 constexpr int kStageBytes = (kAFloats + kBFloats) * 4;
-constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 256;
+constexpr size_t kSmemBytes = 1024 + static_cast<size_t>(kStages) * kStageBytes + 512;
 
 __device__ __forceinline__ int64_t snake(int64_t r, int G, int b) { return r * G + ((r & 1) ? (G - 1 - b) : b); }
 
@@ -41,12 +42,18 @@ __device__ __forceinline__ float comp(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 
+// kFuse (small problems, spamm_run): the producer warp decides each tile's skip list itself
+// (skipdecide.cuh fuse_tile_list: the skip kernel's predicate and list format, plus U, L, row work,
+// totals and the identity order for the getters) and hands (tile, k-steps) to the compute warps
+// through a 2-slot shared-memory queue; the compute warps read the just-written masks coherently.
+template <bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     spamm_mul_simt_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                           float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
-                          const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint2* __restrict__ ment,
+                          const int64_t* __restrict__ mstart, const int64_t* __restrict__ mcount, const uint2* ment,
                           const int32_t* __restrict__ order, int64_t n_tiles, const int64_t* __restrict__ rng,
-                          int64_t GN, const Axpby ab, double* __restrict__ nC, int64_t ldn, int64_t BM, int64_t BN) {
+                          int64_t GN, const Axpby ab, double* __restrict__ nC, int64_t ldn, int64_t BM, int64_t BN,
+                          const XFuse fz) {
   if (rng != nullptr) n_tiles = (rng[1] - rng[0]) * GN;   // multi-GPU range decided on the device
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned base derived from smem_raw by an offset (not an integer round trip), so the compiler
@@ -56,12 +63,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sB = sA + kStages * kAFloats;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(kStages) * kStageBytes);
   uint64_t* empty = full + kStages;
+  uint64_t* tl_full = empty + kStages;    // kFuse: 2-slot tile queue (tile, k-step count)
+  uint64_t* tl_empty = tl_full + 2;
+  int64_t* tl_info = reinterpret_cast<int64_t*>(tl_empty + 2);   // [2][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kComputeWarps);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&tl_full[q], 1);
+      mbar_init(&tl_empty[q], kComputeWarps);
     }
     fence_mbar_init();
   }
@@ -71,6 +85,48 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     // ------------------------------------------------------ TMA producer (warpgroup 0)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    if constexpr (kFuse) {
+      if (warp == 0) {   // the whole warp decides the lists; lane 0 issues the loads
+        if (lane == 0) {
+          tma_prefetch_desc(&tA);
+          tma_prefetch_desc(&tB);
+        }
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t r = 0;; ++r) {
+          const int64_t t = snake(r, G, b);   // static assignment, identity order
+          const int slot = static_cast<int>(r & 1);
+          const uint32_t tph = static_cast<uint32_t>((r >> 1) & 1);
+          uint2 reg = make_uint2(0u, 0u);
+          uint32_t any = 0u;
+          const int64_t u = t < n_tiles ? fuse_tile_list(fz, t, GN, lane, &reg, &any) : 0;
+          if (lane == 0) {   // publish (tile, k-steps), or the end marker
+            mbar_wait(&tl_empty[slot], tph ^ 1);
+            tl_info[2 * slot] = t < n_tiles ? t : -1;
+            tl_info[2 * slot + 1] = u;
+            mbar_arrive(&tl_full[slot]);   // release: the list written above is visible to the CTA
+          }
+          if (t >= n_tiles) break;
+          const int32_t I = static_cast<int32_t>(t / GN), J = static_cast<int32_t>(t % GN);
+          for (int64_t q = 0; q < u; ++q) {
+            uint32_t kx;
+            if (fz.BK <= 32) kx = __shfl_sync(0xffffffffu, reg.x, static_cast<int>(__fns(any, 0u, static_cast<int>(q) + 1)));
+            else kx = __ldcg(ment + t * fz.BK + q).x;
+            if (lane == 0) {
+              mbar_wait(&empty[s], ph ^ 1);
+              mbar_arrive_expect_tx(&full[s], kStageBytes);
+              tma_load_2d(sA + s * kAFloats, &tA, &full[s], static_cast<int32_t>(kx) * 32, I * 128);
+              tma_load_2d(sB + s * kBFloats, &tB, &full[s], J * 128, static_cast<int32_t>(kx) * 32);
+            }
+            if (++s == kStages) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+      return;
+    }
     if (warp == 0 && lane == 0) {
       tma_prefetch_desc(&tA);
       tma_prefetch_desc(&tB);
@@ -116,9 +172,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   int s = 0;
   uint32_t ph = 0;
   for (int64_t r = 0;; ++r) {
-    const int64_t idx = snake(r, G, b);
-    if (idx >= n_tiles) break;
-    const int64_t t = order[idx];
+    int64_t t, e0, e1;
+    if constexpr (kFuse) {
+      const int slot = static_cast<int>(r & 1);
+      mbar_wait(&tl_full[slot], static_cast<uint32_t>((r >> 1) & 1));
+      t = tl_info[2 * slot];
+      e0 = t * fz.BK;
+      e1 = e0 + tl_info[2 * slot + 1];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tl_empty[slot]);
+      if (t < 0) break;
+    } else {
+      const int64_t idx = snake(r, G, b);
+      if (idx >= n_tiles) break;
+      t = order[idx];
+      e0 = mstart[t];
+      e1 = e0 + mcount[t];
+    }
     const int64_t I = t / GN, J = t % GN;
     float run[8][8];
 #pragma unroll
@@ -126,10 +196,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < 8; ++j) run[i][j] = 0.f;
     bool first_a = true, first_b = true;
-    const int64_t e0 = mstart[t], e1 = e0 + mcount[t];
     for (int64_t e = e0; e < e1; ++e) {
       mbar_wait(&full[s], ph);
-      const uint32_t mask = __ldg(&ment[e].y);   // the k-step's keep bits (read-only, L1-resident)
+      // the k-step's keep bits (kFuse: written by this CTA's producer warp, read coherently)
+      const uint32_t mask = kFuse ? __ldcg(&ment[e].y) : __ldg(&ment[e].y);
       const bool ka = (mask >> bit_a) & 1u, kb = (mask >> bit_b) & 1u;
       if (ka || kb) {
         const float* a_base = sA + s * kAFloats + (li * 32 + g) * 32;
@@ -228,26 +298,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 spamm_status launch_multiply_simt(Plan& p, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
-                                  int64_t ldc, cudaStream_t s) {
+                                  int64_t ldc, bool fuse, cudaStream_t s) {
   CUtensorMap tA, tB;
   SPAMM_TRY(encode_tmap_2d(&tA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, A, p.K, p.M, lda, 32, 128,
                            CU_TENSOR_MAP_SWIZZLE_128B));
   SPAMM_TRY(encode_tmap_2d(&tB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, p.N, p.K, ldb, 128, 32,
                            CU_TENSOR_MAP_SWIZZLE_NONE));
-  SPAMM_SET_SMEM(spamm_mul_simt_kernel, static_cast<int>(kSmemBytes), p.device);
+  auto kern = fuse ? spamm_mul_simt_kernel<true> : spamm_mul_simt_kernel<false>;
+  SPAMM_SET_SMEM(spamm_mul_simt_kernel<true>, static_cast<int>(kSmemBytes), p.device);
+  SPAMM_SET_SMEM(spamm_mul_simt_kernel<false>, static_cast<int>(kSmemBytes), p.device);
   const int64_t n_tiles = p.range_on_device ? 0 : static_cast<int64_t>(p.row_end_macro - p.row_begin_macro) * p.GN;
   if (!p.range_on_device && n_tiles <= 0) return SPAMM_OK;
   const int grid = static_cast<int>(!p.range_on_device && n_tiles < p.num_sms ? n_tiles : p.num_sms);
-  spamm_mul_simt_kernel<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.mstart, p.U,
-                                                           static_cast<const uint2*>(p.macro_ent), p.order, n_tiles,
-                                                           p.range_on_device ? p.d_range : nullptr, p.GN,
-                                                           Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
-                                                           p.out_norms ? p.nC : nullptr, p.BN, p.BM, p.BN);
+  kern<<<grid, kThreads, kSmemBytes, s>>>(tA, tB, C, ldc, p.M, p.N, p.mstart, p.U, static_cast<const uint2*>(p.macro_ent),
+                                          p.order, n_tiles, p.range_on_device ? p.d_range : nullptr, p.GN,
+                                          Axpby{static_cast<float>(p.alpha), static_cast<float>(p.beta)},
+                                          p.out_norms ? p.nC : nullptr, p.BN, p.BM, p.BN,
+                                          XFuse{p.nA, p.nBt, p.BM, p.BK, p.BN, p.tau, p.U, p.L,
+                                                static_cast<uint2*>(p.macro_ent), p.order,
+                                                reinterpret_cast<unsigned long long*>(p.row_work),
+                                                reinterpret_cast<unsigned long long*>(p.totals)});
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, spamm_mul_simt_kernel);
+    cudaFuncGetAttributes(&fa, spamm_mul_simt_kernel<false>);
     return fail(SPAMM_E_CUDA, std::string("spamm_mul_simt_kernel launch: ") + cudaGetErrorString(e) +
                                   " (regs " + std::to_string(fa.numRegs) + ", maxThreads " +
                                   std::to_string(fa.maxThreadsPerBlock) + ", static smem " +

@@ -1,5 +1,6 @@
 """GPU: the fused small-problem path (spamm_run on plans of at most one 128 x 128 macro-tile per
-SM: the multiply's producer warps decide their own tiles' skip lists, no skip-map launch) against
+SM -- BF16/FP16 small problems, FP32X3 and FP32: the multiply's producer warps decide their own
+tiles' skip lists, no skip-map launch) against
 the staged path (SPAMM_FLAG_STAGED: norm -> skip-map -> multiply kernels) on the same inputs.
 
 Both take every decision with the same float64 predicate keep <=> !(nA*nB < tau) (PAPER.md:47,
@@ -70,12 +71,12 @@ def _compare(sp, fused, staged, A_d, B_d, M, N):
     return Cf, sf
 
 
-@pytest.mark.parametrize("prec", ["bf16", "fp16", "fp32x3"])
+@pytest.mark.parametrize("prec", ["bf16", "fp16", "fp32x3", "fp32"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("q", [0.0, 0.5, 0.9, 1.0])
 def test_fused_equals_staged(sp, prec, shape, q):
     M, N, K = shape
-    if prec == "fp32x3" and shape == (256, 6400, 1152) and q in (0.5, 0.9):
+    if prec in ("fp32x3", "fp32") and shape == (256, 6400, 1152) and q in (0.5, 0.9):
         pytest.skip("covered by q = 0 / 1 (oracle on the large shape is slow)")
     A, B = _inputs(shape, prec, 31)
     nA, nB = oracle.tile_norms(A, T), oracle.tile_norms(B, T)
@@ -95,7 +96,7 @@ def test_fused_equals_staged(sp, prec, shape, q):
 
 
 @pytest.mark.parametrize("lam", [0.9, 0.99])
-@pytest.mark.parametrize("prec", ["bf16", "fp32x3"])
+@pytest.mark.parametrize("prec", ["bf16", "fp32x3", "fp32"])
 def test_fused_configs0(sp, lam, prec):
     """configs[0]: N = 1024 exponential decay, tau = 1e-4 (Table 1's N)."""
     N = 1024
