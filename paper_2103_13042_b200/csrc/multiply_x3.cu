@@ -46,13 +46,18 @@ struct XCfg {
   // P = 1: a stage carries up to two k-steps (two 16 KB slots): the per-stage round trip (full /
   // empty barriers, descriptor, commit) was ~700 cycles for 132 cycles of MMA per k-step
   static constexpr int kPack = P == 3 ? 1 : 2;
-  static constexpr int kStages = P == 3 ? 4 : 4;
+#ifndef SPAMM_X1_STAGES
+#define SPAMM_X1_STAGES 4
+#endif
+  // P = 1: SPAMM_X1_STAGES stages of two k-steps; 6 leaves no room for the 64 KB C staging (the
+  // epilogue then stores from registers)
+  static constexpr int kStages = P == 3 ? 4 : SPAMM_X1_STAGES;
   static constexpr int kBCol = P * kBBox;                     // one 32-column tile, P planes
   static constexpr int kStageA = P * kAPlane;
   static constexpr int kSlotBytes = kStageA + 4 * kBCol;      // one k-step: 48 KB (P = 3) / 16 KB (P = 1)
   static constexpr int kStageBytes = kPack * kSlotBytes;
   // P = 1: a 64 KB staging tile for the TMA-store epilogue (4 boxes of [128 rows x 32] FP32, SWIZZLE_128B)
-  static constexpr int kStageC = P == 1 ? 65536 : 0;
+  static constexpr int kStageC = (P == 1 && kStages <= 4) ? 65536 : 0;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 2048 + kStageC;
 };
 constexpr int kThreads = 384;
@@ -796,7 +801,7 @@ spamm_status launch_multiply_x1(Plan& p, const void* A, int64_t lda, const void*
     }
   }
   const bool gen = p.alpha != 1.0 || p.beta != 0.0 || p.out_norms || p.out_low != nullptr;
-  mp.tstore = !gen && C != nullptr;
+  mp.tstore = !gen && C != nullptr && XCfg<1>::kStageC > 0;
   if (mp.tstore)
     SPAMM_TRY(encode_tmap_2d(&mp.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, p.N, p.M, ldc, 32, 128,
                              CU_TENSOR_MAP_SWIZZLE_128B));
