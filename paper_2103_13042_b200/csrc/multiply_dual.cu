@@ -170,7 +170,36 @@ __global__ void __launch_bounds__(kDThreads, 1)
   // Interleaved with the accumulator waits only when the empty tiles dominate (measured, ms of the
   // multiply, zero-fill last -> interleaved: N = 16384 lambda 0.99 tau 1e-6 0.343 -> 0.318 (3.5 empty
   // tiles per working tile), N = 8192 0.135 -> 0.141 (1.2), N = 65536 58.8 -> 59.0; scripts/gpu_r02zi.sh)
-  const bool zf_inter = SPAMM_ZF_INTERLEAVE && n_empty >= 2 * n_work;
+#ifndef SPAMM_ZF_RATIO
+#define SPAMM_ZF_RATIO 2
+#endif
+#ifndef SPAMM_ZF_LSU
+#define SPAMM_ZF_LSU 0
+#endif
+  const bool zf_inter = SPAMM_ZF_INTERLEAVE && n_empty >= SPAMM_ZF_RATIO * n_work;
+  // interleaved units with 16-byte LSU stores instead of the bulk-copy engine (experiment
+  // SPAMM_ZF_LSU=1, scripts/gpu_r02zr.sh: multiply at N = 16384 0.321 -> 0.338 ms, N = 8192 0.135 ->
+  // 0.142 ms when always interleaved -- slower than the bulk stores, not used)
+  auto zero_unit_lsu = [&]() -> bool {
+    unsigned int u32 = 0;
+    if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
+    const int64_t u = __shfl_sync(0xffffffffu, u32, 0);
+    if (u >= n_units) return false;
+    const int64_t t = order[n_work + u / 8];
+    const int64_t r0 = (t / GN) * 256 + (u % 8) * 32, c0 = (t % GN) * 256;
+    const int64_t ncol = N - c0 < 256 ? N - c0 : 256;
+    for (int r = 0; r < 32; ++r) {
+      const int64_t row = r0 + r;
+      if (row >= M) break;
+      float* crow = C + row * ldc + c0;
+      for (int64_t cc = 4 * lane; cc < ncol; cc += 128) {
+        if (cc + 4 <= ncol) st_zero16_hint(crow + cc, zf_pol);
+        else
+          for (int64_t x = cc; x < ncol; ++x) crow[x] = 0.f;
+      }
+    }
+    return true;
+  };
   auto zero_unit = [&]() -> bool {
     unsigned int u32 = 0;
     if (lane == 0) u32 = atomicAdd(sched + 1, 1u);
@@ -568,7 +597,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
         // kept pairs (evict-first bulk stores); the phase is monotone, so any lane seeing it
         // complete means complete for the warp (zero_unit is warp-collective)
         while (!__any_sync(0xffffffffu, mbar_try_wait(&tfull[h], par))) {
-          if (!zero_unit()) break;
+          if (!(SPAMM_ZF_LSU ? zero_unit_lsu() : zero_unit())) break;
         }
       }
       mbar_wait(&tfull[h], par);

@@ -109,6 +109,13 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// 16-byte zero store through the LSU with an L2 cache policy (not the TMA / bulk-copy engine)
+__device__ __forceinline__ void st_zero16_hint(void* gdst, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(
+                   reinterpret_cast<uint64_t>(gdst)),
+               "r"(0u), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_group() {
